@@ -1,0 +1,786 @@
+"""TEST INFRASTRUCTURE ONLY: numpy restatement of the reference hot path.
+
+Every numerical expression keeps the reference's IEEE evaluation order
+(numpy evaluates left to right, never contracts a*b+c, and its +,-,*,/,sqrt
+are correctly rounded), so for identical inputs this module reproduces the
+reference's fields bit for bit.  Citations are into /root/reference/pkg/src/
+blockflow/.  Geometry (metrics) and manufactured-solution values are setup
+inputs injected by the caller; this module restates only the per-step path.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from paper_2012_02925_b200.errors import ConfigError, NonPhysicalStateError
+
+RK_ALPHAS = {1: (1.0,), 2: (0.5, 1.0), 4: (0.25, 1.0 / 3.0, 0.5, 1.0)}   # solver.py:33
+PRIMS = ("rho", "u", "v", "w", "p")
+ALL_FIELDS = ("rho", "u", "v", "w", "p", "T")
+FACE_NAMES = ("i_min", "i_max", "j_min", "j_max", "k_min", "k_max")
+
+
+# ---------------------------------------------------------------------------
+# Point physics (physics.py:136-297)
+# ---------------------------------------------------------------------------
+
+def encode(rho, u, v, w, p, gamma):
+    """Primitive -> conserved (physics.py:136-140)."""
+    kinetic = 0.5 * ((u * u + v * v) + w * w)
+    return rho, rho * u, rho * v, rho * w, (p / (gamma - 1.0) + rho * kinetic)
+
+
+def decode(q0, q1, q2, q3, q4, gamma):
+    """Conserved -> primitive, no flooring (physics.py:143-149)."""
+    u, v, w = q1 / q0, q2 / q0, q3 / q0
+    p = (gamma - 1.0) * (q4 - 0.5 * ((q1 * u + q2 * v) + q3 * w))
+    return q0, u, v, w, p
+
+
+def euler_flux(rho, u, v, w, p, nx, ny, nz, gamma):
+    """Analytic normal flux (physics.py:169-175)."""
+    vn = (u * nx + v * ny) + w * nz
+    kinetic = 0.5 * ((u * u + v * v) + w * w)
+    enthalpy = ((gamma / (gamma - 1.0)) * p) / rho + kinetic
+    mdot = rho * vn
+    return (mdot, mdot * u + nx * p, mdot * v + ny * p, mdot * w + nz * p, mdot * enthalpy)
+
+
+def _entropy_fixed_abs(lam, delta):
+    """Harten smoothing of |lam| (physics.py:183-187)."""
+    mag = np.abs(lam)
+    denom = np.where(delta > 0.0, delta, 1.0)
+    return np.where(mag < delta, (lam * lam + delta * delta) / (2.0 * denom), mag)
+
+
+def roe(left, right, nx, ny, nz, gamma, efix):
+    """Roe FDS flux density (physics.py:190-255)."""
+    rl, ul, vl, wl, pl = left
+    rr, ur, vr, wr, pr = right
+    fl = euler_flux(rl, ul, vl, wl, pl, nx, ny, nz, gamma)
+    fr = euler_flux(rr, ur, vr, wr, pr, nx, ny, nz, gamma)
+    c = gamma / (gamma - 1.0)
+    hl = (c * pl) / rl + 0.5 * ((ul * ul + vl * vl) + wl * wl)
+    hr = (c * pr) / rr + 0.5 * ((ur * ur + vr * vr) + wr * wr)
+    ratio = np.sqrt(rr / rl)
+    weight = 1.0 / (1.0 + ratio)
+    rho = ratio * rl
+    u = (ul + ratio * ur) * weight
+    v = (vl + ratio * vr) * weight
+    w = (wl + ratio * wr) * weight
+    h = (hl + ratio * hr) * weight
+    a2 = (gamma - 1.0) * (h - 0.5 * ((u * u + v * v) + w * w))
+    if np.any(a2 <= 0.0):
+        where = np.argwhere(np.atleast_1d(a2) <= 0.0)
+        raise NonPhysicalStateError(
+            f"Roe-averaged state has non-positive sound speed at index {where[0]}")
+    a = np.sqrt(a2)
+    vn = (u * nx + v * ny) + w * nz
+    jr, jp = rr - rl, pr - pl
+    ju, jv, jw = ur - ul, vr - vl, wr - wl
+    jvn = (ju * nx + jv * ny) + jw * nz
+    delta = efix * (np.abs(vn) + a)
+    l1 = _entropy_fixed_abs(vn - a, delta)
+    l2 = _entropy_fixed_abs(vn, delta)
+    l5 = _entropy_fixed_abs(vn + a, delta)
+    al1 = (jp - (rho * a) * jvn) / (2.0 * a2)
+    al2 = jr - jp / a2
+    al5 = (jp + (rho * a) * jvn) / (2.0 * a2)
+    su, sv, sw = ju - jvn * nx, jv - jvn * ny, jw - jvn * nz
+    kinetic = 0.5 * ((u * u + v * v) + w * w)
+    w1, w5 = l1 * al1, l5 * al5
+    diss = (
+        (w1 + l2 * al2) + w5,
+        (w1 * (u - a * nx) + l2 * (al2 * u + rho * su)) + w5 * (u + a * nx),
+        (w1 * (v - a * ny) + l2 * (al2 * v + rho * sv)) + w5 * (v + a * ny),
+        (w1 * (w - a * nz) + l2 * (al2 * w + rho * sw)) + w5 * (w + a * nz),
+        (w1 * (h - a * vn) + l2 * (al2 * kinetic + rho * ((u * su + v * sv) + w * sw)))
+        + w5 * (h + a * vn),
+    )
+    return tuple(0.5 * (x + y) - 0.5 * d for x, y, d in zip(fl, fr, diss))
+
+
+def _van_leer_half(state, nx, ny, nz, gamma, sign):
+    """One-sided Van Leer split flux (physics.py:267-290)."""
+    rho, u, v, w, p = state
+    a = np.sqrt(gamma * p / rho)
+    vn = (u * nx + v * ny) + w * nz
+    mach = vn / a
+    kinetic = 0.5 * ((u * u + v * v) + w * w)
+    whole = euler_flux(rho, u, v, w, p, nx, ny, nz, gamma)
+    shifted = mach + sign
+    fmass = (((sign * 0.25) * rho) * a) * (shifted * shifted)
+    corr = (-vn + (sign * 2.0) * a) / gamma
+    e_top = (gamma - 1.0) * vn + (sign * 2.0) * a
+    part = (fmass,
+            fmass * (u + nx * corr),
+            fmass * (v + ny * corr),
+            fmass * (w + nz * corr),
+            fmass * (((e_top * e_top) / (2.0 * (gamma * gamma - 1.0)) + kinetic)
+                     - (0.5 * vn) * vn))
+    upwind = sign * mach >= 1.0
+    blocked = sign * mach <= -1.0
+    return tuple(np.where(upwind, full, np.where(blocked, np.zeros_like(sp), sp))
+                 for sp, full in zip(part, whole))
+
+
+def van_leer(left, right, nx, ny, nz, gamma):
+    """Van Leer FVS (physics.py:293-297)."""
+    plus = _van_leer_half(left, nx, ny, nz, gamma, +1.0)
+    minus = _van_leer_half(right, nx, ny, nz, gamma, -1.0)
+    return tuple(a + b for a, b in zip(plus, minus))
+
+
+def farfield(rho, u, v, w, p, fs, nx, ny, nz, gamma):
+    """Riemann-invariant farfield state; (nx,ny,nz) outward (solver.py:138-171)."""
+    g = gamma
+    ai = np.sqrt(g * p / rho)
+    vni = (u * nx + v * ny) + w * nz
+    af = np.sqrt(g * fs.p / fs.rho)
+    vnf = (fs.u * nx + fs.v * ny) + fs.w * nz
+    rout = vni + 2.0 * ai / (g - 1.0)
+    rin = vnf - 2.0 * af / (g - 1.0)
+    vnb = 0.5 * (rout + rin)
+    ab = (0.25 * (g - 1.0)) * (rout - rin)
+    out = vnb > 0.0
+    sb = np.where(out, p / rho ** g, fs.p / fs.rho ** g)
+    ut = np.where(out, u - vni * nx, fs.u - vnf * nx)
+    vt = np.where(out, v - vni * ny, fs.v - vnf * ny)
+    wt = np.where(out, w - vni * nz, fs.w - vnf * nz)
+    rb = (ab * ab / (g * sb)) ** (1.0 / (g - 1.0))
+    pb = ((rb * ab) * ab) / g
+    sup_out = vnb >= ab
+    sup_in = vnb <= -ab
+    pick = lambda mine, theirs, other: np.where(sup_out, mine, np.where(sup_in, theirs, other))
+    return (pick(rho, fs.rho, rb), pick(u, fs.u, ut + vnb * nx), pick(v, fs.v, vt + vnb * ny),
+            pick(w, fs.w, wt + vnb * nz), pick(p, fs.p, pb))
+
+
+def along(arr, d, lo, hi):
+    """View of `arr` restricted to [lo, hi) on axis d."""
+    cut = [slice(None)] * arr.ndim
+    cut[d] = slice(lo, hi)
+    return arr[tuple(cut)]
+
+
+# ---------------------------------------------------------------------------
+# Limiters (solver.py:105-131)
+# ---------------------------------------------------------------------------
+
+def _lim_none(a, b):
+    return np.ones_like(b)
+
+
+def _lim_van_albada(a, b):
+    return np.maximum(0.0, ((2.0 * a) * b + 1e-12) / ((a * a + b * b) + 1e-12))
+
+
+def _lim_minmod(a, b):
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = a / b
+    return np.where(a * b > 0.0, np.minimum(1.0, r), 0.0)
+
+
+def _lim_van_leer(a, b):
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = a / b
+        phi = (2.0 * r) / (1.0 + r)
+    return np.where(a * b > 0.0, phi, 0.0)
+
+
+LIMITER = {"none": _lim_none, "van_albada": _lim_van_albada,
+           "minmod": _lim_minmod, "van_leer": _lim_van_leer}
+
+
+# ---------------------------------------------------------------------------
+# Halo pack / unpack (halo.py:27-115, topology.py:224-262)
+# ---------------------------------------------------------------------------
+
+def _halo_boxes(spec, dims, ghost, round_no):
+    ax = FACE_NAMES.index(spec.face) // 2
+    side = FACE_NAMES.index(spec.face) % 2
+    g = ghost[ax]
+    top = g + dims[ax]
+    send = [(g, 2 * g) if side == 0 else (top - g, top)]
+    recv = [(0, g) if side == 0 else (top, top + g)]
+    boxes_s, boxes_r = [], []
+    for a in range(3):
+        if a == ax:
+            boxes_s.append(send[0])
+            boxes_r.append(recv[0])
+        else:
+            ext = ghost[a] if round_no == 2 else 0
+            lo, hi = spec.box[a]
+            boxes_s.append((ghost[a] + lo - ext, ghost[a] + hi + ext))
+            boxes_r.append((ghost[a] + lo - ext, ghost[a] + hi + ext))
+    return tuple(boxes_s), tuple(boxes_r)
+
+
+def _exchanged(ndim):
+    """Fields moved by an exchange, in buffer order (halo.py:27-32)."""
+    return ("rho",) + ("u", "v", "w")[:ndim] + ("p", "T")
+
+
+def pack_face(fields, spec, dims, ghost, round_no=1):
+    """Send-box values, i-fastest, one flat array per exchanged field."""
+    send, _ = _halo_boxes(spec, dims, ghost, round_no)
+    cut = tuple(slice(lo, hi) for lo, hi in send)
+    ndim = 2 if ghost[2] == 0 else 3
+    return {n: fields[n][cut].ravel(order="F") for n in _exchanged(ndim)}
+
+
+def unpack_face(buffers, fields, spec, dims, ghost, partner_side, round_no=1):
+    """Scatter a partner's packed buffers into this block's ghost box."""
+    _, recv = _halo_boxes(spec, dims, ghost, round_no)
+    own_shape = tuple(hi - lo for lo, hi in recv)
+    perm = [spec.axis_map[a][0] for a in range(3)]
+    partner_shape = [0, 0, 0]
+    for a in range(3):
+        partner_shape[perm[a]] = own_shape[a]
+    ax = FACE_NAMES.index(spec.face) // 2
+    own_side = FACE_NAMES.index(spec.face) % 2
+    cut = tuple(slice(lo, hi) for lo, hi in recv)
+    ndim = 2 if ghost[2] == 0 else 3
+    for n in _exchanged(ndim):
+        flat = np.asarray(buffers[n])
+        if flat.size != int(np.prod(partner_shape)):
+            raise ValueError(f"buffer for {n!r} has {flat.size} entries, "
+                             f"boundary needs {int(np.prod(partner_shape))}")
+        arr = np.transpose(flat.reshape(partner_shape, order="F"), axes=perm)
+        for a in range(3):
+            flip = (own_side == partner_side) if a == ax else spec.axis_map[a][1] < 0
+            if flip:
+                arr = np.flip(arr, axis=a)
+        fields[n][cut] = arr
+
+
+# ---------------------------------------------------------------------------
+# Per-block state (solver.py:178-756)
+# ---------------------------------------------------------------------------
+
+class OracleBlock:
+    """One block's fields and residual machinery on the CPU."""
+
+    def __init__(self, block, specs, metrics, gas, config, freestream,
+                 mms_solution=None, mms_source=None):
+        self.block = block
+        self.gas = gas
+        self.config = config
+        self.fs = freestream
+        self.metrics = metrics
+        ordered = sorted(specs, key=lambda s: s.canonical_key())
+        self.physical = [s for s in ordered if s.kind == "physical"]
+        self.dirs = (0, 1) if block.ndim == 2 else (0, 1, 2)
+        self.g = block.ghost
+        self.n = block.dims
+        self.fields = {nm: block.allocate_field() for nm in ALL_FIELDS}
+        self.q = [block.allocate_field() for _ in range(5)]
+        self.psi = {}
+        self.frozen = False
+        self.inner = block.interior()
+        self.vol = metrics.volume[self.inner]
+        self.normal, self.area = {}, {}
+        for d in self.dirs:
+            sv = metrics.face_vectors[d]
+            area = np.sqrt((sv[0] * sv[0] + sv[1] * sv[1]) + sv[2] * sv[2])
+            with np.errstate(invalid="ignore", divide="ignore"):
+                self.normal[d] = np.where(area > 0.0, sv / area, 0.0)
+            self.area[d] = area
+        self.mms_solution = mms_solution
+        self.source = None
+        self._dirichlet = {}
+        if config.mms_id is not None:
+            c = metrics.centers
+            xs, ys, zs = (c[i][self.inner] for i in range(3))
+            self.source = [np.asarray(s) * self.vol for s in mms_source(xs, ys, zs, config.mms_id, gas)]
+
+    # index helpers ----------------------------------------------------------
+    def run(self, d, start, stop):
+        """Padded cells [start, stop) along d, interior on the other axes."""
+        cut = list(self.inner)
+        cut[d] = slice(start, stop)
+        return tuple(cut)
+
+    def face_cut(self, d):
+        """Interior-tangential window of a padded face array (with leading comp axis)."""
+        cut = [slice(self.g[a], self.g[a] + self.n[a]) for a in range(3)]
+        cut[d] = slice(None)
+        return (slice(None), *cut)
+
+    # initial state ------------------------------------------------------------
+    def init_uniform(self, state=None):
+        st = state or self.fs
+        for nm in ALL_FIELDS:
+            self.fields[nm].fill(getattr(st, nm))
+        self.sync_conserved()
+
+    def init_manufactured(self):
+        c = self.metrics.centers
+        for nm in PRIMS:
+            self.fields[nm][...] = self.mms_solution[nm](c[0], c[1], c[2])
+        self.fields["T"][...] = self.fields["p"] / (self.fields["rho"] * self.gas.R)
+        self.sync_conserved()
+
+    def sync_conserved(self):
+        for dst, src in zip(self.q, encode(*(self.fields[n] for n in PRIMS), self.gas.gamma)):
+            dst[...] = src
+
+    # physical boundary ghosts (solver.py:281-403) ----------------------------------
+    def _layers(self, spec, extended):
+        d = FACE_NAMES.index(spec.face) // 2
+        side = FACE_NAMES.index(spec.face) % 2
+        g, n = self.g, self.n[d]
+        tang = []
+        for a in range(3):
+            if a == d:
+                tang.append(None)
+            else:
+                ext = g[a] if extended else 0
+                tang.append(slice(g[a] + spec.box[a][0] - ext, g[a] + spec.box[a][1] + ext))
+        if side == 0:
+            pairs = [(g[d] - 1 - k, g[d] + k) for k in range(self.block.ghost_depth)]
+        else:
+            pairs = [(g[d] + n + k, g[d] + n - 1 - k) for k in range(self.block.ghost_depth)]
+        return d, side, pairs, tang
+
+    @staticmethod
+    def _at(d, pos, tang):
+        cut = list(tang)
+        cut[d] = pos
+        return tuple(cut)
+
+    def _outward(self, d, side, tang):
+        cut = list(tang)
+        cut[d] = 0 if side == 0 else self.n[d]
+        nh = self.normal[d][(slice(None), *cut)]
+        s = -1.0 if side == 0 else 1.0
+        return s * nh[0], s * nh[1], s * nh[2]
+
+    def fill_physical_ghosts(self, extended=False):
+        for spec in self.physical:
+            self._fill_one(spec, extended)
+
+    def _fill_one(self, spec, extended):
+        f = self.fields
+        d, side, pairs, tang = self._layers(spec, extended)
+        kind = spec.bc_type
+        if kind == "supersonic_inflow":
+            for gp, _ in pairs:
+                for nm in ALL_FIELDS:
+                    f[nm][self._at(d, gp, tang)] = getattr(self.fs, nm)
+        elif kind == "supersonic_outflow":
+            src = self._at(d, pairs[0][1], tang)
+            vals = {nm: f[nm][src] for nm in ALL_FIELDS}
+            for gp, _ in pairs:
+                for nm in ALL_FIELDS:
+                    f[nm][self._at(d, gp, tang)] = vals[nm]
+        elif kind in ("slip_wall", "noslip_wall"):
+            nx, ny, nz = self._outward(d, side, tang)
+            tw = self.config.wall_temperature
+            for gp, ip in pairs:
+                gi, ii = self._at(d, gp, tang), self._at(d, ip, tang)
+                u, v, w = f["u"][ii], f["v"][ii], f["w"][ii]
+                if kind == "slip_wall":
+                    vn = (u * nx + v * ny) + w * nz
+                    f["u"][gi] = u - (2.0 * vn) * nx
+                    f["v"][gi] = v - (2.0 * vn) * ny
+                    f["w"][gi] = w - (2.0 * vn) * nz
+                else:
+                    f["u"][gi], f["v"][gi], f["w"][gi] = -u, -v, -w
+                f["p"][gi] = f["p"][ii]
+                if kind == "noslip_wall" and tw is not None:
+                    f["T"][gi] = 2.0 * tw - f["T"][ii]
+                else:
+                    f["T"][gi] = f["T"][ii]
+                f["rho"][gi] = f["p"][gi] / (self.gas.R * f["T"][gi])
+        elif kind == "farfield":
+            nx, ny, nz = self._outward(d, side, tang)
+            src = self._at(d, pairs[0][1], tang)
+            rb, ub, vb, wb, pb = farfield(f["rho"][src], f["u"][src], f["v"][src], f["w"][src],
+                                          f["p"][src], self.fs, nx, ny, nz, self.gas.gamma)
+            tb = pb / (rb * self.gas.R)
+            for gp, _ in pairs:
+                gi = self._at(d, gp, tang)
+                for nm, val in zip(ALL_FIELDS, (rb, ub, vb, wb, pb, tb)):
+                    f[nm][gi] = val
+        elif kind == "mms_dirichlet":
+            key = (spec.canonical_key(), extended)
+            if key not in self._dirichlet:
+                c = self.metrics.centers
+                store = []
+                for gp, _ in pairs:
+                    gi = self._at(d, gp, tang)
+                    vals = {nm: self.mms_solution[nm](c[0][gi], c[1][gi], c[2][gi])
+                            for nm in PRIMS}
+                    vals["T"] = vals["p"] / (vals["rho"] * self.gas.R)
+                    store.append((gi, vals))
+                self._dirichlet[key] = store
+            for gi, vals in self._dirichlet[key]:
+                for nm, val in vals.items():
+                    f[nm][gi] = val
+        else:
+            raise ConfigError(f"unknown physical bc type {kind!r}")
+
+    def dirichlet_ghosts(self):
+        """Cached MMS ghost values per patch, for lowering to the device."""
+        return self._dirichlet
+
+    # limiters + MUSCL (solver.py:413-474) -------------------------------------------
+    def compute_limiters(self):
+        if self.frozen and self.psi:
+            return
+        fn = LIMITER[self.config.limiter]
+        for d in self.dirs:
+            g, n = self.g[d], self.n[d]
+            plus, minus = [], []
+            for nm in PRIMS:
+                w = self.fields[nm]
+                jump = w[self.run(d, g - 1, g + n + 2)] - w[self.run(d, g - 2, g + n + 1)]
+                upper = along(jump, d, 1, n + 3)
+                lower = along(jump, d, 0, n + 2)
+                plus.append(fn(upper, lower))
+                minus.append(fn(lower, upper))
+            self.psi[d] = (np.stack(plus), np.stack(minus))
+
+    def reconstruct(self, d):
+        g, n = self.g[d], self.n[d]
+        eps = float(self.config.epsilon)
+        kap = self.config.kappa
+        plus, minus = self.psi[d]
+        left, right = [], []
+        for iv, nm in enumerate(PRIMS):
+            w = self.fields[nm]
+            wl = w[self.run(d, g - 1, g + n)]
+            wr = w[self.run(d, g, g + n + 1)]
+            if eps == 0.0:
+                left.append(wl.copy())
+                right.append(wr.copy())
+                continue
+            jump = w[self.run(d, g - 1, g + n + 2)] - w[self.run(d, g - 2, g + n + 1)]
+            take = lambda arr, lo: along(arr, d, lo, lo + n + 1)
+            jm, j0, jp = take(jump, 0), take(jump, 1), take(jump, 2)
+            pp, pm = plus[iv], minus[iv]
+            qtr = eps / 4.0
+            left.append(wl + qtr * (((1.0 - kap) * take(pp, 0)) * jm
+                                    + ((1.0 + kap) * take(pm, 0)) * j0))
+            right.append(wr - qtr * (((1.0 + kap) * take(pp, 1)) * j0
+                                     + ((1.0 - kap) * take(pm, 1)) * jp))
+        return left, right
+
+    # residual (solver.py:478-580) ------------------------------------------------------
+    def residual(self, return_face_fluxes=False):
+        R = [np.zeros(self.n) for _ in range(5)]
+        fluxes = {}
+        for d in self.dirs:
+            F = self.direction_flux(d)
+            fluxes[d] = F
+            n = self.n[d]
+            for eq in range(5):
+                R[eq] += along(F[eq], d, 1, n + 1) - along(F[eq], d, 0, n)
+        if self.source is not None:
+            for eq in range(5):
+                R[eq] -= self.source[eq]
+        return (R, fluxes) if return_face_fluxes else R
+
+    def direction_flux(self, d):
+        left, right = self.reconstruct(d)
+        for label, st in (("left", left), ("right", right)):
+            bad = (np.asarray(st[0]) <= 0.0) | (np.asarray(st[4]) <= 0.0)
+            if np.any(bad):
+                first = np.argwhere(bad)[0]
+                raise NonPhysicalStateError(
+                    f"block {self.block.id}: non-physical {label} face state, "
+                    f"direction {d}, face index {tuple(first)}")
+        cut = self.face_cut(d)
+        nh = self.normal[d][cut]
+        ar = self.area[d][cut[1:]]
+        if self.config.flux == "roe":
+            F = roe(tuple(left), tuple(right), nh[0], nh[1], nh[2], self.gas.gamma,
+                    self.config.entropy_fix_coeff)
+        else:
+            F = van_leer(tuple(left), tuple(right), nh[0], nh[1], nh[2], self.gas.gamma)
+        F = [comp * ar for comp in F]
+        self._boundary_fluxes(d, F)
+        if self.config.viscous:
+            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+        return F
+
+    def _boundary_fluxes(self, d, F):
+        f, g = self.fields, self.g
+        n = self.n[d]
+        for spec in self.physical:
+            ax = FACE_NAMES.index(spec.face) // 2
+            if ax != d or spec.bc_type not in ("slip_wall", "noslip_wall", "farfield"):
+                continue
+            side = FACE_NAMES.index(spec.face) % 2
+            plane = 0 if side == 0 else n
+            fcut, pcut = [], []
+            for a in range(3):
+                lo, hi = spec.box[a]
+                fcut.append(plane if a == d else slice(lo, hi))
+                pcut.append(None if a == d else slice(g[a] + lo, g[a] + hi))
+            fcut = tuple(fcut)
+            first, second = list(pcut), list(pcut)
+            if side == 0:
+                first[d], second[d] = g[d], g[d] + 1
+            else:
+                first[d], second[d] = g[d] + n - 1, g[d] + n - 2
+            first, second = tuple(first), tuple(second)
+            ncut = list(pcut)
+            ncut[d] = plane
+            nh = self.normal[d][(slice(None), *ncut)]
+            ar = self.area[d][tuple(ncut)]
+            if spec.bc_type != "farfield":
+                pw = 1.5 * f["p"][first] - 0.5 * f["p"][second]
+                F[0][fcut] = 0.0
+                F[1][fcut] = (nh[0] * pw) * ar
+                F[2][fcut] = (nh[1] * pw) * ar
+                F[3][fcut] = (nh[2] * pw) * ar
+                F[4][fcut] = 0.0
+            else:
+                s = -1.0 if side == 0 else 1.0
+                qb = farfield(f["rho"][first], f["u"][first], f["v"][first], f["w"][first],
+                              f["p"][first], self.fs, s * nh[0], s * nh[1], s * nh[2],
+                              self.gas.gamma)
+                Fb = euler_flux(*qb, nh[0], nh[1], nh[2], self.gas.gamma)
+                for eq in range(5):
+                    F[eq][fcut] = Fb[eq] * ar
+
+    # time step and update (solver.py:696-756) ------------------------------------------
+    def local_time_step(self, cfl=None):
+        cfl = self.config.cfl if cfl is None else cfl
+        f = self.fields
+        rho = f["rho"][self.inner]
+        u, v, w = f["u"][self.inner], f["v"][self.inner], f["w"][self.inner]
+        a = np.sqrt(self.gas.gamma * f["p"][self.inner] / rho)
+        lam = np.zeros(self.n)
+        for d in self.dirs:
+            cut = self.face_cut(d)
+            nh = self.normal[d][cut]
+            ar = self.area[d][cut[1:]]
+            for lo in (0, 1):
+                nx, ny, nz = (along(nh[i], d, lo, lo + self.n[d]) for i in range(3))
+                lam += (np.abs((u * nx + v * ny) + w * nz) + a) * along(ar, d, lo, lo + self.n[d])
+        if self.config.viscous:
+            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+        return (cfl * self.vol) / lam
+
+    def snapshot(self):
+        return [q[self.inner].copy() for q in self.q]
+
+    def apply_stage(self, q0, alpha, dtv, R):
+        qn = [q0[eq] - (alpha * dtv) * R[eq] for eq in range(5)]
+        rho, u, v, w, p = decode(*qn, self.gas.gamma)
+        bad = (rho <= 0.0) | (p <= 0.0)
+        if np.any(bad):
+            raise NonPhysicalStateError(
+                f"block {self.block.id}: non-physical update at cell "
+                f"{tuple(np.argwhere(bad)[0])} (CFL {self.config.cfl} may be too high)")
+        for eq in range(5):
+            self.q[eq][self.inner] = qn[eq]
+        for nm, val in zip(PRIMS, (rho, u, v, w, p)):
+            self.fields[nm][self.inner] = val
+        self.fields["T"][self.inner] = p / (rho * self.gas.R)
+
+    @staticmethod
+    def sumsq(R):
+        return np.array([float(np.sum(r * r)) for r in R])
+
+
+# ---------------------------------------------------------------------------
+# Drivers (solver.py:763-936, exchange.py:599-682)
+# ---------------------------------------------------------------------------
+
+class OracleStepper:
+    """RankStepper semantics: snapshots/dt for all blocks, then per stage
+    ghosts -> residuals for all -> updates for all (solver.py:786-814)."""
+
+    def __init__(self, blocks, exchange_fn, config):
+        self.blocks = dict(sorted(blocks.items()))
+        self.exchange_fn = exchange_fn
+        self.config = config
+        self.alphas = RK_ALPHAS[config.rk_stages]
+
+    def update_ghosts(self):
+        self.exchange_fn(1)
+        for b in self.blocks.values():
+            b.fill_physical_ghosts(extended=False)
+        if self.config.viscous:
+            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+
+    def step(self, step_index):
+        fz = self.config.limiter_freeze_at
+        for b in self.blocks.values():
+            b.frozen = fz is not None and step_index > fz
+        q0 = {cid: b.snapshot() for cid, b in self.blocks.items()}
+        dtv = {cid: b.local_time_step() / b.vol for cid, b in self.blocks.items()}
+        total = np.zeros(5)
+        cells = 0
+        for k, alpha in enumerate(self.alphas):
+            self.update_ghosts()
+            res = {}
+            for cid, b in self.blocks.items():
+                b.compute_limiters()
+                res[cid] = b.residual()
+                if k == 0:
+                    total += b.sumsq(res[cid])
+                    cells += b.block.cell_count()
+            for cid, b in self.blocks.items():
+                b.apply_stage(q0[cid], alpha, dtv[cid], res[cid])
+        return total, cells
+
+
+def _peer_spec(plan, entry):
+    for s in plan.boundaries[entry.peer_child]:
+        if s.kind == "connected" and s.link_id == entry.spec.link_id and s is not entry.spec:
+            if s.face != entry.spec.face or s.box != entry.spec.box or \
+                    entry.peer_child != entry.child:
+                return s
+    raise KeyError(f"no peer spec for link {entry.spec.link_id}")
+
+
+def make_serial_exchange(plan, schedule, blocks):
+    """Round-1 local copies in rank-major schedule order (solver.py:869-899)."""
+    order = [e for r in sorted(schedule.per_rank) for e in schedule.per_rank[r]]
+
+    def exchange(round_no):
+        if round_no != 1:
+            raise NotImplementedError("round 2 is viscous-only")
+        for e in order:
+            dst, src = blocks[e.child], blocks[e.peer_child]
+            ps = _peer_spec(plan, e)
+            bufs = pack_face(src.fields, ps, src.block.dims, src.block.ghost, 1)
+            side = FACE_NAMES.index(ps.face) % 2
+            unpack_face(bufs, dst.fields, e.spec, dst.block.dims, dst.block.ghost, side, 1)
+    return exchange
+
+
+def _default_setup():
+    from paper_2012_02925_b200 import geometry, mms
+    return geometry.compute_metrics, mms.manufactured_solution, mms.mms_source
+
+
+def build_blocks(plan, gas, config, freestream, child_ids=None, metrics_fn=None,
+                 mms_solution=None, mms_source=None, metrics=None):
+    mfn, msol, msrc = _default_setup()
+    metrics_fn = metrics_fn or mfn
+    sol = msol(config.mms_id) if (config.mms_id is not None and mms_solution is None) \
+        else mms_solution
+    src = mms_source or msrc
+    out = {}
+    for c in plan.children:
+        if child_ids is not None and c.id not in child_ids:
+            continue
+        blk = plan.child_block(c.id)
+        m = metrics[c.id] if metrics is not None else metrics_fn(blk)
+        out[c.id] = OracleBlock(blk, plan.boundaries[c.id], m, gas, config, freestream,
+                                mms_solution=sol, mms_source=src)
+    return out
+
+
+def _init(blocks, init):
+    for b in blocks.values():
+        b.init_manufactured() if init == "manufactured" else b.init_uniform()
+
+
+def check_guards(history, step, residual_target, divergence_factor=1e6, residual_floor=None):
+    """solver.py:836-855 (DivergenceError raised by the caller's class)."""
+    from paper_2012_02925_b200.errors import DivergenceError
+    if residual_floor is not None and float(np.max(history[step])) <= residual_floor:
+        return True
+    base = history[0]
+    active = base > 1e-12 * np.max(base)
+    if not np.any(active):
+        return False
+    rel = history[step][active] / base[active]
+    if np.any(~np.isfinite(rel)) or np.max(rel) > divergence_factor:
+        raise DivergenceError(
+            f"residual grew by more than {divergence_factor:.0e} at step {step + 1}")
+    return residual_target is not None and float(np.max(rel)) <= residual_target
+
+
+class OracleResult:
+    def __init__(self, blocks, history, steps, converged):
+        self.solvers = blocks
+        self.history = history
+        self.steps = steps
+        self.converged = converged
+
+
+def iterate(plan, schedule, gas, config, freestream, max_steps, residual_target=None,
+            init="uniform", residual_floor=None, blocks=None, **setup):
+    """Serial iteration over all children (solver.py:914-936)."""
+    blocks = blocks if blocks is not None else build_blocks(plan, gas, config, freestream,
+                                                            **setup)
+    _init(blocks, init)
+    stepper = OracleStepper(blocks, make_serial_exchange(plan, schedule, blocks), config)
+    hist, done = [], False
+    for k in range(max_steps):
+        ss, _ = stepper.step(k + 1)
+        hist.append(np.sqrt(np.asarray(ss)))
+        if check_guards(hist, k, residual_target, residual_floor=residual_floor):
+            done = True
+            break
+    return OracleResult(blocks, np.array(hist), len(hist), done)
+
+
+def run_threaded(plan, schedule, gas, config, freestream, max_steps, init="uniform",
+                 **setup):
+    """One thread per rank, deterministic rank-ordered sum of the per-rank
+    Σ R² (exchange.py:294-309, 599-682).  Exchanges are in-process copies in
+    schedule order behind a barrier per stage, which yields the same fields
+    as any message ordering (halo regions are disjoint)."""
+    nr = plan.np_ranks
+    per_rank = {r: build_blocks(plan, gas, config, freestream,
+                                child_ids=[c.id for c in plan.rank_children(r)], **setup)
+                for r in range(nr)}
+    everyone = {cid: b for blocks in per_rank.values() for cid, b in blocks.items()}
+    _init(everyone, init)
+    bar = threading.Barrier(nr)
+    order = {r: schedule.entries(r) for r in range(nr)}
+    partial = {}
+    errors = {}
+    history = []
+
+    def exchange_for(rank):
+        def ex(round_no):
+            bar.wait()  # every rank finished its previous update
+            for e in order[rank]:
+                src = everyone[e.peer_child]
+                dst = everyone[e.child]
+                ps = _peer_spec(plan, e)
+                bufs = pack_face(src.fields, ps, src.block.dims, src.block.ghost, 1)
+                unpack_face(bufs, dst.fields, e.spec, dst.block.dims, dst.block.ghost,
+                            FACE_NAMES.index(ps.face) % 2, 1)
+            bar.wait()
+        return ex
+
+    def worker(rank):
+        try:
+            st = OracleStepper(per_rank[rank], exchange_for(rank), config)
+            for k in range(max_steps):
+                ss, _ = st.step(k + 1)
+                partial[(k, rank)] = ss
+                bar.wait()
+                if rank == 0:
+                    tot = None
+                    for r in range(nr):
+                        tot = partial[(k, r)] if tot is None else tot + partial[(k, r)]
+                    history.append(np.sqrt(np.asarray(tot)))
+                bar.wait()
+        except threading.BrokenBarrierError:
+            pass
+        except BaseException as exc:  # noqa: BLE001
+            errors[rank] = exc
+            bar.abort()
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(nr)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errors:
+        raise sorted(errors.items())[0][1]
+    return OracleResult(everyone, np.array(history), len(history), False)
