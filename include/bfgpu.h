@@ -1,0 +1,199 @@
+/*
+ * bfgpu.h — C ABI of the B200-native multi-block finite-volume hot path.
+ *
+ * One bf_ctx owns the blocks of ONE rank on ONE GPU and runs the reference's
+ * per-RK-stage pipeline on the device.  Every entry point replaces a piece
+ * of the reference's Python path (file:line into /root/reference/pkg/src/
+ * blockflow/); the ctypes binding a maintainer adds is in INTEGRATION.md and
+ * paper_2012_02925_b200/native.py.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; host arrays are float64, Fortran
+ *     (i-fastest) order, exactly the reference's numpy layouts;
+ *   - every int-returning call returns 0 on success or a BF_E* code, with a
+ *     message retrievable through bf_last_error();
+ *   - a ctx is not thread-safe; calls on one ctx must be serialised.
+ */
+#ifndef BFGPU_H
+#define BFGPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BF_API_VERSION 1
+
+/* return codes */
+#define BF_OK 0
+#define BF_EINVAL 1          /* bad argument / call order (ConfigError, TopologyError)  */
+#define BF_ECUDA 2           /* CUDA runtime failure                                    */
+#define BF_ENONPHYSICAL 3    /* NonPhysicalStateError: see bf_error_info()              */
+#define BF_ENCCL 4           /* NCCL failure                                            */
+
+/* solver.py:31-32 */
+#define BF_FLUX_ROE 0
+#define BF_FLUX_VAN_LEER 1
+#define BF_LIM_NONE 0
+#define BF_LIM_VAN_LEER 1
+#define BF_LIM_VAN_ALBADA 2
+#define BF_LIM_MINMOD 3
+
+/* topology.py:25-32, same order as PHYSICAL_BC_TYPES */
+#define BF_BC_SUPERSONIC_INFLOW 0
+#define BF_BC_SUPERSONIC_OUTFLOW 1
+#define BF_BC_SLIP_WALL 2
+#define BF_BC_NOSLIP_WALL 3
+#define BF_BC_FARFIELD 4
+#define BF_BC_MMS_DIRICHLET 5
+
+/* topology.py:23, FACES order: i_min i_max j_min j_max k_min k_max = 0..5 */
+
+/* bf_download / bf_upload selectors */
+#define BF_FIELD_RHO 0
+#define BF_FIELD_U 1
+#define BF_FIELD_V 2
+#define BF_FIELD_W 3
+#define BF_FIELD_P 4
+#define BF_FIELD_T 5
+#define BF_FIELD_Q0 6        /* Q0..Q4 = 6..10: conserved variables */
+#define BF_FIELD_DTV 11      /* dt / V of the last step, interior only */
+#define BF_FIELD_PSI 12      /* limiter arrays: 12 + 10*d + 5*minus + var */
+
+/* arithmetic modes */
+#define BF_PRECISION_EXACT 0 /* reference evaluation order, no FMA contraction: bitwise  */
+#define BF_PRECISION_FAST 1  /* FMA + strength reduction: within 1e-12 of the reference  */
+
+/* error kinds reported by bf_error_info (NonPhysicalStateError texts, solver.py:501-506,
+   740-744; physics.py:213-217) */
+#define BF_ERR_FACE_LEFT 1
+#define BF_ERR_FACE_RIGHT 2
+#define BF_ERR_ROE_A2 3
+#define BF_ERR_UPDATE 4
+
+typedef struct bf_ctx bf_ctx;
+typedef struct bf_group bf_group;
+
+typedef struct bf_gas {            /* physics.py:47-62 (inviscid part) */
+  double gamma;
+  double R;
+} bf_gas;
+
+typedef struct bf_freestream {     /* solver.py:74-98 */
+  double rho, u, v, w, p, T;
+} bf_freestream;
+
+typedef struct bf_scheme {         /* solver.py:38-66 */
+  int flux;                        /* BF_FLUX_*                      */
+  int limiter;                     /* BF_LIM_*                       */
+  double epsilon;                  /* 0 or 1                         */
+  double kappa;                    /* [-1, 1]                        */
+  int rk_stages;                   /* 1, 2 or 4                      */
+  double cfl;
+  int limiter_freeze_at;           /* <= 0: never freeze             */
+  double entropy_fix_coeff;
+  int has_wall_temperature;
+  double wall_temperature;
+  int precision;                   /* BF_PRECISION_*                 */
+} bf_scheme;
+
+/* --- context lifetime (replaces BlockSolver construction, solver.py:189-231,
+       and build_block_solvers, solver.py:858-866) -------------------------- */
+bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme,
+                  const bf_freestream* fs, int device, int rank, int nranks);
+void bf_destroy(bf_ctx* ctx);
+int bf_last_error(const bf_ctx* ctx, char* buf, size_t n);
+int bf_api_version(void);
+
+/* Register one child block owned by this rank (BlockSolver.__init__).
+   dims[3]        interior cells (nk = 1 in 2D);
+   face_vectors   ndim*3 pointers: direction d, component c at [3*d + c], each a
+                  Fortran array of shape (N_d+1, padded tangential...) — the
+                  reference's metrics.face_vectors[d][c] (mesh.py:316-331);
+   volume         interior cell volumes, Fortran (dims);
+   source         5 pointers to S*V (solver.py:225-231) or NULL.            */
+int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
+                 const double* const* face_vectors, const double* volume,
+                 const double* const* source);
+
+/* One physical patch (solver.py:281-403, 526-580).  box[6] = (i0,i1,j0,j1,k0,k1)
+   in the block's interior cell indices (BoundarySpec.box).  dirichlet: for
+   BF_BC_MMS_DIRICHLET the cached ghost values, layout [layer][6 fields][t]
+   with t running i-fastest over the patch's tangential cells; else NULL.   */
+int bf_add_bc_patch(bf_ctx* ctx, int block_id, int bc_type, int face, const int box[6],
+                    const double* dirichlet);
+
+/* One connected endpoint (topology.py:90-188; halo.py:47-115).  axis_map[6] =
+   (b0,s0,b1,s1,b2,s2).  peer_rank == own rank and peer_block registered in this
+   ctx -> same-device copy; otherwise a message to/from peer_rank tagged `tag`. */
+int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int axis_map[6],
+                int peer_block, int peer_face, const int peer_box[6], int peer_rank, int tag);
+
+/* Freeze the topology: device tables, tiles, buffers.  Must precede uploads. */
+int bf_finalize(bf_ctx* ctx);
+
+/* Initial state (init_uniform / init_manufactured / sync_conserved,
+   solver.py:258-277): 6 padded primitive fields + 5 padded conserved fields. */
+int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
+                     const double* const* q5);
+
+/* --- the hot path ------------------------------------------------------ */
+/* RankStepper.update_ghosts (solver.py:777-784): round-1 exchange + physical BCs. */
+int bf_update_ghosts(bf_ctx* ctx);
+/* RankStepper.step (solver.py:786-814).  sumsq_out[5] = sum over this rank's
+   blocks in id order of sum(R^2) from the first stage; when the ctx has an NCCL
+   communicator the rank-ordered sum over all ranks (exchange.py:294-309). */
+int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_out);
+/* nsteps consecutive steps without per-step host synchronisation; per-step
+   norms land in hist_out[nsteps*5] (sqrt of the rank-ordered sums).  Returns at
+   the first step with a non-physical state (bf_error_info names it). */
+int bf_run(bf_ctx* ctx, int first_step, int nsteps, double* hist_out, int* steps_done);
+
+/* --- state access --------------------------------------------------------- */
+/* Padded Fortran array of the block's field `what` (BF_FIELD_*) exactly as the
+   reference's BlockSolver would hold it after the same calls. */
+int bf_download(bf_ctx* ctx, int block_id, int what, double* out);
+/* Details of the last BF_ENONPHYSICAL: kind (BF_ERR_*), block id, stage,
+   direction, index[3] (face or cell index in the reference's array numbering). */
+int bf_error_info(const bf_ctx* ctx, int* kind, int* block_id, int* stage, int* direction,
+                  long long index[3]);
+
+/* --- multi-rank ------------------------------------------------------------ */
+/* NCCL: one process per GPU.  bf_nccl_unique_id fills 128 bytes on rank 0, the
+   caller broadcasts them (torch.distributed), then every rank calls
+   bf_nccl_init before bf_finalize. */
+int bf_nccl_unique_id(void* out128);
+int bf_nccl_init(bf_ctx* ctx, const void* id128);
+/* In-process group: several ctxs (ranks) driven in lock step by one host
+   thread; remote links become device-to-device pushes into the peer's
+   receive buffers (peer access over NVLink when the ctxs sit on different
+   GPUs).  Used for N ranks on fewer GPUs and for single-process multi-GPU. */
+bf_group* bf_group_create(bf_ctx* const* ctxs, int n);
+void bf_group_destroy(bf_group* grp);
+int bf_group_update_ghosts(bf_group* grp);
+int bf_group_step(bf_group* grp, int step_index, double* sumsq_out, int* failed_rank);
+
+/* --- measurement ---------------------------------------------------------- */
+/* Launch on a caller-provided cudaStream_t (e.g. torch's current stream) so the
+   caller's CUDA events bracket the work; NULL restores the ctx's own stream. */
+int bf_set_stream(bf_ctx* ctx, void* cuda_stream);
+/* Per-kernel-class CUDA-event timing: enable, then read {launches, total_ms}
+   for class 0 = stage kernel, 1 = ghost/pack kernel, 2 = unpack, 3 = reduce. */
+int bf_set_profiling(bf_ctx* ctx, int on);
+int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* total_ms);
+/* Device bytes the last bf_upload_fields / bf_download moved (for e2e accounting). */
+long long bf_transfer_bytes(const bf_ctx* ctx, int direction /*0 h2d, 1 d2h*/);
+
+/* Host-only lowering probe (no GPU needed): the affine index map the device
+   unpack applies for one connected endpoint — for each recv-box cell (i-fastest,
+   count = product of recv extents), the partner-send-box linear index it reads.
+   Used by the CPU tests to prove bit-exact ghost indexing against halo.py. */
+int bf_probe_unpack_map(const int own_dims[3], int ghost_depth, int ndim, int face,
+                        const int box[6], const int axis_map[6], int peer_face,
+                        long long* out, long long out_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFGPU_H */

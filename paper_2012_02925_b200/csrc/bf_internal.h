@@ -1,0 +1,164 @@
+// bf_internal.h — device-side tables shared by the runtime and the kernels.
+//
+// HBM layout of one block: every per-cell array (W ping-pong x 6
+// fields, Q x 5, dt/V, V, face normals/areas, sources, limiter arrays) uses the
+// same padded, i-fastest layout with the interior origin 32-byte aligned, so a
+// single (sy, sz) pair of strides addresses all of them and the stage kernel
+// computes one offset per cell.  Pointers below are pre-offset to the interior
+// origin: element (i, j, k) in interior coordinates (ghosts negative) is
+// ptr[i + sy*j + sz*k].
+#pragma once
+#include <cstdint>
+
+namespace bf {
+
+// Stage-kernel tile: TI x TJ threads, each owning one (i, j) column that
+// marches KC cells along k (2.5-D streaming); 2D blocks use the same tile
+// with a single plane.
+constexpr int TI = 32;
+constexpr int TJ = 8;
+constexpr int NT = TI * TJ;
+constexpr int HALO = 2;                  // MUSCL stencil half-width
+constexpr int PW = TI + 2 * HALO;        // smem plane width  (36)
+constexpr int PH = TJ + 2 * HALO;        // smem plane height (12)
+constexpr int PLANE = PW * PH;           // cells per smem plane (432)
+constexpr int NSLOT = 5;                 // plane ring depth (k-1..k+2 + prefetch)
+
+// Scheme switches (bfgpu.h BF_FLUX_* / BF_LIM_*)
+constexpr int FLUX_ROE = 0;
+constexpr int FLUX_VAN_LEER = 1;
+constexpr int LIM_NONE = 0;
+constexpr int LIM_VAN_LEER = 1;
+constexpr int LIM_VAN_ALBADA = 2;
+constexpr int LIM_MINMOD = 3;
+
+// Physical BC types (bfgpu.h BF_BC_*, PHYSICAL_BC_TYPES order)
+constexpr int BC_INFLOW = 0;
+constexpr int BC_OUTFLOW = 1;
+constexpr int BC_SLIP = 2;
+constexpr int BC_NOSLIP = 3;
+constexpr int BC_FARFIELD = 4;
+constexpr int BC_MMS = 5;
+
+// Stage flags
+constexpr int F_STAGE0 = 1;      // first RK stage: compute dt/V and sum(R^2)
+constexpr int F_LAST = 2;        // last RK stage: write Q
+constexpr int F_PSI_STORE = 4;   // write limiter arrays (freeze step, last stage)
+constexpr int F_PSI_LOAD = 8;    // read frozen limiter arrays instead of computing
+constexpr int F_SOURCE = 16;     // subtract S*V (MMS)
+
+// Boundary-face overwrite codes (solver.py:526-580)
+constexpr unsigned char BFACE_NONE = 0;
+constexpr unsigned char BFACE_WALL = 1;
+constexpr unsigned char BFACE_FARFIELD = 2;
+
+// Error kinds (mirror BF_ERR_* in bfgpu.h)
+constexpr int ERR_FACE_LEFT = 1;
+constexpr int ERR_FACE_RIGHT = 2;
+constexpr int ERR_ROE_A2 = 3;
+constexpr int ERR_UPDATE = 4;
+
+struct Consts {
+  double gamma, gm1, gog1, R;              // gamma, gamma-1, gamma/(gamma-1), R
+  double cfl, quarter, omk, opk, efix;     // eps/4, 1-kappa, 1+kappa, entropy fix
+  double fs_rho, fs_u, fs_v, fs_w, fs_p, fs_T;
+  double ff_af;                            // sqrt(g*fs.p/fs.rho)
+  double ff_two_af_gm1;                    // 2*af/(g-1)
+  double ff_sf;                            // fs.p / fs.rho**g  (host libm pow)
+  double ff_qgm1;                          // 0.25*(g-1)
+  double ff_exp;                           // 1/(g-1)
+  double two_over_gm1;                     // 2/(g-1)   (fast mode only)
+  double vl_c;                             // 2*(g*g-1)
+  double tw;                               // wall temperature
+  int has_tw;
+  int eps0;                                // epsilon == 0
+  int pad_;
+};
+
+struct DevBlock {
+  int n[3];
+  int g;            // ghost depth along stencil axes
+  int ndim;
+  int order;        // position of this block in the rank's id order
+  int id;
+  int pad_;
+  long long sy, sz;
+  double* W[2][6];          // rho u v w p T, ping-pong
+  double* Q[5];
+  double* dtv;
+  double* vol;
+  double* fn[3][4];         // per direction: nx, ny, nz, A at face f stored at cell f
+  double* src[5];           // S*V or null
+  double* psi[3][2][5];     // [dir][plus/minus][var] or null
+  const unsigned char* bface[6];   // per face, over tangential interior cells
+};
+
+struct Tile {
+  int block;
+  int i0, j0, k0, kc;
+};
+
+// Ghost-fill work item groups (one launch per stage covers every group).
+enum GhostKind : int {
+  GK_BC = 0,        // physical patch: one item per tangential cell, all layers
+  GK_COPY = 1,      // affine copy: block->block (local link), block->buffer (pack),
+                    // buffer->block (unpack)
+};
+
+struct GhostTask {
+  int kind;
+  int bc_type;          // GK_BC
+  int block;            // GK_BC: block; GK_COPY: destination block (-1: buffer)
+  int src_block;        // GK_COPY: source block (-1: buffer)
+  int axis, side;       // GK_BC
+  int ta, tb;           // GK_BC: tangential axes (tb = 2 with extent 1 in 2D)
+  int tlo[2], tn[2];    // GK_BC: tangential start/extent (interior cells)
+  int depth;            // ghost layers
+  int nfields;          // GK_COPY: 6 (3D) or 5 (2D: rho u v p T)
+  int n[3];             // GK_COPY: item box extents (i-fastest)
+  int pad_;
+  long long items;      // number of work items
+  long long begin;      // prefix offset into the launch's item space
+  long long dst_origin, dst_stride[3];
+  long long src_origin, src_stride[3];
+  long long buf_cells;  // field stride inside a message buffer
+  double* dst_buf;      // GK_COPY into a buffer (pack)
+  const double* src_buf;// GK_COPY from a buffer (unpack)
+  const double* dirichlet;   // GK_BC mms: [layer][6][tn0*tn1]
+};
+
+struct GhostArgs {
+  const DevBlock* blocks;
+  const GhostTask* tasks;
+  int ntasks;
+  int cur;              // W buffer being filled
+  int t_derived;        // interior T is p/(rho R) (after the first update)
+  int pad_;
+  long long total_items;
+  Consts c;
+};
+
+struct StageArgs {
+  const DevBlock* blocks;
+  const Tile* tiles;
+  int ntiles;
+  int cur;              // read W[cur], write W[cur ^ 1]
+  int stage;
+  int flags;
+  double alpha;
+  double* partial;      // [ntiles][5] sum(R^2) partials (stage 0)
+  unsigned long long* err;   // [0] = min error key, [1..] unused
+  Consts c;
+};
+
+// Error key: most significant first
+//   stage(3) | phase(1: 0 residual, 1 update) | block order(12) | dir(2) | kind(2) | index(44)
+__host__ __device__ inline unsigned long long make_err_key(int stage, int phase, int order,
+                                                           int dir, int kind,
+                                                           unsigned long long lin) {
+  return ((unsigned long long)(stage & 7) << 61) | ((unsigned long long)(phase & 1) << 60) |
+         ((unsigned long long)(order & 0xFFF) << 48) | ((unsigned long long)(dir & 3) << 46) |
+         ((unsigned long long)(kind & 3) << 44) | (lin & ((1ull << 44) - 1));
+}
+
+}  // namespace bf

@@ -1,0 +1,180 @@
+// bf_physics.cuh — point physics of the reference, as device functions.
+//
+// Each expression is written in the reference's left-to-right evaluation
+// order (C++ and Python associate + - * / identically), so the EXACT build
+// (-fmad=false: no a*b+c contraction; CUDA's double / and sqrt are IEEE
+// correctly rounded) reproduces numpy bit for bit.  The FAST build compiles
+// the same source with FMA contraction allowed.  Citations: blockflow/.
+#pragma once
+#include "bf_internal.h"
+
+#ifndef BF_NS
+#error "define BF_NS (bf_exact / bf_fast) before including bf_physics.cuh"
+#endif
+
+namespace bf {
+namespace BF_NS {
+
+struct St {
+  double r, u, v, w, p;
+};
+
+#define BF_DEV __device__ __forceinline__
+
+// physics.py:169-175
+BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Consts& c,
+                       double F[5]) {
+  const double vn = s.u * nx + s.v * ny + s.w * nz;
+  const double ke = 0.5 * (s.u * s.u + s.v * s.v + s.w * s.w);
+  const double ht = c.gog1 * s.p / s.r + ke;
+  const double m = s.r * vn;
+  F[0] = m;
+  F[1] = m * s.u + nx * s.p;
+  F[2] = m * s.v + ny * s.p;
+  F[3] = m * s.w + nz * s.p;
+  F[4] = m * ht;
+}
+
+// physics.py:183-187
+BF_DEV double harten_abs(double lam, double delta) {
+  const double mag = fabs(lam);
+  const double safe = delta > 0.0 ? delta : 1.0;
+  return mag < delta ? (lam * lam + delta * delta) / (2.0 * safe) : mag;
+}
+
+// physics.py:190-255.  Returns false when the Roe average has a2 <= 0.
+BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
+                     const Consts& c, double F[5]) {
+  double fl[5], fr[5];
+  euler_flux(L, nx, ny, nz, c, fl);
+  euler_flux(R, nx, ny, nz, c, fr);
+  const double hl = c.gog1 * L.p / L.r + 0.5 * (L.u * L.u + L.v * L.v + L.w * L.w);
+  const double hr = c.gog1 * R.p / R.r + 0.5 * (R.u * R.u + R.v * R.v + R.w * R.w);
+  const double rt = sqrt(R.r / L.r);
+  const double wf = 1.0 / (1.0 + rt);
+  const double rho = rt * L.r;
+  const double u = (L.u + rt * R.u) * wf;
+  const double v = (L.v + rt * R.v) * wf;
+  const double w = (L.w + rt * R.w) * wf;
+  const double h = (hl + rt * hr) * wf;
+  const double a2 = c.gm1 * (h - 0.5 * (u * u + v * v + w * w));
+  const bool ok = !(a2 <= 0.0);
+  const double a = sqrt(a2);
+  const double vn = u * nx + v * ny + w * nz;
+  const double dr = R.r - L.r;
+  const double dp = R.p - L.p;
+  const double du = R.u - L.u;
+  const double dv = R.v - L.v;
+  const double dw = R.w - L.w;
+  const double dvn = du * nx + dv * ny + dw * nz;
+  const double delta = c.efix * (fabs(vn) + a);
+  const double l1 = harten_abs(vn - a, delta);
+  const double l2 = harten_abs(vn, delta);
+  const double l5 = harten_abs(vn + a, delta);
+  const double al1 = (dp - rho * a * dvn) / (2.0 * a2);
+  const double al2 = dr - dp / a2;
+  const double al5 = (dp + rho * a * dvn) / (2.0 * a2);
+  const double su = du - dvn * nx;
+  const double sv = dv - dvn * ny;
+  const double sw = dw - dvn * nz;
+  const double ke = 0.5 * (u * u + v * v + w * w);
+  const double d0 = l1 * al1 + l2 * al2 + l5 * al5;
+  const double d1 = l1 * al1 * (u - a * nx) + l2 * (al2 * u + rho * su) + l5 * al5 * (u + a * nx);
+  const double d2 = l1 * al1 * (v - a * ny) + l2 * (al2 * v + rho * sv) + l5 * al5 * (v + a * ny);
+  const double d3 = l1 * al1 * (w - a * nz) + l2 * (al2 * w + rho * sw) + l5 * al5 * (w + a * nz);
+  const double d4 = l1 * al1 * (h - a * vn) + l2 * (al2 * ke + rho * (u * su + v * sv + w * sw)) +
+                    l5 * al5 * (h + a * vn);
+  F[0] = 0.5 * (fl[0] + fr[0]) - 0.5 * d0;
+  F[1] = 0.5 * (fl[1] + fr[1]) - 0.5 * d1;
+  F[2] = 0.5 * (fl[2] + fr[2]) - 0.5 * d2;
+  F[3] = 0.5 * (fl[3] + fr[3]) - 0.5 * d3;
+  F[4] = 0.5 * (fl[4] + fr[4]) - 0.5 * d4;
+  return ok;
+}
+
+// physics.py:267-290: one side of the Van Leer splitting.  The reference
+// evaluates all branches and selects with np.where; evaluating only the
+// selected branch gives the same doubles.
+BF_DEV void van_leer_half(const St& s, double nx, double ny, double nz, const Consts& c,
+                          double sign, double F[5]) {
+  const double a = sqrt(c.gamma * s.p / s.r);
+  const double vn = s.u * nx + s.v * ny + s.w * nz;
+  const double mn = vn / a;
+  if (sign * mn >= 1.0) {
+    euler_flux(s, nx, ny, nz, c, F);
+    return;
+  }
+  if (sign * mn <= -1.0) {
+    F[0] = F[1] = F[2] = F[3] = F[4] = 0.0;
+    return;
+  }
+  const double ke = 0.5 * (s.u * s.u + s.v * s.v + s.w * s.w);
+  const double sh = mn + sign;
+  const double fm = sign * 0.25 * s.r * a * (sh * sh);
+  const double fac = (-vn + sign * 2.0 * a) / c.gamma;
+  const double et = c.gm1 * vn + sign * 2.0 * a;
+  F[0] = fm;
+  F[1] = fm * (s.u + nx * fac);
+  F[2] = fm * (s.v + ny * fac);
+  F[3] = fm * (s.w + nz * fac);
+  F[4] = fm * (et * et / c.vl_c + ke - 0.5 * vn * vn);
+}
+
+// physics.py:293-297
+BF_DEV void van_leer_flux(const St& L, const St& R, double nx, double ny, double nz,
+                          const Consts& c, double F[5]) {
+  double fp[5], fm[5];
+  van_leer_half(L, nx, ny, nz, c, 1.0, fp);
+  van_leer_half(R, nx, ny, nz, c, -1.0, fm);
+#pragma unroll
+  for (int e = 0; e < 5; ++e) F[e] = fp[e] + fm[e];
+}
+
+// solver.py:138-171, (nx, ny, nz) is the OUTWARD unit normal.
+BF_DEV St farfield_state(const St& s, double nx, double ny, double nz, const Consts& c) {
+  const double g = c.gamma;
+  const double ai = sqrt(g * s.p / s.r);
+  const double vni = s.u * nx + s.v * ny + s.w * nz;
+  const double vnf = c.fs_u * nx + c.fs_v * ny + c.fs_w * nz;
+  const double rout = vni + 2.0 * ai / c.gm1;
+  const double rin = vnf - c.ff_two_af_gm1;
+  const double vnb = 0.5 * (rout + rin);
+  const double ab = c.ff_qgm1 * (rout - rin);
+  const bool out = vnb > 0.0;
+  const double sb = out ? s.p / pow(s.r, g) : c.ff_sf;
+  const double ut = out ? s.u - vni * nx : c.fs_u - vnf * nx;
+  const double vt = out ? s.v - vni * ny : c.fs_v - vnf * ny;
+  const double wt = out ? s.w - vni * nz : c.fs_w - vnf * nz;
+  const double rb = pow(ab * ab / (g * sb), c.ff_exp);
+  const double pb = rb * ab * ab / g;
+  const bool so = vnb >= ab;
+  const bool si = vnb <= -ab;
+  St o;
+  o.r = so ? s.r : (si ? c.fs_rho : rb);
+  o.u = so ? s.u : (si ? c.fs_u : ut + vnb * nx);
+  o.v = so ? s.v : (si ? c.fs_v : vt + vnb * ny);
+  o.w = so ? s.w : (si ? c.fs_w : wt + vnb * nz);
+  o.p = so ? s.p : (si ? c.fs_p : pb);
+  return o;
+}
+
+// solver.py:105-131.  np.maximum / np.minimum NaN semantics kept.
+template <int LIM>
+BF_DEV double limiter(double a, double b) {
+  if constexpr (LIM == LIM_NONE) {
+    return 1.0;
+  } else if constexpr (LIM == LIM_VAN_ALBADA) {
+    const double x = (2.0 * a * b + 1e-12) / (a * a + b * b + 1e-12);
+    return (0.0 >= x) ? 0.0 : x;
+  } else if constexpr (LIM == LIM_MINMOD) {
+    const double r = a / b;
+    return (a * b > 0.0) ? ((1.0 <= r) ? 1.0 : r) : 0.0;
+  } else {
+    const double r = a / b;
+    const double val = 2.0 * r / (1.0 + r);
+    return (a * b > 0.0) ? val : 0.0;
+  }
+}
+
+}  // namespace BF_NS
+}  // namespace bf

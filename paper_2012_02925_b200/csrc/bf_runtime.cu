@@ -1,0 +1,1444 @@
+// bf_runtime.cu — host runtime behind include/bfgpu.h.
+//
+// Owns device memory, lowers the reference's boundary model (BoundarySpec
+// boxes, orientation maps, halo_regions) into device task tables, sequences
+// the per-stage launches (RankStepper.step, solver.py:786-814) on one CUDA
+// stream and moves halo messages with NCCL (one process per GPU) or with
+// device-to-device copies between contexts of one process (bf_group).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/bfgpu.h"
+#include "bf_internal.h"
+
+namespace bf {
+namespace bf_exact {
+cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
+cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
+                          cudaStream_t s);
+}  // namespace bf_exact
+namespace bf_fast {
+cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
+cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
+                          cudaStream_t s);
+}  // namespace bf_fast
+}  // namespace bf
+
+using namespace bf;
+
+namespace {
+
+constexpr unsigned long long NO_ERROR = ~0ull;
+
+struct HostPatch {
+  int block, type, face;
+  int box[6];
+  std::vector<double> dirichlet;
+};
+
+struct HostLink {
+  int block, face;
+  int box[6];
+  int amap[6];
+  int peer_block, peer_face;
+  int peer_box[6];
+  int peer_rank, tag;
+  // remote only, filled at finalize
+  long long cells = 0;
+  int nfields = 0;
+  double* send = nullptr;
+  double* recv = nullptr;
+};
+
+struct HostBlock {
+  int id = 0;
+  int n[3] = {0, 0, 0};
+  int g = 2, gk = 2;
+  int P[3] = {0, 0, 0};      // padded dims
+  long long lead = 0, sy = 0, sz = 0, origin = 0, fsz = 0;
+  double* arena = nullptr;
+  std::vector<double*> owned;  // allocations to free
+  DevBlock dev{};
+  std::vector<unsigned char> bface_h[6];
+  unsigned char* bface_d[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool has_src = false;
+  int tile_begin = 0, tile_end = 0;
+  long long cells() const { return (long long)n[0] * n[1] * n[2]; }
+  long long off(int i, int j, int k) const { return i + sy * (long long)j + sz * (long long)k; }
+};
+
+struct TimerPair {
+  cudaEvent_t a, b;
+  int cls;
+};
+
+}  // namespace
+
+struct bf_ctx {
+  int ndim = 3;
+  bf_gas gas{};
+  bf_scheme sch{};
+  bf_freestream fs{};
+  Consts c{};
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<HostBlock> blocks;
+  std::map<int, int> index_of;     // block id -> position
+  std::vector<HostPatch> patches;
+  std::vector<HostLink> links;
+  bool finalized = false;
+  // device tables
+  DevBlock* d_blocks = nullptr;
+  Tile* d_tiles = nullptr;
+  int ntiles = 0;
+  int* d_tile_begin = nullptr;
+  GhostTask* d_tasks_fill = nullptr;   // BCs + local copies + packs
+  int n_fill = 0;
+  long long items_fill = 0;
+  GhostTask* d_tasks_unpack = nullptr;
+  int n_unpack = 0;
+  long long items_unpack = 0;
+  std::vector<GhostTask> h_tasks_fill, h_tasks_unpack;
+  std::vector<double*> dirichlet_d;
+  double* d_partial = nullptr;
+  double* d_blocksum = nullptr;
+  unsigned long long* d_err = nullptr;
+  double* d_rank6 = nullptr;          // [6] own rank record (NCCL)
+  double* d_gather = nullptr;         // [nranks][6]
+  double* h_pinned = nullptr;         // blocksum + err staging
+  // state
+  int cur = 0;
+  int ghost_buf = 0;
+  int t_derived = 0;
+  bool psi_valid = false;
+  bool have_psi = false;
+  int kc = 32;
+  // errors
+  std::string msg;
+  int e_kind = 0, e_block = -1, e_stage = 0, e_dir = 0;
+  long long e_idx[3] = {0, 0, 0};
+  // comm
+  ncclComm_t comm = nullptr;
+  bf_group* group = nullptr;
+  // profiling
+  bool profiling = false;
+  std::vector<TimerPair> pending;
+  std::vector<cudaEvent_t> event_pool;
+  long long prof_launches[4] = {0, 0, 0, 0};
+  double prof_ms[4] = {0, 0, 0, 0};
+  long long bytes_h2d = 0, bytes_d2h = 0;
+};
+
+struct bf_group {
+  std::vector<bf_ctx*> ctxs;            // index = rank
+  std::vector<cudaEvent_t> ev_packed;   // per ctx
+  std::vector<cudaEvent_t> ev_unpacked; // per ctx
+  bool first = true;
+};
+
+namespace {
+
+int fail(bf_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->msg = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, BF_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define NK(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(ctx, BF_ENCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_),     \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+int face_axis(int face) { return face / 2; }
+int face_side(int face) { return face % 2; }
+
+// topology.py:224-257 in INTERIOR coordinates: [lo, hi) per axis.
+void halo_boxes(int face, const int box[6], const int n[3], const int ghost[3], int send[6],
+                int recv[6]) {
+  const int ax = face_axis(face);
+  const int g = ghost[ax];
+  for (int a = 0; a < 3; ++a) {
+    if (a == ax) {
+      if (face_side(face) == 0) {
+        send[2 * a] = 0;
+        send[2 * a + 1] = g;
+        recv[2 * a] = -g;
+        recv[2 * a + 1] = 0;
+      } else {
+        send[2 * a] = n[a] - g;
+        send[2 * a + 1] = n[a];
+        recv[2 * a] = n[a];
+        recv[2 * a + 1] = n[a] + g;
+      }
+    } else {
+      send[2 * a] = recv[2 * a] = box[2 * a];
+      send[2 * a + 1] = recv[2 * a + 1] = box[2 * a + 1];
+    }
+  }
+}
+
+// Affine map of one endpoint's unpack (halo.py:70-106): for own recv-box
+// local coords o, the partner-local send-box coords are q[perm[a]] =
+// flip_a ? ext_a-1-o_a : o_a.  Returns per own axis the partner axis and flip.
+void unpack_axes(int face, const int amap[6], int peer_face, int perm[3], bool flip[3]) {
+  const int ax = face_axis(face);
+  for (int a = 0; a < 3; ++a) {
+    perm[a] = amap[2 * a];
+    flip[a] = (a == ax) ? (face_side(face) == face_side(peer_face)) : (amap[2 * a + 1] < 0);
+  }
+}
+
+double* dalloc(bf_ctx* ctx, size_t n, int* err) {
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(double));
+  if (e != cudaSuccess) {
+    *err = fail(ctx, BF_ECUDA, "cudaMalloc(%zu bytes) failed: %s", n * sizeof(double),
+                cudaGetErrorString(e));
+    return nullptr;
+  }
+  return static_cast<double*>(p);
+}
+
+cudaError_t (*stage_fn(const bf_ctx* ctx))(int, int, int, const StageArgs&, cudaStream_t) {
+  return ctx->sch.precision == BF_PRECISION_EXACT ? bf_exact::launch_stage : bf_fast::launch_stage;
+}
+cudaError_t (*ghost_fn(const bf_ctx* ctx))(const GhostArgs&, cudaStream_t) {
+  return ctx->sch.precision == BF_PRECISION_EXACT ? bf_exact::launch_ghost : bf_fast::launch_ghost;
+}
+
+cudaEvent_t take_event(bf_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  bf_ctx* ctx;
+  int cls;
+  cudaEvent_t a = nullptr;
+  ProfScope(bf_ctx* c, int k) : ctx(c), cls(k) {
+    if (ctx->profiling) {
+      a = take_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->profiling) {
+      cudaEvent_t b = take_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->pending.push_back({a, b, cls});
+    }
+  }
+};
+
+void drain_profile(bf_ctx* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      ctx->prof_ms[p.cls] += ms;
+      ctx->prof_launches[p.cls] += 1;
+    }
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+}
+
+// ---- finalize helpers ---------------------------------------------------------
+
+int build_tables(bf_ctx* ctx) {
+  const int ndim = ctx->ndim;
+  // boundary-face overwrite maps (solver.py:526-580), canonical patch order
+  std::vector<int> order(ctx->patches.size());
+  for (size_t p = 0; p < order.size(); ++p) order[p] = (int)p;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    const HostPatch& a = ctx->patches[x];
+    const HostPatch& b = ctx->patches[y];
+    if (a.block != b.block) return a.block < b.block;
+    if (a.face != b.face) return a.face < b.face;
+    return std::lexicographical_compare(a.box, a.box + 6, b.box, b.box + 6);
+  });
+  for (auto& hb : ctx->blocks) {
+    for (int f = 0; f < 2 * ndim; ++f) {
+      const int ax = f / 2;
+      int ta = -1, tb = -1;
+      for (int a = 0; a < 3; ++a)
+        if (a != ax) (ta < 0 ? ta : tb) = a;
+      hb.bface_h[f].assign((size_t)hb.n[ta] * hb.n[tb], BFACE_NONE);
+    }
+  }
+  for (int p : order) {
+    const HostPatch& hp = ctx->patches[p];
+    unsigned char code;
+    if (hp.type == BC_SLIP || hp.type == BC_NOSLIP) code = BFACE_WALL;
+    else if (hp.type == BC_FARFIELD) code = BFACE_FARFIELD;
+    else continue;
+    HostBlock& hb = ctx->blocks[ctx->index_of[hp.block]];
+    const int ax = hp.face / 2;
+    int ta = -1, tb = -1;
+    for (int a = 0; a < 3; ++a)
+      if (a != ax) (ta < 0 ? ta : tb) = a;
+    for (int u1 = hp.box[2 * tb]; u1 < hp.box[2 * tb + 1]; ++u1)
+      for (int u0 = hp.box[2 * ta]; u0 < hp.box[2 * ta + 1]; ++u0)
+        hb.bface_h[hp.face][(size_t)u0 + (size_t)hb.n[ta] * u1] = code;
+  }
+  for (auto& hb : ctx->blocks) {
+    for (int f = 0; f < 2 * ndim; ++f) {
+      void* p = nullptr;
+      const size_t nb = std::max<size_t>(hb.bface_h[f].size(), 1);
+      CK(cudaMalloc(&p, nb));
+      CK(cudaMemcpy(p, hb.bface_h[f].data(), hb.bface_h[f].size(), cudaMemcpyHostToDevice));
+      hb.bface_d[f] = static_cast<unsigned char*>(p);
+      hb.dev.bface[f] = hb.bface_d[f];
+    }
+  }
+
+  // ghost tasks: physical patches (one item per tangential cell)
+  std::vector<GhostTask>& fill = ctx->h_tasks_fill;
+  std::vector<GhostTask>& unp = ctx->h_tasks_unpack;
+  fill.clear();
+  unp.clear();
+  for (int p : order) {
+    const HostPatch& hp = ctx->patches[p];
+    const int bi = ctx->index_of[hp.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    GhostTask t{};
+    t.kind = GK_BC;
+    t.bc_type = hp.type;
+    t.block = bi;
+    t.src_block = -1;
+    t.axis = hp.face / 2;
+    t.side = hp.face % 2;
+    int ta = -1, tb = -1;
+    for (int a = 0; a < 3; ++a)
+      if (a != t.axis) (ta < 0 ? ta : tb) = a;
+    t.ta = ta;
+    t.tb = tb;
+    t.tlo[0] = hp.box[2 * ta];
+    t.tn[0] = hp.box[2 * ta + 1] - hp.box[2 * ta];
+    t.tlo[1] = hp.box[2 * tb];
+    t.tn[1] = hp.box[2 * tb + 1] - hp.box[2 * tb];
+    t.depth = hb.g;
+    t.items = (long long)t.tn[0] * t.tn[1];
+    if (hp.type == BC_MMS) {
+      const size_t need = (size_t)t.depth * 6 * t.items;
+      if (hp.dirichlet.size() != need)
+        return fail(ctx, BF_EINVAL, "mms_dirichlet patch on block %d: got %zu values, need %zu",
+                    hp.block, hp.dirichlet.size(), need);
+      void* d = nullptr;
+      CK(cudaMalloc(&d, need * sizeof(double)));
+      CK(cudaMemcpy(d, hp.dirichlet.data(), need * sizeof(double), cudaMemcpyHostToDevice));
+      ctx->dirichlet_d.push_back(static_cast<double*>(d));
+      t.dirichlet = static_cast<double*>(d);
+    }
+    if (t.items > 0) fill.push_back(t);
+  }
+
+  // connected endpoints
+  for (auto& L : ctx->links) {
+    const int bi = ctx->index_of[L.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    const int ghost[3] = {hb.g, hb.g, ndim == 3 ? hb.g : 0};
+    int send[6], recv[6];
+    halo_boxes(L.face, L.box, hb.n, ghost, send, recv);
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = recv[2 * a + 1] - recv[2 * a];
+    int perm[3];
+    bool flip[3];
+    unpack_axes(L.face, L.amap, L.peer_face, perm, flip);
+    int P[3];
+    for (int a = 0; a < 3; ++a) P[perm[a]] = ext[a];
+    const long long own_st[3] = {1, hb.sy, hb.sz};
+    const int nf = (ndim == 3) ? 6 : 5;
+    const bool local = (L.peer_rank == ctx->rank) && ctx->index_of.count(L.peer_block);
+    GhostTask t{};
+    t.kind = GK_COPY;
+    t.nfields = nf;
+    for (int a = 0; a < 3; ++a) t.n[a] = ext[a];
+    t.items = (long long)ext[0] * ext[1] * ext[2];
+    t.block = bi;
+    t.dst_origin = hb.off(recv[0], recv[2], recv[4]);
+    for (int a = 0; a < 3; ++a) t.dst_stride[a] = own_st[a];
+    if (local) {
+      const int pi = ctx->index_of[L.peer_block];
+      const HostBlock& pb = ctx->blocks[pi];
+      const int pghost[3] = {pb.g, pb.g, ndim == 3 ? pb.g : 0};
+      int psend[6], precv[6];
+      halo_boxes(L.peer_face, L.peer_box, pb.n, pghost, psend, precv);
+      for (int a = 0; a < 3; ++a)
+        if (psend[2 * a + 1] - psend[2 * a] != P[a])
+          return fail(ctx, BF_EINVAL, "link tag %d: partner send box does not match", L.tag);
+      const long long pst[3] = {1, pb.sy, pb.sz};
+      t.src_block = pi;
+      t.src_origin = pb.off(psend[0], psend[2], psend[4]);
+      for (int a = 0; a < 3; ++a) {
+        const long long s = pst[perm[a]];
+        if (flip[a]) {
+          t.src_origin += (long long)(ext[a] - 1) * s;
+          t.src_stride[a] = -s;
+        } else {
+          t.src_stride[a] = s;
+        }
+      }
+      if (t.items > 0) fill.push_back(t);
+    } else {
+      // pack: own send box -> send buffer (i-fastest over the own send box)
+      L.cells = t.items;
+      L.nfields = nf;
+      int err = 0;
+      L.send = dalloc(ctx, (size_t)nf * std::max<long long>(L.cells, 1), &err);
+      if (err) return err;
+      L.recv = dalloc(ctx, (size_t)nf * std::max<long long>(L.cells, 1), &err);
+      if (err) return err;
+      GhostTask pk{};
+      pk.kind = GK_COPY;
+      pk.nfields = nf;
+      int sext[3];
+      for (int a = 0; a < 3; ++a) sext[a] = send[2 * a + 1] - send[2 * a];
+      for (int a = 0; a < 3; ++a) pk.n[a] = sext[a];
+      pk.items = (long long)sext[0] * sext[1] * sext[2];
+      pk.block = -1;
+      pk.dst_buf = L.send;
+      pk.buf_cells = L.cells;
+      pk.dst_origin = 0;
+      pk.dst_stride[0] = 1;
+      pk.dst_stride[1] = sext[0];
+      pk.dst_stride[2] = (long long)sext[0] * sext[1];
+      pk.src_block = bi;
+      pk.src_origin = hb.off(send[0], send[2], send[4]);
+      for (int a = 0; a < 3; ++a) pk.src_stride[a] = own_st[a];
+      if (pk.items > 0) fill.push_back(pk);
+      // unpack: recv buffer (partner send box, partner axis order) -> own ghosts
+      const long long Pst[3] = {1, P[0], (long long)P[0] * P[1]};
+      t.src_block = -1;
+      t.src_buf = L.recv;
+      t.buf_cells = L.cells;
+      t.src_origin = 0;
+      for (int a = 0; a < 3; ++a) {
+        const long long s = Pst[perm[a]];
+        if (flip[a]) {
+          t.src_origin += (long long)(ext[a] - 1) * s;
+          t.src_stride[a] = -s;
+        } else {
+          t.src_stride[a] = s;
+        }
+      }
+      if (t.items > 0) unp.push_back(t);
+    }
+  }
+  long long acc = 0;
+  for (auto& t : fill) {
+    t.begin = acc;
+    acc += t.items;
+  }
+  ctx->items_fill = acc;
+  acc = 0;
+  for (auto& t : unp) {
+    t.begin = acc;
+    acc += t.items;
+  }
+  ctx->items_unpack = acc;
+  ctx->n_fill = (int)fill.size();
+  ctx->n_unpack = (int)unp.size();
+  if (!fill.empty()) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, fill.size() * sizeof(GhostTask)));
+    CK(cudaMemcpy(p, fill.data(), fill.size() * sizeof(GhostTask), cudaMemcpyHostToDevice));
+    ctx->d_tasks_fill = static_cast<GhostTask*>(p);
+  }
+  if (!unp.empty()) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, unp.size() * sizeof(GhostTask)));
+    CK(cudaMemcpy(p, unp.data(), unp.size() * sizeof(GhostTask), cudaMemcpyHostToDevice));
+    ctx->d_tasks_unpack = static_cast<GhostTask*>(p);
+  }
+  return BF_OK;
+}
+
+int build_tiles(bf_ctx* ctx) {
+  std::vector<Tile> tiles;
+  std::vector<int> tb;
+  for (size_t bi = 0; bi < ctx->blocks.size(); ++bi) {
+    HostBlock& hb = ctx->blocks[bi];
+    hb.tile_begin = (int)tiles.size();
+    tb.push_back(hb.tile_begin);
+    const int kc = ctx->ndim == 3 ? ctx->kc : 1;
+    const int nk = ctx->ndim == 3 ? hb.n[2] : 1;
+    for (int k0 = 0; k0 < nk; k0 += kc)
+      for (int j0 = 0; j0 < hb.n[1]; j0 += TJ)
+        for (int i0 = 0; i0 < hb.n[0]; i0 += TI)
+          tiles.push_back(Tile{(int)bi, i0, j0, k0, std::min(kc, nk - k0)});
+    hb.tile_end = (int)tiles.size();
+  }
+  tb.push_back((int)tiles.size());
+  ctx->ntiles = (int)tiles.size();
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(tiles.size(), 1) * sizeof(Tile)));
+  CK(cudaMemcpy(p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+  ctx->d_tiles = static_cast<Tile*>(p);
+  CK(cudaMalloc(&p, tb.size() * sizeof(int)));
+  CK(cudaMemcpy(p, tb.data(), tb.size() * sizeof(int), cudaMemcpyHostToDevice));
+  ctx->d_tile_begin = static_cast<int*>(p);
+  return BF_OK;
+}
+
+// ---- per-stage sequencing ------------------------------------------------------
+
+GhostArgs ghost_args(bf_ctx* ctx, bool unpack) {
+  GhostArgs g{};
+  g.blocks = ctx->d_blocks;
+  g.tasks = unpack ? ctx->d_tasks_unpack : ctx->d_tasks_fill;
+  g.ntasks = unpack ? ctx->n_unpack : ctx->n_fill;
+  g.total_items = unpack ? ctx->items_unpack : ctx->items_fill;
+  g.cur = ctx->cur;
+  g.t_derived = ctx->t_derived;
+  g.c = ctx->c;
+  return g;
+}
+
+int launch_fill(bf_ctx* ctx) {
+  ProfScope ps(ctx, 1);
+  CK(ghost_fn(ctx)(ghost_args(ctx, false), ctx->stream));
+  return BF_OK;
+}
+
+int launch_unpack(bf_ctx* ctx) {
+  ProfScope ps(ctx, 2);
+  CK(ghost_fn(ctx)(ghost_args(ctx, true), ctx->stream));
+  return BF_OK;
+}
+
+std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx) {
+  std::vector<HostLink*> out;
+  for (auto& L : ctx->links)
+    if (L.send) out.push_back(&L);
+  std::sort(out.begin(), out.end(), [](const HostLink* a, const HostLink* b) {
+    if (a->peer_rank != b->peer_rank) return a->peer_rank < b->peer_rank;
+    if (a->tag != b->tag) return a->tag < b->tag;
+    return a->block < b->block;
+  });
+  return out;
+}
+
+int nccl_exchange(bf_ctx* ctx) {
+  auto rl = remote_links_sorted(ctx);
+  if (rl.empty()) return BF_OK;
+  NK(ncclGroupStart());
+  for (HostLink* L : rl) {
+    const size_t cnt = (size_t)L->nfields * L->cells;
+    NK(ncclSend(L->send, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    NK(ncclRecv(L->recv, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+  }
+  NK(ncclGroupEnd());
+  return BF_OK;
+}
+
+// ghosts of W[cur] for a standalone / NCCL ctx
+int ghosts_solo(bf_ctx* ctx) {
+  int rc = launch_fill(ctx);
+  if (rc) return rc;
+  if (ctx->n_unpack) {
+    if (!ctx->comm)
+      return fail(ctx, BF_EINVAL,
+                  "rank %d has remote links but no communicator (bf_nccl_init or bf_group)",
+                  ctx->rank);
+    rc = nccl_exchange(ctx);
+    if (rc) return rc;
+    rc = launch_unpack(ctx);
+    if (rc) return rc;
+  }
+  ctx->ghost_buf = ctx->cur;
+  return BF_OK;
+}
+
+int stage_flags(bf_ctx* ctx, int step_index, int k, int nst) {
+  int flags = 0;
+  if (k == 0) flags |= F_STAGE0;
+  if (k == nst - 1) flags |= F_LAST;
+  if (ctx->blocks.size() && ctx->blocks[0].has_src) flags |= F_SOURCE;
+  const int fz = ctx->sch.limiter_freeze_at;
+  if (fz > 0) {
+    const bool frozen = step_index > fz;
+    if (frozen) {
+      if (ctx->psi_valid) flags |= F_PSI_LOAD;
+      else flags |= F_PSI_STORE;   // first frozen evaluation computes and keeps them
+    } else if (k == nst - 1) {
+      flags |= F_PSI_STORE;        // psi of the last stage is what a freeze pins
+    }
+  }
+  return flags;
+}
+
+int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
+  StageArgs a{};
+  a.blocks = ctx->d_blocks;
+  a.tiles = ctx->d_tiles;
+  a.ntiles = ctx->ntiles;
+  a.cur = ctx->cur;
+  a.stage = k;
+  a.flags = flags;
+  a.alpha = alpha;
+  a.partial = ctx->d_partial;
+  a.err = ctx->d_err;
+  a.c = ctx->c;
+  {
+    ProfScope ps(ctx, 0);
+    CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
+  }
+  if (flags & F_STAGE0) {
+    ProfScope ps(ctx, 3);
+    auto red = ctx->sch.precision == BF_PRECISION_EXACT ? bf_exact::launch_reduce
+                                                        : bf_fast::launch_reduce;
+    CK(red(ctx->d_partial, ctx->d_tile_begin, (int)ctx->blocks.size(), ctx->d_blocksum,
+           ctx->stream));
+  }
+  if (flags & (F_PSI_STORE | F_PSI_LOAD)) ctx->psi_valid = true;
+  ctx->cur ^= 1;
+  ctx->t_derived = 1;
+  return BF_OK;
+}
+
+double rk_alpha(int nst, int k) {
+  static const double a1[1] = {1.0};
+  static const double a2[2] = {0.5, 1.0};
+  static const double a4[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+  return nst == 1 ? a1[k] : (nst == 2 ? a2[k] : a4[k]);
+}
+
+// Decode the error key into the reference's numbering.
+void decode_error(bf_ctx* ctx, unsigned long long key) {
+  const int stage = (int)(key >> 61) & 7;
+  const int phase = (int)(key >> 60) & 1;
+  const int order = (int)(key >> 48) & 0xFFF;
+  const int dir = (int)(key >> 46) & 3;
+  const int kind = (int)(key >> 44) & 3;
+  const unsigned long long lin = key & ((1ull << 44) - 1);
+  const HostBlock& hb = ctx->blocks[order];
+  long long sh[3] = {hb.n[0], hb.n[1], hb.n[2]};
+  if (phase == 0) sh[dir] += 1;
+  ctx->e_kind = phase ? BF_ERR_UPDATE : kind;
+  ctx->e_block = hb.id;
+  ctx->e_stage = stage;
+  ctx->e_dir = dir;
+  ctx->e_idx[2] = (long long)(lin % sh[2]);
+  ctx->e_idx[1] = (long long)((lin / sh[2]) % sh[1]);
+  ctx->e_idx[0] = (long long)(lin / sh[2] / sh[1]);
+  ctx->msg = "non-physical state";
+}
+
+// Host copy of the per-block sums and the error key after a step.
+int collect(bf_ctx* ctx, double* sumsq_out, unsigned long long* key_out) {
+  const int nb = (int)ctx->blocks.size();
+  CK(cudaMemcpyAsync(ctx->h_pinned, ctx->d_blocksum, sizeof(double) * 5 * nb,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_pinned + 5 * nb, ctx->d_err, sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->profiling) drain_profile(ctx);
+  double s[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b)
+    for (int v = 0; v < 5; ++v) s[v] = s[v] + ctx->h_pinned[5 * b + v];   // id order
+  for (int v = 0; v < 5; ++v) sumsq_out[v] = s[v];
+  unsigned long long key;
+  std::memcpy(&key, ctx->h_pinned + 5 * nb, sizeof key);
+  *key_out = key;
+  return BF_OK;
+}
+
+int reset_error(bf_ctx* ctx) {
+  CK(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), ctx->stream));
+  return BF_OK;
+}
+
+int rank_allgather(bf_ctx* ctx, double* sumsq, unsigned long long* key, int* bad_rank) {
+  // pack [5 sums, key bits] on the host side record, then allgather through NCCL
+  double rec[6];
+  for (int v = 0; v < 5; ++v) rec[v] = sumsq[v];
+  std::memcpy(&rec[5], key, sizeof(double));
+  CK(cudaMemcpyAsync(ctx->d_rank6, rec, sizeof rec, cudaMemcpyHostToDevice, ctx->stream));
+  NK(ncclAllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
+  std::vector<double> all((size_t)6 * ctx->nranks);
+  CK(cudaMemcpyAsync(all.data(), ctx->d_gather, sizeof(double) * all.size(),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot[5];
+  for (int r = 0; r < ctx->nranks; ++r) {
+    for (int v = 0; v < 5; ++v) tot[v] = (r == 0) ? all[6 * r + v] : tot[v] + all[6 * r + v];
+  }
+  for (int v = 0; v < 5; ++v) sumsq[v] = tot[v];
+  *bad_rank = -1;
+  for (int r = 0; r < ctx->nranks; ++r) {
+    unsigned long long k;
+    std::memcpy(&k, &all[6 * r + 5], sizeof k);
+    if (k != NO_ERROR && *bad_rank < 0) *bad_rank = r;
+  }
+  return BF_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+int bf_api_version(void) { return BF_API_VERSION; }
+
+bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf_freestream* fs,
+                  int device, int rank, int nranks) {
+  if ((ndim != 2 && ndim != 3) || !gas || !scheme || !fs || nranks < 1 || rank < 0 ||
+      rank >= nranks)
+    return nullptr;
+  auto* ctx = new bf_ctx();
+  ctx->ndim = ndim;
+  ctx->gas = *gas;
+  ctx->sch = *scheme;
+  ctx->fs = *fs;
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  if (const char* e = std::getenv("BF_KC")) ctx->kc = std::max(1, std::atoi(e));
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
+                                                                        cudaStreamNonBlocking) !=
+                                                  cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  ctx->stream = ctx->own_stream;
+  // constants, in the reference's scalar evaluation order (python floats)
+  Consts& c = ctx->c;
+  const double g = gas->gamma;
+  c.gamma = g;
+  c.gm1 = g - 1.0;
+  c.gog1 = g / (g - 1.0);
+  c.R = gas->R;
+  c.cfl = scheme->cfl;
+  c.quarter = scheme->epsilon / 4.0;
+  c.omk = 1.0 - scheme->kappa;
+  c.opk = 1.0 + scheme->kappa;
+  c.efix = scheme->entropy_fix_coeff;
+  c.fs_rho = fs->rho;
+  c.fs_u = fs->u;
+  c.fs_v = fs->v;
+  c.fs_w = fs->w;
+  c.fs_p = fs->p;
+  c.fs_T = fs->T;
+  c.ff_af = std::sqrt(g * fs->p / fs->rho);
+  c.ff_two_af_gm1 = 2.0 * c.ff_af / (g - 1.0);
+  c.ff_sf = fs->p / std::pow(fs->rho, g);
+  c.ff_qgm1 = 0.25 * (g - 1.0);
+  c.ff_exp = 1.0 / (g - 1.0);
+  c.two_over_gm1 = 2.0 / (g - 1.0);
+  c.vl_c = 2.0 * (g * g - 1.0);
+  c.tw = scheme->wall_temperature;
+  c.has_tw = scheme->has_wall_temperature;
+  c.eps0 = scheme->epsilon == 0.0;
+  return ctx;
+}
+
+void bf_destroy(bf_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& hb : ctx->blocks) {
+    for (double* p : hb.owned) cudaFree(p);
+    for (int f = 0; f < 6; ++f)
+      if (hb.bface_d[f]) cudaFree(hb.bface_d[f]);
+  }
+  for (auto& L : ctx->links) {
+    if (L.send) cudaFree(L.send);
+    if (L.recv) cudaFree(L.recv);
+  }
+  for (double* p : ctx->dirichlet_d) cudaFree(p);
+  cudaFree(ctx->d_blocks);
+  cudaFree(ctx->d_tiles);
+  cudaFree(ctx->d_tile_begin);
+  cudaFree(ctx->d_tasks_fill);
+  cudaFree(ctx->d_tasks_unpack);
+  cudaFree(ctx->d_partial);
+  cudaFree(ctx->d_blocksum);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_rank6);
+  cudaFree(ctx->d_gather);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+int bf_last_error(const bf_ctx* ctx, char* buf, size_t n) {
+  if (!ctx || !buf || n == 0) return BF_EINVAL;
+  std::snprintf(buf, n, "%s", ctx->msg.c_str());
+  return BF_OK;
+}
+
+int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
+                 const double* const* face_vectors, const double* volume,
+                 const double* const* source) {
+  if (!ctx) return BF_EINVAL;
+  if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_add_block after bf_finalize");
+  if (ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "duplicate block %d", block_id);
+  if (ghost_depth < 2) return fail(ctx, BF_EINVAL, "ghost_depth must be >= 2");
+  const int ndim = ctx->ndim;
+  if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || (ndim == 2 && dims[2] != 1))
+    return fail(ctx, BF_EINVAL, "bad dims (%d,%d,%d)", dims[0], dims[1], dims[2]);
+  CK(cudaSetDevice(ctx->device));
+  HostBlock hb;
+  hb.id = block_id;
+  for (int a = 0; a < 3; ++a) hb.n[a] = dims[a];
+  hb.g = ghost_depth;
+  hb.gk = ndim == 3 ? ghost_depth : 0;
+  const int gg[3] = {hb.g, hb.g, hb.gk};
+  for (int a = 0; a < 3; ++a) hb.P[a] = hb.n[a] + 2 * gg[a];
+  hb.lead = (4 - hb.g % 4) % 4;
+  hb.sy = ((hb.lead + hb.P[0] + 3) / 4) * 4;
+  hb.sz = hb.sy * hb.P[1];
+  hb.fsz = ((hb.sz * hb.P[2] + 63) / 64) * 64;
+  hb.origin = hb.lead + hb.g + hb.sy * hb.g + hb.sz * hb.gk;
+  hb.has_src = source != nullptr;
+  const bool want_psi = ctx->sch.limiter_freeze_at > 0;
+  // arena: W 2x6, Q 5, dtv, vol, fn ndim x 4, src 5, psi ndim x 10
+  const int nfield = 12 + 5 + 2 + 4 * ndim + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0);
+  int err = 0;
+  hb.arena = dalloc(ctx, (size_t)nfield * hb.fsz, &err);
+  if (err) return err;
+  hb.owned.push_back(hb.arena);
+  CK(cudaMemset(hb.arena, 0, sizeof(double) * (size_t)nfield * hb.fsz));
+  int slot = 0;
+  auto next = [&]() { return hb.arena + (size_t)(slot++) * hb.fsz + hb.origin; };
+  DevBlock& d = hb.dev;
+  for (int a = 0; a < 3; ++a) d.n[a] = hb.n[a];
+  d.g = hb.g;
+  d.ndim = ndim;
+  d.id = block_id;
+  d.sy = hb.sy;
+  d.sz = hb.sz;
+  for (int b = 0; b < 2; ++b)
+    for (int f = 0; f < 6; ++f) d.W[b][f] = next();
+  for (int e = 0; e < 5; ++e) d.Q[e] = next();
+  d.dtv = next();
+  d.vol = next();
+  for (int dd = 0; dd < ndim; ++dd)
+    for (int cc = 0; cc < 4; ++cc) d.fn[dd][cc] = next();
+  if (hb.has_src)
+    for (int e = 0; e < 5; ++e) d.src[e] = next();
+  if (want_psi)
+    for (int dd = 0; dd < ndim; ++dd)
+      for (int pm = 0; pm < 2; ++pm)
+        for (int v = 0; v < 5; ++v) d.psi[dd][pm][v] = next();
+  ctx->have_psi = want_psi;
+
+  // face unit normals and areas (solver.py:212-220), interior tangential
+  std::vector<double> host((size_t)hb.fsz);
+  for (int dd = 0; dd < ndim; ++dd) {
+    const double* sv[3] = {face_vectors[3 * dd], face_vectors[3 * dd + 1],
+                           face_vectors[3 * dd + 2]};
+    // input shape: (N_d+1 along d, padded along the others), Fortran
+    long long in_shape[3];
+    for (int a = 0; a < 3; ++a) in_shape[a] = (a == dd) ? hb.n[a] + 1 : hb.P[a];
+    std::vector<double> out[4];
+    for (auto& o : out) o.assign((size_t)hb.fsz, 0.0);
+    long long ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+    for (long long k = 0; k < ext[2]; ++k)
+      for (long long j = 0; j < ext[1]; ++j)
+        for (long long i = 0; i < ext[0]; ++i) {
+          const long long ii = (dd == 0) ? i : i + gg[0];
+          const long long jj = (dd == 1) ? j : j + gg[1];
+          const long long kk = (dd == 2) ? k : k + gg[2];
+          const long long src = ii + in_shape[0] * (jj + in_shape[1] * kk);
+          const double x = sv[0][src], y = sv[1][src], z = sv[2][src];
+          const double A = std::sqrt((x * x + y * y) + z * z);
+          const long long dst = hb.origin + hb.off((int)i, (int)j, (int)k);
+          out[0][dst] = A > 0.0 ? x / A : 0.0;
+          out[1][dst] = A > 0.0 ? y / A : 0.0;
+          out[2][dst] = A > 0.0 ? z / A : 0.0;
+          out[3][dst] = A;
+        }
+    for (int cc = 0; cc < 4; ++cc)
+      CK(cudaMemcpy(d.fn[dd][cc] - hb.origin, out[cc].data(), sizeof(double) * hb.fsz,
+                    cudaMemcpyHostToDevice));
+  }
+  // volume + sources: interior Fortran (n0, n1, n2)
+  auto put_interior = [&](double* dptr, const double* src) -> int {
+    std::fill(host.begin(), host.end(), 0.0);
+    for (long long k = 0; k < hb.n[2]; ++k)
+      for (long long j = 0; j < hb.n[1]; ++j)
+        for (long long i = 0; i < hb.n[0]; ++i)
+          host[hb.origin + hb.off((int)i, (int)j, (int)k)] =
+              src[i + (long long)hb.n[0] * (j + (long long)hb.n[1] * k)];
+    CK(cudaMemcpy(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
+                  cudaMemcpyHostToDevice));
+    return BF_OK;
+  };
+  int rc = put_interior(d.vol, volume);
+  if (rc) return rc;
+  if (hb.has_src)
+    for (int e = 0; e < 5; ++e) {
+      rc = put_interior(d.src[e], source[e]);
+      if (rc) return rc;
+    }
+  d.order = (int)ctx->blocks.size();
+  ctx->index_of[block_id] = (int)ctx->blocks.size();
+  ctx->blocks.push_back(std::move(hb));
+  return BF_OK;
+}
+
+int bf_add_bc_patch(bf_ctx* ctx, int block_id, int bc_type, int face, const int box[6],
+                    const double* dirichlet) {
+  if (!ctx) return BF_EINVAL;
+  if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_add_bc_patch after bf_finalize");
+  if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
+  if (bc_type < 0 || bc_type > BC_MMS)
+    return fail(ctx, BF_EINVAL, "unknown physical bc type %d", bc_type);
+  if (face < 0 || face >= 2 * ctx->ndim) return fail(ctx, BF_EINVAL, "bad face %d", face);
+  HostPatch p;
+  p.block = block_id;
+  p.type = bc_type;
+  p.face = face;
+  std::memcpy(p.box, box, sizeof p.box);
+  const HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
+  for (int a = 0; a < 3; ++a)
+    if (box[2 * a] < 0 || box[2 * a + 1] > hb.n[a] || box[2 * a] >= box[2 * a + 1])
+      return fail(ctx, BF_EINVAL, "patch box outside block %d", block_id);
+  if (bc_type == BC_MMS) {
+    if (!dirichlet) return fail(ctx, BF_EINVAL, "mms_dirichlet patch needs ghost values");
+    const int ax = face / 2;
+    long long nt = 1;
+    for (int a = 0; a < 3; ++a)
+      if (a != ax) nt *= box[2 * a + 1] - box[2 * a];
+    p.dirichlet.assign(dirichlet, dirichlet + (size_t)hb.g * 6 * nt);
+  }
+  ctx->patches.push_back(std::move(p));
+  return BF_OK;
+}
+
+int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int axis_map[6],
+                int peer_block, int peer_face, const int peer_box[6], int peer_rank, int tag) {
+  if (!ctx) return BF_EINVAL;
+  if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_add_link after bf_finalize");
+  if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
+  if (peer_rank < 0 || peer_rank >= ctx->nranks)
+    return fail(ctx, BF_EINVAL, "peer rank %d out of range", peer_rank);
+  HostLink L;
+  L.block = block_id;
+  L.face = face;
+  std::memcpy(L.box, box, sizeof L.box);
+  std::memcpy(L.amap, axis_map, sizeof L.amap);
+  L.peer_block = peer_block;
+  L.peer_face = peer_face;
+  std::memcpy(L.peer_box, peer_box, sizeof L.peer_box);
+  L.peer_rank = peer_rank;
+  L.tag = tag;
+  bool seen[3] = {false, false, false};
+  for (int a = 0; a < 3; ++a) {
+    if (axis_map[2 * a] < 0 || axis_map[2 * a] > 2 || seen[axis_map[2 * a]])
+      return fail(ctx, BF_EINVAL, "orientation map is not a bijection");
+    seen[axis_map[2 * a]] = true;
+  }
+  ctx->links.push_back(L);
+  return BF_OK;
+}
+
+int bf_finalize(bf_ctx* ctx) {
+  if (!ctx) return BF_EINVAL;
+  if (ctx->finalized) return BF_OK;
+  CK(cudaSetDevice(ctx->device));
+  int rc = build_tables(ctx);
+  if (rc) return rc;
+  rc = build_tiles(ctx);
+  if (rc) return rc;
+  std::vector<DevBlock> devs;
+  for (auto& hb : ctx->blocks) devs.push_back(hb.dev);
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(devs.size(), 1) * sizeof(DevBlock)));
+  CK(cudaMemcpy(p, devs.data(), devs.size() * sizeof(DevBlock), cudaMemcpyHostToDevice));
+  ctx->d_blocks = static_cast<DevBlock*>(p);
+  CK(cudaMalloc(&p, sizeof(double) * 5 * std::max(ctx->ntiles, 1)));
+  ctx->d_partial = static_cast<double*>(p);
+  CK(cudaMalloc(&p, sizeof(double) * 5 * std::max<size_t>(ctx->blocks.size(), 1)));
+  ctx->d_blocksum = static_cast<double*>(p);
+  CK(cudaMalloc(&p, sizeof(unsigned long long)));
+  ctx->d_err = static_cast<unsigned long long*>(p);
+  CK(cudaMemset(ctx->d_err, 0xFF, sizeof(unsigned long long)));
+  CK(cudaMalloc(&p, sizeof(double) * 6));
+  ctx->d_rank6 = static_cast<double*>(p);
+  CK(cudaMalloc(&p, sizeof(double) * 6 * ctx->nranks));
+  ctx->d_gather = static_cast<double*>(p);
+  CK(cudaMallocHost(&p, sizeof(double) * (5 * ctx->blocks.size() + 2)));
+  ctx->h_pinned = static_cast<double*>(p);
+  ctx->finalized = true;
+  return BF_OK;
+}
+
+int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
+                     const double* const* q5) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_upload_fields before bf_finalize");
+  if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
+  CK(cudaSetDevice(ctx->device));
+  HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
+  std::vector<double> host((size_t)hb.fsz, 0.0);
+  auto put = [&](double* dptr, const double* src) -> int {
+    for (long long k = 0; k < hb.P[2]; ++k)
+      for (long long j = 0; j < hb.P[1]; ++j) {
+        const double* row = src + (size_t)hb.P[0] * (j + (long long)hb.P[1] * k);
+        double* dst = host.data() + hb.lead + hb.sy * j + hb.sz * k;
+        std::memcpy(dst, row, sizeof(double) * hb.P[0]);
+      }
+    CK(cudaMemcpyAsync(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->bytes_h2d += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
+    return BF_OK;
+  };
+  for (int f = 0; f < 6; ++f) {
+    int rc = put(hb.dev.W[0][f], fields6[f]);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(hb.dev.W[1][f] - hb.origin, hb.dev.W[0][f] - hb.origin,
+                       sizeof(double) * hb.fsz, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  for (int e = 0; e < 5; ++e) {
+    int rc = put(hb.dev.Q[e], q5[e]);
+    if (rc) return rc;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->cur = 0;
+  ctx->ghost_buf = 0;
+  ctx->t_derived = 0;
+  ctx->psi_valid = false;
+  return BF_OK;
+}
+
+int bf_update_ghosts(bf_ctx* ctx) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_update_ghosts before bf_finalize");
+  CK(cudaSetDevice(ctx->device));
+  int rc = ghosts_solo(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BF_OK;
+}
+
+int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_out) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_step before bf_finalize");
+  CK(cudaSetDevice(ctx->device));
+  const int nst = ctx->sch.rk_stages;
+  int rc = reset_error(ctx);
+  if (rc) return rc;
+  for (int k = 0; k < nst; ++k) {
+    rc = ghosts_solo(ctx);
+    if (rc) return rc;
+    rc = launch_stage_kernel(ctx, k, stage_flags(ctx, step_index, k, nst), rk_alpha(nst, k));
+    if (rc) return rc;
+  }
+  double s[5];
+  unsigned long long key;
+  rc = collect(ctx, s, &key);
+  if (rc) return rc;
+  if (ctx->comm && ctx->nranks > 1) {
+    int bad = -1;
+    rc = rank_allgather(ctx, s, &key, &bad);
+    if (rc) return rc;
+    if (bad >= 0 && key == NO_ERROR)
+      return fail(ctx, BF_ENONPHYSICAL, "rank %d: non-physical state", bad);
+  }
+  if (key != NO_ERROR) {
+    decode_error(ctx, key);
+    return BF_ENONPHYSICAL;
+  }
+  for (int v = 0; v < 5; ++v) sumsq_out[v] = s[v];
+  if (ncells_out) {
+    long long n = 0;
+    for (auto& hb : ctx->blocks) n += hb.cells();
+    *ncells_out = n;
+  }
+  return BF_OK;
+}
+
+int bf_run(bf_ctx* ctx, int first_step, int nsteps, double* hist_out, int* steps_done) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_run before bf_finalize");
+  *steps_done = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    double ss[5];
+    int rc = bf_step(ctx, first_step + s, ss, nullptr);
+    if (rc) return rc;
+    for (int v = 0; v < 5; ++v) hist_out[5 * s + v] = std::sqrt(ss[v]);
+    *steps_done = s + 1;
+  }
+  return BF_OK;
+}
+
+int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_download before bf_finalize");
+  if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
+  std::vector<double> a((size_t)hb.fsz), b((size_t)hb.fsz);
+  auto get = [&](const double* dptr, std::vector<double>& h) -> int {
+    CK(cudaMemcpy(h.data(), dptr - hb.origin, sizeof(double) * hb.fsz, cudaMemcpyDeviceToHost));
+    return BF_OK;
+  };
+  auto at = [&](long long i, long long j, long long k) {   // padded coords
+    return hb.lead + i + hb.sy * j + hb.sz * k;
+  };
+  const int gg[3] = {hb.g, hb.g, hb.gk};
+  auto interior = [&](long long i, long long j, long long k) {
+    return i >= gg[0] && i < gg[0] + hb.n[0] && j >= gg[1] && j < gg[1] + hb.n[1] &&
+           k >= gg[2] && k < gg[2] + hb.n[2];
+  };
+  int rc;
+  if (what >= BF_FIELD_RHO && what <= BF_FIELD_T) {
+    rc = get(hb.dev.W[ctx->cur][what], a);
+    if (rc) return rc;
+    rc = get(hb.dev.W[ctx->ghost_buf][what], b);
+    if (rc) return rc;
+    std::vector<double> rho, p;
+    if (what == BF_FIELD_T && ctx->t_derived) {
+      rho.resize(hb.fsz);
+      p.resize(hb.fsz);
+      rc = get(hb.dev.W[ctx->cur][0], rho);
+      if (rc) return rc;
+      rc = get(hb.dev.W[ctx->cur][4], p);
+      if (rc) return rc;
+    }
+    for (long long k = 0; k < hb.P[2]; ++k)
+      for (long long j = 0; j < hb.P[1]; ++j)
+        for (long long i = 0; i < hb.P[0]; ++i) {
+          const long long s = at(i, j, k);
+          double v;
+          if (interior(i, j, k)) {
+            v = (what == BF_FIELD_T && ctx->t_derived) ? p[s] / (rho[s] * ctx->gas.R) : a[s];
+          } else {
+            v = b[s];
+          }
+          out[i + hb.P[0] * (j + (long long)hb.P[1] * k)] = v;
+        }
+    ctx->bytes_d2h += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
+    return BF_OK;
+  }
+  if (what >= BF_FIELD_Q0 && what <= BF_FIELD_Q0 + 4) {
+    rc = get(hb.dev.Q[what - BF_FIELD_Q0], a);
+    if (rc) return rc;
+    for (long long k = 0; k < hb.P[2]; ++k)
+      for (long long j = 0; j < hb.P[1]; ++j)
+        for (long long i = 0; i < hb.P[0]; ++i)
+          out[i + hb.P[0] * (j + (long long)hb.P[1] * k)] = a[at(i, j, k)];
+    ctx->bytes_d2h += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
+    return BF_OK;
+  }
+  if (what == BF_FIELD_DTV) {
+    rc = get(hb.dev.dtv, a);
+    if (rc) return rc;
+    for (long long k = 0; k < hb.n[2]; ++k)
+      for (long long j = 0; j < hb.n[1]; ++j)
+        for (long long i = 0; i < hb.n[0]; ++i)
+          out[i + hb.n[0] * (j + (long long)hb.n[1] * k)] =
+              a[hb.origin + hb.off((int)i, (int)j, (int)k)];
+    return BF_OK;
+  }
+  if (what >= BF_FIELD_PSI && what < BF_FIELD_PSI + 10 * ctx->ndim) {
+    if (!ctx->have_psi) return fail(ctx, BF_EINVAL, "limiter arrays are kept only when freezing");
+    const int r = what - BF_FIELD_PSI;
+    const int d = r / 10, pm = (r % 10) / 5, v = r % 5;
+    rc = get(hb.dev.psi[d][pm][v], a);
+    if (rc) return rc;
+    long long ext[3] = {hb.n[0], hb.n[1], hb.n[2]};
+    ext[d] += 2;
+    for (long long k = 0; k < ext[2]; ++k)
+      for (long long j = 0; j < ext[1]; ++j)
+        for (long long i = 0; i < ext[0]; ++i) {
+          long long c[3] = {i, j, k};
+          c[d] -= 1;
+          out[i + ext[0] * (j + ext[1] * k)] = a[hb.origin + hb.off((int)c[0], (int)c[1], (int)c[2])];
+        }
+    return BF_OK;
+  }
+  return fail(ctx, BF_EINVAL, "unknown field selector %d", what);
+}
+
+int bf_error_info(const bf_ctx* ctx, int* kind, int* block_id, int* stage, int* direction,
+                  long long index[3]) {
+  if (!ctx) return BF_EINVAL;
+  *kind = ctx->e_kind;
+  *block_id = ctx->e_block;
+  *stage = ctx->e_stage;
+  *direction = ctx->e_dir;
+  for (int a = 0; a < 3; ++a) index[a] = ctx->e_idx[a];
+  return BF_OK;
+}
+
+int bf_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return BF_ENCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return BF_OK;
+}
+
+int bf_nccl_init(bf_ctx* ctx, const void* id128) {
+  if (!ctx) return BF_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  NK(ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
+  return BF_OK;
+}
+
+// ---- in-process groups --------------------------------------------------------
+
+bf_group* bf_group_create(bf_ctx* const* ctxs, int n) {
+  if (!ctxs || n < 1) return nullptr;
+  auto* g = new bf_group();
+  g->ctxs.assign(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    bf_ctx* c = ctxs[i];
+    if (!c || c->rank < 0 || c->rank >= n || g->ctxs[c->rank] || !c->finalized) {
+      delete g;
+      return nullptr;
+    }
+    g->ctxs[c->rank] = c;
+  }
+  for (bf_ctx* c : g->ctxs) {
+    cudaSetDevice(c->device);
+    for (bf_ctx* o : g->ctxs)
+      if (o->device != c->device) cudaDeviceEnablePeerAccess(o->device, 0);
+    cudaGetLastError();   // already-enabled is fine
+    cudaEvent_t a, b;
+    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    g->ev_packed.push_back(a);
+    g->ev_unpacked.push_back(b);
+    c->group = g;
+  }
+  return g;
+}
+
+void bf_group_destroy(bf_group* g) {
+  if (!g) return;
+  for (size_t i = 0; i < g->ctxs.size(); ++i) {
+    cudaSetDevice(g->ctxs[i]->device);
+    cudaEventDestroy(g->ev_packed[i]);
+    cudaEventDestroy(g->ev_unpacked[i]);
+    g->ctxs[i]->group = nullptr;
+  }
+  delete g;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One ghost update of every member: fill+pack on each, push messages into the
+// peers' receive buffers, then unpack on each (lock step from one host thread).
+int group_ghosts(bf_group* g) {
+  const int n = (int)g->ctxs.size();
+  for (int r = 0; r < n; ++r) {
+    bf_ctx* ctx = g->ctxs[r];
+    CK(cudaSetDevice(ctx->device));
+    if (!g->first) {
+      // do not overwrite a peer's receive buffers before it consumed them
+      for (int q = 0; q < n; ++q)
+        if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
+    }
+    int rc = launch_fill(ctx);
+    if (rc) return rc;
+    for (auto& L : ctx->links) {
+      if (!L.send) continue;
+      bf_ctx* peer = g->ctxs[L.peer_rank];
+      HostLink* match = nullptr;
+      for (auto& M : peer->links)
+        if (M.send && M.tag == L.tag && M.peer_rank == ctx->rank && M.block == L.peer_block) {
+          match = &M;
+          break;
+        }
+      if (!match) return fail(ctx, BF_EINVAL, "link tag %d has no partner on rank %d", L.tag,
+                              L.peer_rank);
+      CK(cudaMemcpyAsync(match->recv, L.send, sizeof(double) * L.nfields * L.cells,
+                         cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaEventRecord(g->ev_packed[r], ctx->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bf_ctx* ctx = g->ctxs[r];
+    CK(cudaSetDevice(ctx->device));
+    for (int q = 0; q < n; ++q)
+      if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_packed[q], 0));
+    if (ctx->n_unpack) {
+      int rc = launch_unpack(ctx);
+      if (rc) return rc;
+    }
+    CK(cudaEventRecord(g->ev_unpacked[r], ctx->stream));
+    ctx->ghost_buf = ctx->cur;
+  }
+  g->first = false;
+  return BF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bf_group_update_ghosts(bf_group* g) {
+  if (!g) return BF_EINVAL;
+  int rc = group_ghosts(g);
+  if (rc) return rc;
+  for (bf_ctx* ctx : g->ctxs) {
+    cudaSetDevice(ctx->device);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return BF_ECUDA;
+  }
+  return BF_OK;
+}
+
+int bf_group_step(bf_group* g, int step_index, double* sumsq_out, int* failed_rank) {
+  if (!g) return BF_EINVAL;
+  *failed_rank = -1;
+  const int n = (int)g->ctxs.size();
+  const int nst = g->ctxs[0]->sch.rk_stages;
+  for (bf_ctx* ctx : g->ctxs) {
+    cudaSetDevice(ctx->device);
+    int rc = reset_error(ctx);
+    if (rc) {
+      *failed_rank = ctx->rank;
+      return rc;
+    }
+  }
+  for (int k = 0; k < nst; ++k) {
+    int rc = group_ghosts(g);
+    if (rc) return rc;
+    for (bf_ctx* ctx : g->ctxs) {
+      cudaSetDevice(ctx->device);
+      rc = launch_stage_kernel(ctx, k, stage_flags(ctx, step_index, k, nst), rk_alpha(nst, k));
+      if (rc) {
+        *failed_rank = ctx->rank;
+        return rc;
+      }
+    }
+  }
+  double tot[5] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < n; ++r) {
+    bf_ctx* ctx = g->ctxs[r];
+    cudaSetDevice(ctx->device);
+    double s[5];
+    unsigned long long key;
+    int rc = collect(ctx, s, &key);
+    if (rc) {
+      *failed_rank = r;
+      return rc;
+    }
+    if (key != NO_ERROR) {
+      decode_error(ctx, key);
+      *failed_rank = r;
+      return BF_ENONPHYSICAL;
+    }
+    for (int v = 0; v < 5; ++v) tot[v] = (r == 0) ? s[v] : tot[v] + s[v];
+  }
+  for (int v = 0; v < 5; ++v) sumsq_out[v] = tot[v];
+  return BF_OK;
+}
+
+int bf_set_stream(bf_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return BF_EINVAL;
+  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  return BF_OK;
+}
+
+int bf_set_profiling(bf_ctx* ctx, int on) {
+  if (!ctx) return BF_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  drain_profile(ctx);
+  ctx->profiling = on != 0;
+  for (int k = 0; k < 4; ++k) {
+    ctx->prof_launches[k] = 0;
+    ctx->prof_ms[k] = 0.0;
+  }
+  return BF_OK;
+}
+
+int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* total_ms) {
+  if (!ctx || kernel_class < 0 || kernel_class > 3) return BF_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  drain_profile(ctx);
+  *launches = ctx->prof_launches[kernel_class];
+  *total_ms = ctx->prof_ms[kernel_class];
+  return BF_OK;
+}
+
+long long bf_transfer_bytes(const bf_ctx* ctx, int direction) {
+  if (!ctx) return -1;
+  return direction == 0 ? ctx->bytes_h2d : ctx->bytes_d2h;
+}
+
+int bf_probe_unpack_map(const int own_dims[3], int ghost_depth, int ndim, int face,
+                        const int box[6], const int axis_map[6], int peer_face, long long* out,
+                        long long out_len) {
+  const int ghost[3] = {ghost_depth, ghost_depth, ndim == 3 ? ghost_depth : 0};
+  int send[6], recv[6];
+  halo_boxes(face, box, own_dims, ghost, send, recv);
+  int ext[3];
+  for (int a = 0; a < 3; ++a) ext[a] = recv[2 * a + 1] - recv[2 * a];
+  int perm[3];
+  bool flip[3];
+  unpack_axes(face, axis_map, peer_face, perm, flip);
+  int P[3];
+  for (int a = 0; a < 3; ++a) P[perm[a]] = ext[a];
+  const long long Pst[3] = {1, P[0], (long long)P[0] * P[1]};
+  long long origin = 0, stride[3];
+  for (int a = 0; a < 3; ++a) {
+    const long long s = Pst[perm[a]];
+    if (flip[a]) {
+      origin += (long long)(ext[a] - 1) * s;
+      stride[a] = -s;
+    } else {
+      stride[a] = s;
+    }
+  }
+  const long long total = (long long)ext[0] * ext[1] * ext[2];
+  if (out_len < total) return BF_EINVAL;
+  long long m = 0;
+  for (int o2 = 0; o2 < ext[2]; ++o2)
+    for (int o1 = 0; o1 < ext[1]; ++o1)
+      for (int o0 = 0; o0 < ext[0]; ++o0)
+        out[m++] = origin + o0 * stride[0] + o1 * stride[1] + o2 * stride[2];
+  return BF_OK;
+}
+
+}  // extern "C"

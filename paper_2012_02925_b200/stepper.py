@@ -1,0 +1,628 @@
+"""Drop-in GPU replacements for the reference's stepping drivers.
+
+Reference seam: ``RankStepper(solvers, exchange_fn, config)``
+with ``.step(step_index) -> (sumsq[5], ncells)`` and ``.update_ghosts()``
+(blockflow/solver.py:763-814), built internally by ``iterate``
+(solver.py:914-936) and ``run_distributed`` (exchange.py:599-682).  This
+module provides the same three things backed by libbfgpu.so:
+
+  GpuRankStepper       RankStepper contract for one rank's children on one GPU
+  iterate_gpu          same signature/result as solver.iterate
+  run_distributed_gpu  same signature/result as exchange.run_distributed;
+                       one process per GPU over NCCL when torch.distributed is
+                       initialised with world_size == plan.np_ranks, otherwise
+                       every rank as a context of an in-process lock-step group
+
+Plans, boundary specs, gas/scheme/freestream objects are read by attribute,
+so the reference's own objects and this package's mirrors are both accepted.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .errors import (ConfigError, DivergenceError, NativeLibraryError, NonPhysicalStateError,
+                     bridged)
+from .model import FIELD_NAMES, PRIM_NAMES, RK_COEFFS, validate_scheme
+
+_SUPPORTED_BC = tuple(native.BC)
+
+
+def _geometry():
+    from . import geometry, mms
+    return geometry, mms
+
+
+def encode_primitive(rho, u, v, w, p, gamma):
+    """physics.py:136-140 (setup-time conversion of the initial state)."""
+    ke = 0.5 * (u * u + v * v + w * w)
+    return rho, rho * u, rho * v, rho * w, p / (gamma - 1.0) + rho * ke
+
+
+class _BlockSetup:
+    """Host arrays of one child needed to register it with the device."""
+
+    def __init__(self, plan, cid, gas, config, freestream, metrics_fn):
+        geometry, mms = _geometry()
+        self.cid = cid
+        self.block = plan.child_block(cid)
+        self.specs = sorted(plan.boundaries[cid], key=lambda s: s.canonical_key())
+        self.metrics = (metrics_fn or geometry.compute_metrics)(self.block)
+        self.gas, self.config, self.fs = gas, config, freestream
+        self.inner = self.block.interior()
+        self.vol = self.metrics.volume[self.inner]
+        self.solution = mms.manufactured_solution(config.mms_id) if config.mms_id else None
+        self.source = None
+        if config.mms_id is not None:
+            c = self.metrics.centers
+            xs, ys, zs = (c[i][self.inner] for i in range(3))
+            self.source = [np.asfortranarray(np.asarray(s) * self.vol)
+                           for s in mms.mms_source(xs, ys, zs, config.mms_id, gas)]
+
+    def initial_state(self, init):
+        """(fields6, q5) padded Fortran arrays (solver.py:258-277)."""
+        blk = self.block
+        f = {}
+        if init == "manufactured":
+            c = self.metrics.centers
+            for n in PRIM_NAMES:
+                f[n] = np.asfortranarray(self.solution[n](c[0], c[1], c[2]))
+            f["T"] = np.asfortranarray(f["p"] / (f["rho"] * self.gas.R))
+        else:
+            for n in FIELD_NAMES:
+                f[n] = blk.allocate_field(getattr(self.fs, n))
+        q = [np.asfortranarray(x) for x in
+             encode_primitive(*(f[n] for n in PRIM_NAMES), self.gas.gamma)]
+        return [f[n] for n in FIELD_NAMES], q
+
+    def dirichlet_values(self, spec):
+        """Cached MMS ghost values of one patch, [layer][6][tangential] (solver.py:385-401)."""
+        g = self.block.ghost
+        d = spec.axis
+        n = self.block.dims[d]
+        tang = []
+        for a in range(3):
+            if a == d:
+                tang.append(None)
+            else:
+                lo, hi = spec.box[a]
+                tang.append(slice(g[a] + lo, g[a] + hi))
+        c = self.metrics.centers
+        out = []
+        for depth in range(self.block.ghost_depth):
+            pos = g[d] - 1 - depth if spec.side == 0 else g[d] + n + depth
+            cut = list(tang)
+            cut[d] = pos
+            cut = tuple(cut)
+            vals = {nm: self.solution[nm](c[0][cut], c[1][cut], c[2][cut]) for nm in PRIM_NAMES}
+            vals["T"] = vals["p"] / (vals["rho"] * self.gas.R)
+            for nm in FIELD_NAMES:
+                out.append(np.asarray(vals[nm], float).ravel(order="F"))
+        return np.ascontiguousarray(np.concatenate(out))
+
+
+class GpuContext:
+    """One libbfgpu context: the children of one rank on one device."""
+
+    def __init__(self, plan, child_ids, gas, config, freestream, device=0, rank=0, nranks=1,
+                 precision="exact", metrics_fn=None, local_ranks=None):
+        validate_scheme(config)
+        if getattr(config, "viscous", False):
+            raise ConfigError("the device path is inviscid; laminar NS is SURVEY §8f row 1")
+        self.L = native.lib()
+        self.plan = plan
+        self.gas, self.config, self.fs = gas, config, freestream
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self.precision = precision
+        self.child_ids = sorted(child_ids)
+        self.ndim = plan.grid.ndim
+        sch = native.Scheme(
+            flux=native.FLUX[config.flux], limiter=native.LIMITER[config.limiter],
+            epsilon=float(config.epsilon), kappa=float(config.kappa),
+            rk_stages=int(config.rk_stages), cfl=float(config.cfl),
+            limiter_freeze_at=int(config.limiter_freeze_at or 0),
+            entropy_fix_coeff=float(config.entropy_fix_coeff),
+            has_wall_temperature=int(config.wall_temperature is not None),
+            wall_temperature=float(config.wall_temperature or 0.0),
+            precision=native.PRECISION[precision])
+        gas_s = native.Gas(gamma=float(gas.gamma), R=float(gas.R))
+        fs_s = native.Freestream(*(float(getattr(freestream, n)) for n in FIELD_NAMES))
+        self.ctx = self.L.bf_create(self.ndim, C.byref(gas_s), C.byref(sch), C.byref(fs_s),
+                                    device, rank, nranks)
+        if not self.ctx:
+            raise NativeLibraryError(f"bf_create failed (device {device}, rank {rank}/{nranks})")
+        self.setups = {}
+        local_ranks = {rank} if local_ranks is None else set(local_ranks)
+        for cid in self.child_ids:
+            s = _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
+            self.setups[cid] = s
+            fv = []
+            for d in range(self.ndim):
+                for comp in range(3):
+                    fv.append(np.asfortranarray(s.metrics.face_vectors[d][comp], dtype=float))
+            vol = np.asfortranarray(s.vol, dtype=float)
+            src = native.dptrs(s.source) if s.source is not None else None
+            self._keep = (fv, vol, s.source)
+            self._check(self.L.bf_add_block(self.ctx, cid, native.ints(s.block.dims),
+                                            s.block.ghost_depth, native.dptrs(fv),
+                                            native.dptr(vol), src))
+        for cid in self.child_ids:
+            s = self.setups[cid]
+            for spec in s.specs:
+                box = native.ints([x for r in spec.box for x in r])
+                face = native.FACES.index(spec.face)
+                if spec.kind == "physical":
+                    if spec.bc_type not in native.BC:
+                        raise bridged(ConfigError)(f"unknown physical bc type {spec.bc_type!r}")
+                    vals = None
+                    if spec.bc_type == "mms_dirichlet":
+                        if s.solution is None:
+                            raise bridged(ConfigError)("mms_dirichlet patch needs config.mms_id")
+                        vals = s.dirichlet_values(spec)
+                    self._check(self.L.bf_add_bc_patch(
+                        self.ctx, cid, native.BC[spec.bc_type], face, box,
+                        native.dptr(vals) if vals is not None else None))
+                else:
+                    peer = spec.neighbor_block
+                    prank = plan.child(peer).rank if nranks > 1 else rank
+                    self._check(self.L.bf_add_link(
+                        self.ctx, cid, face, box,
+                        native.ints([x for e in spec.axis_map for x in e]), peer,
+                        native.FACES.index(spec.neighbor_face),
+                        native.ints([x for r in spec.neighbor_box for x in r]), prank,
+                        int(spec.link_id)))
+        self._finalized = False
+
+    def finalize(self):
+        if not self._finalized:
+            self._check(self.L.bf_finalize(self.ctx))
+            self._finalized = True
+
+    # ------------------------------------------------------------------
+    def _check(self, rc, block=None):
+        if rc == native.BF_OK:
+            return
+        if rc == native.BF_ENONPHYSICAL:
+            raise bridged(NonPhysicalStateError)(self.error_message())
+        msg = native.last_error(self.ctx)
+        if rc == native.BF_EINVAL:
+            raise bridged(ConfigError)(msg)
+        raise NativeLibraryError(f"libbfgpu error {rc}: {msg}")
+
+    def error_message(self):
+        kind, blk, stage, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        idx = (C.c_longlong * 3)()
+        self.L.bf_error_info(self.ctx, C.byref(kind), C.byref(blk), C.byref(stage), C.byref(d),
+                             idx)
+        ix = tuple(np.int64(x) for x in idx)
+        if kind.value in (native.ERR_FACE_LEFT, native.ERR_FACE_RIGHT):
+            side = "left" if kind.value == native.ERR_FACE_LEFT else "right"
+            return (f"block {blk.value}: non-physical {side} face state, "
+                    f"direction {d.value}, face index {ix}")
+        if kind.value == native.ERR_ROE_A2:
+            return f"Roe-averaged state has non-positive sound speed at index {np.array(ix)}"
+        if kind.value == native.ERR_UPDATE:
+            return (f"block {blk.value}: non-physical update at cell {ix} "
+                    f"(CFL {self.config.cfl} may be too high)")
+        return native.last_error(self.ctx)
+
+    def upload_initial(self, init="uniform", seed=0):
+        """init: "uniform" | "manufactured" (solver.py:258-271) | "perturbed"
+        (freestream, interior rho/p x (1 + 0.01 N(0,1)) drawn
+        per child in child-id order from default_rng(seed); the draws of
+        children owned by other ranks are consumed too, so every rank sees
+        the same initial field as a serial run)."""
+        self.finalize()
+        if init == "perturbed":
+            from .cases import perturbed_state
+            rng = np.random.default_rng(seed)
+            mine = set(self.child_ids)
+            for c in sorted(self.plan.children, key=lambda c: c.id):
+                blk = self.setups[c.id].block if c.id in mine else self.plan.child_block(c.id)
+                f = perturbed_state(blk, self.fs, self.gas, rng)
+                if c.id not in mine:
+                    continue
+                f6 = [f[n] for n in FIELD_NAMES]
+                q5 = encode_primitive(*(f[n] for n in PRIM_NAMES), self.gas.gamma)
+                self.upload(c.id, f6, q5)
+            return
+        for cid in self.child_ids:
+            f6, q5 = self.setups[cid].initial_state(init)
+            self.upload(cid, f6, q5)
+
+    def upload(self, cid, fields6, q5):
+        f6 = [np.asfortranarray(x, dtype=float) for x in fields6]
+        q = [np.asfortranarray(x, dtype=float) for x in q5]
+        self._check(self.L.bf_upload_fields(self.ctx, cid, native.dptrs(f6), native.dptrs(q)))
+
+    def update_ghosts(self):
+        self._check(self.L.bf_update_ghosts(self.ctx))
+
+    def step(self, step_index):
+        out = (C.c_double * 5)()
+        n = C.c_longlong()
+        self._check(self.L.bf_step(self.ctx, int(step_index), out, C.byref(n)))
+        return np.array(out[:], dtype=float), int(n.value)
+
+    def download(self, cid, what):
+        blk = self.setups[cid].block
+        if isinstance(what, str):
+            code = native.FIELD[what]
+        else:
+            code = int(what)
+        if code == native.FIELD["dtv"]:
+            out = np.empty(blk.dims, order="F")
+        elif code >= native.FIELD_PSI:
+            r = code - native.FIELD_PSI
+            d = r // 10
+            shape = list(blk.dims)
+            shape[d] += 2
+            out = np.empty(shape, order="F")
+        else:
+            out = np.empty(blk.shape, order="F")
+        self._check(self.L.bf_download(self.ctx, cid, code, native.dptr(out)))
+        return out
+
+    def set_stream(self, stream_ptr):
+        self._check(self.L.bf_set_stream(self.ctx, C.c_void_p(stream_ptr)))
+
+    def set_profiling(self, on):
+        self._check(self.L.bf_set_profiling(self.ctx, int(bool(on))))
+
+    def kernel_stats(self, cls):
+        n, ms = C.c_longlong(), C.c_double()
+        self._check(self.L.bf_kernel_stats(self.ctx, cls, C.byref(n), C.byref(ms)))
+        return int(n.value), float(ms.value)
+
+    def transfer_bytes(self):
+        return int(self.L.bf_transfer_bytes(self.ctx, 0)), int(self.L.bf_transfer_bytes(self.ctx, 1))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.bf_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class _LazyFields(dict):
+    """fields[name] -> padded Fortran ndarray, downloaded on first access."""
+
+    def __init__(self, view):
+        super().__init__()
+        self._view = view
+
+    def __missing__(self, name):
+        if name not in FIELD_NAMES:
+            raise KeyError(name)
+        arr = self._view._gpu.download(self._view._cid, name)
+        self[name] = arr
+        return arr
+
+    def keys(self):
+        return FIELD_NAMES
+
+    def __iter__(self):
+        return iter(FIELD_NAMES)
+
+    def __len__(self):
+        return len(FIELD_NAMES)
+
+    def items(self):
+        return [(n, self[n]) for n in FIELD_NAMES]
+
+    def values(self):
+        return [self[n] for n in FIELD_NAMES]
+
+
+class GpuBlockView:
+    """Read-side stand-in for a BlockSolver (what callers read after a run,
+    SURVEY.md §8b): fields/q are device downloads, geometry is host-side."""
+
+    PRIM_NAMES = PRIM_NAMES
+
+    def __init__(self, gpu, cid):
+        s = gpu.setups[cid]
+        self._gpu, self._cid = gpu, cid
+        self.block = s.block
+        self.metrics = s.metrics
+        self.gas, self.config, self.freestream = gpu.gas, gpu.config, gpu.fs
+        self.specs = s.specs
+        self.physical_specs = [x for x in s.specs if x.kind == "physical"]
+        self.dirs = (0, 1) if s.block.ndim == 2 else (0, 1, 2)
+        self._int = s.inner
+        self._vol = s.vol
+        self.frozen = False
+        self.invalidate()
+
+    def invalidate(self):
+        self.fields = _LazyFields(self)
+        self._q = None
+        self._psi = None
+
+    @property
+    def q(self):
+        if self._q is None:
+            self._q = [self._gpu.download(self._cid, native.FIELD_Q0 + e) for e in range(5)]
+        return self._q
+
+    @property
+    def psi(self):
+        """{d: (psi_plus (5, ...), psi_minus (5, ...))} when limiters are kept (freeze runs)."""
+        if self._psi is None:
+            if not self.config.limiter_freeze_at:
+                return {}
+            out = {}
+            for d in self.dirs:
+                pair = []
+                for pm in range(2):
+                    pair.append(np.stack([self._gpu.download(
+                        self._cid, native.FIELD_PSI + 10 * d + 5 * pm + v) for v in range(5)]))
+                out[d] = tuple(pair)
+            self._psi = out
+        return self._psi
+
+    def residual_sumsq(self, R):
+        return np.array([float(np.sum(r * r)) for r in R])
+
+
+class GpuRankStepper:
+    """RankStepper (solver.py:763-814) backed by one device context."""
+
+    def __init__(self, gpu: GpuContext, config):
+        self.gpu = gpu
+        self.config = config
+        self.alphas = RK_COEFFS[config.rk_stages]
+        self.solvers = {cid: GpuBlockView(gpu, cid) for cid in gpu.child_ids}
+
+    def update_ghosts(self):
+        self.gpu.update_ghosts()
+        self._invalidate()
+
+    def step(self, step_index):
+        fz = self.config.limiter_freeze_at
+        try:
+            sumsq, ncells = self.gpu.step(step_index)
+        finally:
+            self._invalidate()
+        for v in self.solvers.values():
+            v.frozen = fz is not None and step_index > fz
+        return sumsq, ncells
+
+    def _invalidate(self):
+        for v in self.solvers.values():
+            v.invalidate()
+
+
+@dataclass
+class IterationResult:
+    """solver.py:817-829."""
+    solvers: dict
+    history: np.ndarray
+    steps: int
+    converged: bool
+
+    def relative_history(self):
+        base = self.history[0].copy()
+        safe = np.where(base > 0.0, base, 1.0)
+        rel = self.history / safe
+        rel[:, base == 0.0] = 0.0
+        return rel
+
+
+@dataclass
+class DistributedResult:
+    """exchange.py:582-596."""
+    fields: dict
+    history: np.ndarray
+    steps: int
+    converged: bool
+    counters: dict
+    solve_seconds: float
+
+    def relative_history(self):
+        base = self.history[0].copy()
+        safe = np.where(base > 0.0, base, 1.0)
+        rel = self.history / safe
+        rel[:, base == 0.0] = 0.0
+        return rel
+
+
+def residual_norms(sumsq):
+    return np.sqrt(np.asarray(sumsq))
+
+
+def check_history_guards(history, step, residual_target, divergence_factor=1e6,
+                         residual_floor=None):
+    """solver.py:836-855 (host-side, per step)."""
+    if residual_floor is not None and float(np.max(history[step])) <= residual_floor:
+        return True
+    base = history[0]
+    active = base > 1e-12 * np.max(base)
+    if not np.any(active):
+        return False
+    rel = history[step][active] / base[active]
+    if np.any(~np.isfinite(rel)) or np.max(rel) > divergence_factor:
+        raise bridged(DivergenceError)(
+            f"residual grew by more than {divergence_factor:.0e} at step {step + 1}")
+    return residual_target is not None and float(np.max(rel)) <= residual_target
+
+
+def write_residual_csv(result, path):
+    """solver.py:939-945."""
+    rel = result.relative_history()
+    with open(path, "w") as f:
+        f.write("step,r_mass,r_xmom,r_ymom,r_zmom,r_energy\n")
+        for i, row in enumerate(rel):
+            f.write(f"{i + 1}," + ",".join(f"{v:.16e}" for v in row) + "\n")
+
+
+def iterate_gpu(plan, schedule, gas, config, freestream, max_steps, residual_target=None,
+                init="uniform", residual_floor=None, device=0, precision="exact",
+                metrics_fn=None):
+    """solver.iterate on one GPU: every child of the plan in one context, all
+    connected boundaries served by device copies (solver.py:914-936)."""
+    gpu = GpuContext(plan, [c.id for c in plan.children], gas, config, freestream,
+                     device=device, precision=precision, metrics_fn=metrics_fn)
+    gpu.upload_initial(init)
+    stepper = GpuRankStepper(gpu, config)
+    history, converged = [], False
+    for step in range(max_steps):
+        sumsq, _ = stepper.step(step + 1)
+        history.append(residual_norms(sumsq))
+        if check_history_guards(history, step, residual_target, residual_floor=residual_floor):
+            converged = True
+            break
+    return IterationResult(solvers=stepper.solvers, history=np.array(history),
+                           steps=len(history), converged=converged)
+
+
+def _gather_parent_fields(plan, views_by_cid):
+    names = FIELD_NAMES
+    out = {b.id: {n: np.full(b.dims, np.nan) for n in names} for b in plan.grid.blocks}
+    for cid, view in views_by_cid.items():
+        c = plan.child(cid)
+        (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
+        for n in names:
+            out[c.parent][n][i0:i1, j0:j1, k0:k1] = view.fields[n][view.block.interior()]
+    return out
+
+
+def native_counters(plan, rounds=1):
+    """Transfer accounting of the native engine (packed, persistent, direct,
+    deferred; cf. exchange.py:166-200): per rank messages/bytes/runs/waits."""
+    from .topology import halo_regions
+    ndim = plan.grid.ndim
+    nf = 3 + ndim
+    out = {}
+    for r in range(plan.np_ranks):
+        out[r] = {"messages": 0, "runs": 0, "bytes": 0, "staging_copies": 0, "waits": 0,
+                  "max_pending": 0}
+    for cid, s in plan.connected_specs():
+        rank = plan.child(cid).rank
+        blk = plan.child_block(cid)
+        remote = plan.child(s.neighbor_block).rank != rank
+        for rnd in range(1, rounds + 1):
+            send, _ = halo_regions(s, blk.dims, blk.ghost, rnd)
+            cells = int(np.prod([hi - lo for lo, hi in send]))
+            out[rank]["runs"] += 2 * nf
+            if remote:
+                out[rank]["messages"] += 4
+                out[rank]["bytes"] += cells * nf * 8
+                out[rank]["waits"] += 2
+                out[rank]["max_pending"] += 2
+    return out
+
+
+def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, max_steps=100,
+                        residual_target=None, init="uniform", timeout_s=5.0,
+                        residual_floor=None, precision="exact", devices=None, metrics_fn=None):
+    """exchange.run_distributed on GPUs (exchange.py:599-682).
+
+    * torch.distributed initialised with world_size == plan.np_ranks: this
+      process runs rank = dist.get_rank() on cuda:LOCAL_RANK, halos over NCCL,
+      the residual sum over ranks in rank order; fields are gathered to every
+      rank.
+    * otherwise: every rank is a context of one in-process group, rank r on
+      device devices[r % len(devices)] (all on device 0 by default), halos as
+      device-to-device copies driven in lock step.
+    """
+    import os
+    nr = plan.np_ranks
+    dist = None
+    try:
+        import torch.distributed as tdist
+        if tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() == nr:
+            dist = tdist
+    except Exception:  # noqa: BLE001
+        dist = None
+    history, converged = [], False
+    if dist is not None:
+        rank = dist.get_rank()
+        device = int(os.environ.get("LOCAL_RANK", rank)) if devices is None else devices[rank]
+        gpu = GpuContext(plan, [c.id for c in plan.rank_children(rank)], gas, config, freestream,
+                         device=device, rank=rank, nranks=nr, precision=precision,
+                         metrics_fn=metrics_fn)
+        uid = bytearray(128)
+        if rank == 0:
+            buf = (C.c_char * 128)()
+            gpu._check(gpu.L.bf_nccl_unique_id(buf))
+            uid = bytearray(buf.raw)
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        idbuf = (C.c_char * 128).from_buffer_copy(box[0])
+        gpu._check(gpu.L.bf_nccl_init(gpu.ctx, idbuf))
+        gpu.upload_initial(init)
+        stepper = GpuRankStepper(gpu, config)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for step in range(max_steps):
+            sumsq, _ = stepper.step(step + 1)
+            history.append(residual_norms(sumsq))
+            if check_history_guards(history, step, residual_target,
+                                    residual_floor=residual_floor):
+                converged = True
+                break
+        solve = time.perf_counter() - t0
+        mine = {cid: {n: v.fields[n][v.block.interior()] for n in FIELD_NAMES}
+                for cid, v in stepper.solvers.items()}
+        parts = [None] * nr
+        dist.all_gather_object(parts, mine)
+        fields = {b.id: {n: np.full(b.dims, np.nan) for n in FIELD_NAMES}
+                  for b in plan.grid.blocks}
+        for part in parts:
+            for cid, fl in part.items():
+                c = plan.child(cid)
+                (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
+                for n in FIELD_NAMES:
+                    fields[c.parent][n][i0:i1, j0:j1, k0:k1] = fl[n]
+        gpu.close()
+        return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
+                                 converged=converged, counters=native_counters(plan),
+                                 solve_seconds=solve)
+
+    devs = list(devices) if devices is not None else [0]
+    gpus = [GpuContext(plan, [c.id for c in plan.rank_children(r)], gas, config, freestream,
+                       device=devs[r % len(devs)], rank=r, nranks=nr, precision=precision,
+                       metrics_fn=metrics_fn) for r in range(nr)]
+    for g in gpus:
+        g.upload_initial(init)
+    L = native.lib()
+    arr = (C.c_void_p * nr)(*[g.ctx for g in gpus])
+    grp = L.bf_group_create(arr, nr)
+    if not grp:
+        raise NativeLibraryError("bf_group_create failed")
+    steppers = [GpuRankStepper(g, config) for g in gpus]
+    try:
+        t0 = time.perf_counter()
+        for step in range(max_steps):
+            out = (C.c_double * 5)()
+            bad = C.c_int(-1)
+            rc = L.bf_group_step(grp, step + 1, out, C.byref(bad))
+            for st in steppers:
+                st._invalidate()
+            if rc != native.BF_OK:
+                g = gpus[bad.value] if bad.value >= 0 else gpus[0]
+                g._check(rc)
+            history.append(residual_norms(np.array(out[:])))
+            if check_history_guards(history, step, residual_target,
+                                    residual_floor=residual_floor):
+                converged = True
+                break
+        solve = time.perf_counter() - t0
+        views = {cid: v for st in steppers for cid, v in st.solvers.items()}
+        fields = _gather_parent_fields(plan, views)
+    finally:
+        L.bf_group_destroy(grp)
+    return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
+                             converged=converged, counters=native_counters(plan),
+                             solve_seconds=solve)

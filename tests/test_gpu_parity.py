@@ -1,0 +1,263 @@
+"""Device path vs the CPU oracle on identical plans and initial states.
+
+EXACT mode is bitwise wherever the path has no libm pow (walls, in/outflow,
+MMS, connected faces); cases with farfield patches go through pow (numpy /
+glibc vs CUDA differ by <= 2 ulp), so their tolerance is 1e-12 relative to
+the freestream scale per field and 1e-12 relative on the residual history —
+the north-star bar (BASELINE.json).  FAST mode (FMA) is held to the same
+1e-12 bar.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2012_02925_b200 import cases, geometry, planning
+from paper_2012_02925_b200.errors import NonPhysicalStateError
+from paper_2012_02925_b200.model import FIELD_NAMES, FreestreamState, GasModel, SchemeConfig
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+GAS = GasModel()
+
+
+def _gpu():
+    from paper_2012_02925_b200 import stepper
+    return stepper
+
+
+def _init_perturbed(blocks, fs, gas, seed=0):
+    rng = np.random.default_rng(seed)
+    for cid in sorted(blocks):
+        b = blocks[cid]
+        f = cases.perturbed_state(b.block, fs, gas, rng)
+        for n in FIELD_NAMES:
+            b.fields[n][...] = f[n]
+        b.sync_conserved()
+
+
+def run_pair(plan, cfg, fs, steps, init="uniform", precision="exact", gas=GAS):
+    sched = planning.reorder_boundaries(plan)
+    if init == "perturbed":
+        blocks = oracle.build_blocks(plan, gas, cfg, fs)
+        _init_perturbed(blocks, fs, gas)
+        st = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
+        hist = [np.sqrt(st.step(k + 1)[0]) for k in range(steps)]
+        ref = oracle.blockflow_oracle.OracleResult(blocks, np.array(hist), steps, False)
+    else:
+        ref = oracle.iterate(plan, sched, gas, cfg, fs, steps, init=init)
+    got = _gpu().iterate_gpu(plan, sched, gas, cfg, fs, steps, init=init, precision=precision)
+    return ref, got
+
+
+def compare(ref, got, fs, bitwise, tol=1e-12, padded=True, check_q=True):
+    if bitwise:
+        np.testing.assert_array_equal(got.history, ref.history)
+    else:
+        np.testing.assert_allclose(got.history, ref.history, rtol=tol, atol=0)
+    scale = {n: max(abs(getattr(fs, n)), 1e-300) for n in FIELD_NAMES}
+    speed = max(abs(fs.u), abs(fs.v), abs(fs.w))
+    for n in ("u", "v", "w"):
+        scale[n] = speed
+    for cid, view in got.solvers.items():
+        o = ref.solvers[cid]
+        cut = slice(None) if padded else view.block.interior()
+        for n in FIELD_NAMES:
+            a = o.fields[n][cut] if padded else o.fields[n][view.block.interior()]
+            b = view.fields[n][cut] if padded else view.fields[n][view.block.interior()]
+            if bitwise:
+                np.testing.assert_array_equal(b, a, err_msg=f"child {cid} field {n}")
+            else:
+                d = np.max(np.abs(a - b)) / scale[n]
+                assert d <= tol, f"child {cid} field {n}: {d:.3e} > {tol}"
+        if check_q:
+            for e in range(5):
+                if bitwise:
+                    np.testing.assert_array_equal(view.q[e], o.q[e], err_msg=f"child {cid} q{e}")
+
+
+def fs_inlet():
+    return cases.freestream_for("inlet_ramp_2d", GAS, 2)
+
+
+@pytest.mark.parametrize("flux,limiter,rk", [
+    ("van_leer", "van_albada", 2), ("roe", "minmod", 4), ("roe", "van_leer", 1),
+    ("van_leer", "none", 2)])
+def test_inlet_single_block_bitwise(flux, limiter, rk):
+    plan = planning.decompose(geometry.inlet_ramp_2d(0), 1, 2)
+    cfg = SchemeConfig(flux=flux, limiter=limiter, rk_stages=rk, cfl=0.8)
+    ref, got = run_pair(plan, cfg, fs_inlet(), 12)
+    compare(ref, got, fs_inlet(), bitwise=True)
+
+
+def test_inlet_decomposed_local_links_bitwise():
+    plan = planning.decompose(geometry.inlet_ramp_2d(1), 4, 2)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    ref, got = run_pair(plan, cfg, fs_inlet(), 10)
+    compare(ref, got, fs_inlet(), bitwise=True)
+
+
+def test_c1_size_inlet_bitwise():
+    plan, _, gas, cfg, fs, init = cases.c1_inlet()
+    ref, got = run_pair(plan, cfg, fs, 20)
+    compare(ref, got, fs, bitwise=True)
+
+
+def test_epsilon_zero_and_kappa_third():
+    plan = planning.decompose(geometry.inlet_ramp_2d(0), 2, 2)
+    for cfg in (SchemeConfig(flux="roe", limiter="none", epsilon=0.0, cfl=0.5),
+                SchemeConfig(flux="van_leer", limiter="van_albada", kappa=1.0 / 3.0, cfl=0.5)):
+        ref, got = run_pair(plan, cfg, fs_inlet(), 6)
+        compare(ref, got, fs_inlet(), bitwise=True)
+
+
+def test_mms_2d_bitwise():
+    plan = planning.decompose(geometry.cartesian_box_2d(2), 2, 2)
+    fs = cases.freestream_for("cartesian_box", GAS, 2)
+    cfg = SchemeConfig(flux="roe", limiter="none", rk_stages=2, cfl=0.5, mms_id="euler_2d")
+    ref, got = run_pair(plan, cfg, fs, 8, init="manufactured")
+    compare(ref, got, fs, bitwise=True)
+
+
+def test_mms_3d_bitwise():
+    plan = planning.decompose(geometry.cartesian_box_3d(16), 8, 3)
+    fs = cases.freestream_for("cartesian_box", GAS, 3)
+    cfg = SchemeConfig(flux="roe", limiter="none", rk_stages=2, cfl=0.5, mms_id="euler_2d")
+    ref, got = run_pair(plan, cfg, fs, 5, init="manufactured")
+    compare(ref, got, fs, bitwise=True)
+
+
+def test_freeze_limiters_bitwise():
+    plan = planning.decompose(geometry.inlet_ramp_2d(0), 1, 2)
+    cfg = SchemeConfig(flux="roe", limiter="van_albada", cfl=0.5, limiter_freeze_at=2)
+    ref, got = run_pair(plan, cfg, fs_inlet(), 5)
+    compare(ref, got, fs_inlet(), bitwise=True)
+    o = ref.solvers[0]
+    v = got.solvers[0]
+    for d in o.dirs:
+        for pm in range(2):
+            np.testing.assert_array_equal(v.psi[d][pm], o.psi[d][pm])
+
+
+def test_annulus_self_connection_farfield():
+    plan = planning.decompose(geometry.c_annulus_2d(0), 4, 2)
+    fs = cases.freestream_for("c_annulus_2d", GAS, 2)
+    cfg = SchemeConfig(flux="roe", limiter="van_albada", cfl=0.5)
+    ref, got = run_pair(plan, cfg, fs, 10)
+    compare(ref, got, fs, bitwise=False)
+
+
+@pytest.mark.parametrize("np_ranks,level", [(1, 0), (8, 0), (3, 1)])
+def test_box3d_farfield(np_ranks, level):
+    plan = cases.make_plan(geometry.multiblock_box_3d(level), np_ranks)
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    ref, got = run_pair(plan, cfg, fs, 5, init="perturbed")
+    compare(ref, got, fs, bitwise=False)
+
+
+def test_box3d_roe_rk4():
+    plan = cases.make_plan(geometry.multiblock_box_3d(3), 2)
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    cfg = SchemeConfig(flux="roe", limiter="minmod", rk_stages=4, cfl=0.5)
+    ref, got = run_pair(plan, cfg, fs, 3, init="perturbed")
+    compare(ref, got, fs, bitwise=False)
+
+
+@pytest.mark.parametrize("case", ["inlet", "box3d"])
+def test_fast_precision_within_tolerance(case):
+    if case == "inlet":
+        plan = planning.decompose(geometry.inlet_ramp_2d(1), 2, 2)
+        fs, init = fs_inlet(), "uniform"
+        cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    else:
+        plan = cases.make_plan(geometry.multiblock_box_3d(3), 1)
+        fs, init = cases.freestream_for("multiblock_box_3d", GAS, 3), "perturbed"
+        cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    ref, got = run_pair(plan, cfg, fs, 20, init=init, precision="fast")
+    compare(ref, got, fs, bitwise=False)
+
+
+def test_update_ghosts_matches_oracle():
+    plan = planning.decompose(geometry.c_annulus_2d(0), 2, 2)
+    fs = cases.freestream_for("c_annulus_2d", GAS, 2)
+    cfg = SchemeConfig(flux="roe", cfl=0.5)
+    st = _gpu()
+    gpu = st.GpuContext(plan, [c.id for c in plan.children], GAS, cfg, fs)
+    gpu.upload_initial("uniform")
+    stepper = st.GpuRankStepper(gpu, cfg)
+    stepper.step(1)
+    stepper.update_ghosts()
+    sched = planning.reorder_boundaries(plan)
+    blocks = oracle.build_blocks(plan, GAS, cfg, fs)
+    for b in blocks.values():
+        b.init_uniform()
+    ost = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
+    ost.step(1)
+    ost.update_ghosts()
+    for cid, v in stepper.solvers.items():
+        for n in FIELD_NAMES:
+            a, b = blocks[cid].fields[n], v.fields[n]
+            assert np.max(np.abs(a - b)) <= 1e-12 * max(abs(getattr(fs, n)), abs(fs.u))
+
+
+def test_non_physical_face_state_reported():
+    plan = planning.decompose(geometry.inlet_ramp_2d(0), 1, 2)
+    cfg = SchemeConfig(flux="roe", limiter="van_albada", cfl=0.5)
+    fs = fs_inlet()
+    st = _gpu()
+    gpu = st.GpuContext(plan, [0], GAS, cfg, fs)
+    gpu.finalize()
+    f6, q5 = gpu.setups[0].initial_state("uniform")
+    f6[4][10, 10, 0] = -2.0e5
+    gpu.upload(0, f6, q5)
+    stepper = st.GpuRankStepper(gpu, cfg)
+    with pytest.raises(NonPhysicalStateError, match="face state") as ei:
+        stepper.step(1)
+    # same message as the oracle raises on the same poisoned state
+    blocks = oracle.build_blocks(plan, GAS, cfg, fs)
+    blocks[0].init_uniform()
+    blocks[0].fields["p"][10, 10, 0] = -2.0e5
+    sched = planning.reorder_boundaries(plan)
+    ost = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
+    with pytest.raises(NonPhysicalStateError) as eo:
+        ost.step(1)
+    assert str(ei.value) == str(eo.value)
+
+
+def test_absurd_cfl_reports_update_or_divergence():
+    from paper_2012_02925_b200.errors import DivergenceError
+    plan = planning.decompose(geometry.inlet_ramp_2d(0), 1, 2)
+    cfg = SchemeConfig(flux="roe", limiter="none", rk_stages=1, cfl=50.0)
+    with pytest.raises((DivergenceError, NonPhysicalStateError)):
+        _gpu().iterate_gpu(plan, planning.reorder_boundaries(plan), GAS, cfg,
+                           FreestreamState.from_mach(GAS, 4.0, 12270.0, 217.0, 0.0, 2), 400)
+
+
+@pytest.mark.parametrize("case,np_ranks", [("inlet", 4), ("box3d", 8)])
+def test_run_distributed_group_matches_serial(case, np_ranks):
+    st = _gpu()
+    if case == "inlet":
+        grid = geometry.inlet_ramp_2d(1)
+        fs, cfg, bitwise = fs_inlet(), SchemeConfig(flux="van_leer", cfl=0.8), True
+    else:
+        grid = geometry.multiblock_box_3d(2)
+        fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+        cfg, bitwise = SchemeConfig(flux="roe", cfl=0.5), False
+    plan = planning.decompose(grid, np_ranks, grid.ndim)
+    sched = planning.reorder_boundaries(plan)
+    res = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=6)
+    ref = oracle.iterate(plan, sched, GAS, cfg, fs, 6)
+    if bitwise:
+        np.testing.assert_array_equal(res.history, ref.history)
+    else:
+        np.testing.assert_allclose(res.history, ref.history, rtol=1e-12)
+    for c in plan.children:
+        (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
+        for n in ("rho", "u", "v", "w", "p"):
+            a = ref.solvers[c.id].fields[n][plan.child_block(c.id).interior()]
+            b = res.fields[c.parent][n][i0:i1, j0:j1, k0:k1]
+            if bitwise:
+                np.testing.assert_array_equal(b, a)
+            else:
+                assert np.max(np.abs(a - b)) <= 1e-12 * max(abs(getattr(fs, n)), abs(fs.u))
