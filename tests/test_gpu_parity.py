@@ -51,10 +51,9 @@ def run_pair(plan, cfg, fs, steps, init="uniform", precision="exact", gas=GAS):
 
 
 def compare(ref, got, fs, bitwise, tol=1e-12, padded=True, check_q=True):
-    if bitwise:
-        np.testing.assert_array_equal(got.history, ref.history)
-    else:
-        np.testing.assert_allclose(got.history, ref.history, rtol=tol, atol=0)
+    # sum(R^2) is accumulated per tile on the device (numpy: pairwise over C
+    # order), so even bitwise-equal residual fields give norms equal to ~1 ulp.
+    np.testing.assert_allclose(got.history, ref.history, rtol=1e-13 if bitwise else tol, atol=0)
     scale = {n: max(abs(getattr(fs, n)), 1e-300) for n in FIELD_NAMES}
     speed = max(abs(fs.u), abs(fs.v), abs(fs.w))
     for n in ("u", "v", "w"):
@@ -86,7 +85,14 @@ def fs_inlet():
 def test_inlet_single_block_bitwise(flux, limiter, rk):
     plan = planning.decompose(geometry.inlet_ramp_2d(0), 1, 2)
     cfg = SchemeConfig(flux=flux, limiter=limiter, rk_stages=rk, cfl=0.8)
-    ref, got = run_pair(plan, cfg, fs_inlet(), 12)
+    try:
+        ref, got = run_pair(plan, cfg, fs_inlet(), 12)
+    except NonPhysicalStateError as exc:
+        # unlimited MUSCL at M=4 breaks down: the device must fail the same way
+        with pytest.raises(NonPhysicalStateError) as ei:
+            _gpu().iterate_gpu(plan, planning.reorder_boundaries(plan), GAS, cfg, fs_inlet(), 12)
+        assert str(ei.value) == str(exc)
+        return
     compare(ref, got, fs_inlet(), bitwise=True)
 
 
@@ -246,12 +252,17 @@ def test_run_distributed_group_matches_serial(case, np_ranks):
         cfg, bitwise = SchemeConfig(flux="roe", cfl=0.5), False
     plan = planning.decompose(grid, np_ranks, grid.ndim)
     sched = planning.reorder_boundaries(plan)
-    res = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=6)
-    ref = oracle.iterate(plan, sched, GAS, cfg, fs, 6)
+    init = "uniform" if bitwise else "perturbed"
+    res = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=6, init=init)
     if bitwise:
-        np.testing.assert_array_equal(res.history, ref.history)
+        ref = oracle.iterate(plan, sched, GAS, cfg, fs, 6)
     else:
-        np.testing.assert_allclose(res.history, ref.history, rtol=1e-12)
+        blocks = oracle.build_blocks(plan, GAS, cfg, fs)
+        _init_perturbed(blocks, fs, GAS)
+        ost = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
+        hist = [np.sqrt(ost.step(k + 1)[0]) for k in range(6)]
+        ref = oracle.blockflow_oracle.OracleResult(blocks, np.array(hist), 6, False)
+    np.testing.assert_allclose(res.history, ref.history, rtol=1e-13 if bitwise else 1e-12)
     for c in plan.children:
         (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
         for n in ("rho", "u", "v", "w", "p"):
