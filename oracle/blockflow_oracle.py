@@ -11,6 +11,7 @@ inputs injected by the caller; this module restates only the per-step path.
 from __future__ import annotations
 
 import threading
+import time
 
 import numpy as np
 
@@ -680,7 +681,18 @@ def build_blocks(plan, gas, config, freestream, child_ids=None, metrics_fn=None,
     return out
 
 
-def _init(blocks, init):
+def _init(blocks, init, seed=0):
+    """uniform / manufactured (solver.py:258-271) or "perturbed": the C4
+    bench state, drawn per child in child-id order."""
+    if init == "perturbed":
+        from paper_2012_02925_b200.cases import perturbed_state
+        rng = np.random.default_rng(seed)
+        for cid in sorted(blocks):
+            b = blocks[cid]
+            for n, arr in perturbed_state(b.block, b.fs, b.gas, rng).items():
+                b.fields[n][...] = arr
+            b.sync_conserved()
+        return
     for b in blocks.values():
         b.init_manufactured() if init == "manufactured" else b.init_uniform()
 
@@ -727,7 +739,7 @@ def iterate(plan, schedule, gas, config, freestream, max_steps, residual_target=
 
 
 def run_threaded(plan, schedule, gas, config, freestream, max_steps, init="uniform",
-                 **setup):
+                 warmup=0, **setup):
     """One thread per rank, deterministic rank-ordered sum of the per-rank
     Σ R² (exchange.py:294-309, 599-682).  Exchanges are in-process copies in
     schedule order behind a barrier per stage, which yields the same fields
@@ -757,10 +769,16 @@ def run_threaded(plan, schedule, gas, config, freestream, max_steps, init="unifo
             bar.wait()
         return ex
 
+    clock = {}
+
     def worker(rank):
         try:
             st = OracleStepper(per_rank[rank], exchange_for(rank), config)
-            for k in range(max_steps):
+            for k in range(warmup + max_steps):
+                if k == warmup:
+                    bar.wait()            # solve timer starts after set-up + warm-up
+                    if rank == 0:
+                        clock["t0"] = time.perf_counter()
                 ss, _ = st.step(k + 1)
                 partial[(k, rank)] = ss
                 bar.wait()
@@ -781,6 +799,9 @@ def run_threaded(plan, schedule, gas, config, freestream, max_steps, init="unifo
         t.start()
     for t in ts:
         t.join()
+    t1 = time.perf_counter()
     if errors:
         raise sorted(errors.items())[0][1]
-    return OracleResult(everyone, np.array(history), len(history), False)
+    res = OracleResult(everyone, np.array(history[warmup:]), len(history) - warmup, False)
+    res.solve_seconds = t1 - clock.get("t0", t1)
+    return res

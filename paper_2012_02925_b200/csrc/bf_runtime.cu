@@ -896,6 +896,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
     for (int cc = 0; cc < 4; ++cc)
       CK(cudaMemcpy(d.fn[dd][cc] - hb.origin, out[cc].data(), sizeof(double) * hb.fsz,
                     cudaMemcpyHostToDevice));
+    ctx->bytes_h2d += 4LL * (long long)sizeof(double) * hb.fsz;
   }
   // volume + sources: interior Fortran (n0, n1, n2)
   auto put_interior = [&](double* dptr, const double* src) -> int {
@@ -907,6 +908,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
               src[i + (long long)hb.n[0] * (j + (long long)hb.n[1] * k)];
     CK(cudaMemcpy(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
                   cudaMemcpyHostToDevice));
+    ctx->bytes_h2d += (long long)sizeof(double) * hb.fsz;
     return BF_OK;
   };
   int rc = put_interior(d.vol, volume);
@@ -1026,7 +1028,7 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
     CK(cudaMemcpyAsync(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->bytes_h2d += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
+    ctx->bytes_h2d += (long long)sizeof(double) * hb.fsz;
     return BF_OK;
   };
   for (int f = 0; f < 6; ++f) {
@@ -1114,6 +1116,7 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
   std::vector<double> a((size_t)hb.fsz), b((size_t)hb.fsz);
   auto get = [&](const double* dptr, std::vector<double>& h) -> int {
     CK(cudaMemcpy(h.data(), dptr - hb.origin, sizeof(double) * hb.fsz, cudaMemcpyDeviceToHost));
+    ctx->bytes_d2h += (long long)sizeof(double) * hb.fsz;
     return BF_OK;
   };
   auto at = [&](long long i, long long j, long long k) {   // padded coords
@@ -1151,7 +1154,6 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
           }
           out[i + hb.P[0] * (j + (long long)hb.P[1] * k)] = v;
         }
-    ctx->bytes_d2h += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
     return BF_OK;
   }
   if (what >= BF_FIELD_Q0 && what <= BF_FIELD_Q0 + 4) {
@@ -1161,7 +1163,6 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
       for (long long j = 0; j < hb.P[1]; ++j)
         for (long long i = 0; i < hb.P[0]; ++i)
           out[i + hb.P[0] * (j + (long long)hb.P[1] * k)] = a[at(i, j, k)];
-    ctx->bytes_d2h += (long long)sizeof(double) * hb.P[0] * hb.P[1] * hb.P[2];
     return BF_OK;
   }
   if (what == BF_FIELD_DTV) {

@@ -44,6 +44,12 @@ def encode_primitive(rho, u, v, w, p, gamma):
     return rho, rho * u, rho * v, rho * w, p / (gamma - 1.0) + rho * ke
 
 
+def host_setups(plan, child_ids, gas, config, freestream, metrics_fn=None):
+    """Host-side setup (metrics, MMS data) of children, reusable across contexts."""
+    return {cid: _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
+            for cid in child_ids}
+
+
 class _BlockSetup:
     """Host arrays of one child needed to register it with the device."""
 
@@ -110,7 +116,7 @@ class GpuContext:
     """One libbfgpu context: the children of one rank on one device."""
 
     def __init__(self, plan, child_ids, gas, config, freestream, device=0, rank=0, nranks=1,
-                 precision="exact", metrics_fn=None, local_ranks=None):
+                 precision="exact", metrics_fn=None, setups=None):
         validate_scheme(config)
         if getattr(config, "viscous", False):
             raise ConfigError("the device path is inviscid; laminar NS is SURVEY §8f row 1")
@@ -137,9 +143,9 @@ class GpuContext:
         if not self.ctx:
             raise NativeLibraryError(f"bf_create failed (device {device}, rank {rank}/{nranks})")
         self.setups = {}
-        local_ranks = {rank} if local_ranks is None else set(local_ranks)
         for cid in self.child_ids:
-            s = _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
+            s = setups[cid] if setups is not None else \
+                _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
             self.setups[cid] = s
             fv = []
             for d in range(self.ndim):
