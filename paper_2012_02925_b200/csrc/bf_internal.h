@@ -15,14 +15,11 @@ namespace bf {
 // Stage-kernel tile: TI x TJ threads, each owning one (i, j) column that
 // marches KC cells along k (2.5-D streaming); 2D blocks use the same tile
 // with a single plane.
-constexpr int TI = 32;
-constexpr int TJ = 8;
-constexpr int NT = TI * TJ;
+constexpr int TI = 32;                   // tile width (one warp per row)
+constexpr int TJ_3D = 16;                // tile rows, 3D (512 threads, 1 CTA/SM)
+constexpr int TJ_2D = 8;                 // tile rows, 2D
 constexpr int HALO = 2;                  // MUSCL stencil half-width
-constexpr int PW = TI + 2 * HALO;        // smem plane width  (36)
-constexpr int PH = TJ + 2 * HALO;        // smem plane height (12)
-constexpr int PLANE = PW * PH;           // cells per smem plane (432)
-constexpr int NSLOT = 5;                 // plane ring depth (k-1..k+2 + prefetch)
+constexpr int NSLOT = 4;                 // plane ring: k, k+1, k+2 resident + k+3 in flight
 
 // Scheme switches (bfgpu.h BF_FLUX_* / BF_LIM_*)
 constexpr int FLUX_ROE = 0;
@@ -69,11 +66,23 @@ struct Consts {
   double ff_exp;                           // 1/(g-1)
   double two_over_gm1;                     // 2/(g-1)   (fast mode only)
   double vl_c;                             // 2*(g*g-1)
+  double inv_gamma, inv_vlc;               // 1/gamma, 1/vl_c (fast mode only)
   double tw;                               // wall temperature
   int has_tw;
   int eps0;                                // epsilon == 0
+  int kappa_m1;                            // kappa == -1 (fast mode drops the zero terms)
   int pad_;
 };
+
+// Field slots of a block arena (each slot fsz doubles, same padded layout).
+constexpr int FW = 0;            // W[b][f] = FW + 6*b + f   (rho u v w p T, ping-pong b)
+constexpr int FQ = 12;           // Q[e]    = FQ + e
+constexpr int FDTV = 17;         // dt / V
+constexpr int FVOL = 18;         // V
+constexpr int FFN = 19;          // face geometry FFN + 4*d + c   (nx, ny, nz, A)
+constexpr int FSRC = 31;         // S*V [5] when present; limiter arrays follow
+__host__ __device__ constexpr int fw(int b, int f) { return FW + 6 * b + f; }
+__host__ __device__ constexpr int ffn(int d, int c) { return FFN + 4 * d + c; }
 
 struct DevBlock {
   int n[3];
@@ -81,16 +90,12 @@ struct DevBlock {
   int ndim;
   int order;        // position of this block in the rank's id order
   int id;
-  int pad_;
+  int psi0;         // first limiter slot (psi[d][pm][v] = psi0 + 10d + 5pm + v), -1: none
   long long sy, sz;
-  double* W[2][6];          // rho u v w p T, ping-pong
-  double* Q[5];
-  double* dtv;
-  double* vol;
-  double* fn[3][4];         // per direction: nx, ny, nz, A at face f stored at cell f
-  double* src[5];           // S*V or null
-  double* psi[3][2][5];     // [dir][plus/minus][var] or null
+  long long fsz;    // doubles per slot
+  double* base;     // arena base, pre-offset to the interior origin
   const unsigned char* bface[6];   // per face, over tangential interior cells
+  __host__ __device__ double* f(int slot) const { return base + (long long)slot * fsz; }
 };
 
 struct Tile {

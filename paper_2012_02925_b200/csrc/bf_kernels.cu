@@ -1,16 +1,19 @@
 // bf_kernels.cu — the per-RK-stage device pipeline.
 //
 // Compiled twice by build.py: -DBF_EXACT=1 -fmad=false (namespace bf_exact,
-// bitwise reference arithmetic) and -DBF_EXACT=0 (namespace bf_fast, FMA).
+// bitwise reference arithmetic) and -DBF_EXACT=0 (namespace bf_fast, FMA and
+// strength reduction).
 //
+//   stage_kernel   fused limiter + MUSCL + face flux + boundary-flux overwrite
+//                  + residual + (stage 0) local dt and sum(R^2) + RK update +
+//                  decode (solver.py:413-753).  2.5-D k-streaming: a CTA owns a
+//                  TI x TJ column tile and marches KC cells in k; the 5
+//                  primitive planes k..k+2 sit in a 4-slot shared-memory ring
+//                  filled by cp.async one plane ahead, so every W value is read
+//                  from HBM once per tile (plus the 2-cell i/j halo).
 //   ghost_kernel   physical-BC ghost fill (solver.py:281-403), same-device
 //                  connected copies and message pack/unpack (halo.py:47-115)
-//                  for every block of the rank in ONE launch;
-//   stage_kernel   fused limiter + MUSCL + face flux + boundary-flux
-//                  overwrite + residual + (stage 0) local dt and sum(R^2) +
-//                  RK update + decode (solver.py:413-753), 2.5-D k-streaming
-//                  over TIxTJ column tiles, plane ring in shared memory filled
-//                  by cp.async;
+//                  for every block of the rank in ONE launch.
 //   reduce_kernel  fixed-order per-block sum of the per-tile sum(R^2) partials.
 #include <cuda_runtime.h>
 
@@ -27,7 +30,7 @@ namespace bf {
 namespace BF_NS {
 
 // ---------------------------------------------------------------------------
-// small helpers
+// helpers
 // ---------------------------------------------------------------------------
 BF_DEV void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -35,63 +38,39 @@ BF_DEV void cp_async8(void* smem, const void* gmem) {
 }
 BF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 BF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+BF_DEV void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 BF_DEV void record_error(unsigned long long* err, unsigned long long key) {
   if (key < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, key);
 }
 
-// Shared-memory layout of the stage kernel (doubles).
-template <int NDIM>
-struct Smem {
+// Compile-time tile geometry and shared-memory layout (in doubles).
+template <int NDIM, int LIM>
+struct Cfg {
+  static constexpr int PC = psi_count<LIM>();
+  static constexpr int TJ = (NDIM == 3 && PC < 2) ? TJ_3D : TJ_2D;
+  static constexpr int NT = TI * TJ;
+  static constexpr int PW = TI + 2 * HALO;                // plane row pitch
+  static constexpr int PH = TJ + 2 * HALO;
+  static constexpr int PLANE = PW * PH;                   // cells per plane
   static constexpr int NS = (NDIM == 3) ? NSLOT : 1;
-  static constexpr int W = 0;                                   // [NS][5][PLANE]
-  static constexpr int PX = W + NS * 5 * PLANE;                 // [2][5][TJ][TI+2]
-  static constexpr int PY = PX + 2 * 5 * TJ * (TI + 2);         // [2][5][TJ+2][TI]
-  static constexpr int FX = PY + 2 * 5 * (TJ + 2) * TI;         // [5][TJ][TI+1]
-  static constexpr int FY = FX + 5 * TJ * (TI + 1);             // [5][TJ+1][TI]
-  static constexpr int TOTAL = FY + 5 * (TJ + 1) * TI;
+  static constexpr int NPX = (TI + 2) * TJ;               // psi_x cells: i = -1..TI
+  static constexpr int NPY = TI * (TJ + 2);               // psi_y cells: j = -1..TJ
+  static constexpr int NFX = (TI + 1) * TJ;               // x faces
+  static constexpr int NFY = TI * (TJ + 1);               // y faces
+  static constexpr int OW = 0;                            // [NS][5][PLANE]
+  static constexpr int OPX = OW + NS * 5 * PLANE;         // [PC][5][NPX]
+  static constexpr int OPY = OPX + PC * 5 * NPX;          // [PC][5][NPY]
+  static constexpr int OFX = OPY + PC * 5 * NPY;          // [5][NFX]
+  static constexpr int OFY = OFX + 5 * NFX;               // [5][NFY]
+  static constexpr int OQ = OFY + 5 * NFY;                // [6][NT] Q0 + dt/V (or V)
+  static constexpr int TOTAL = OQ + 6 * NT;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
+  static constexpr int NITEM = NFX + NFY;                 // x/y face items per plane
+  static constexpr int MAXIT = (NITEM + NT - 1) / NT;
+  static constexpr int NLIM = NPX + NPY;
+  BF_DEV static int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
 };
-
-BF_DEV int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
-
-// Issue the cp.async copies of one k-plane (cross-shaped region: the tile
-// plus a 2-cell halo in i and in j) of the 5 primitive fields.
-template <int NDIM>
-BF_DEV void load_plane(double* sw, const DevBlock& b, const double* const* W, int i0, int j0,
-                       int k) {
-  if (NDIM == 3 && (k < -HALO || k >= b.n[2] + HALO)) return;
-  const long long kofs = (NDIM == 3) ? b.sz * (long long)k : 0;
-  constexpr int ROWS_FULL = TJ * PW;              // rows 0..TJ-1, ii = -2..TI+1
-  constexpr int ROWS_HALO = 2 * HALO * TI;        // rows -2,-1,TJ,TJ+1, ii = 0..TI-1
-  for (int q = threadIdx.x; q < ROWS_FULL + ROWS_HALO; q += NT) {
-    int ii, jj;
-    if (q < ROWS_FULL) {
-      jj = q / PW;
-      ii = q % PW - HALO;
-    } else {
-      const int r = (q - ROWS_FULL) / TI;
-      ii = (q - ROWS_FULL) % TI;
-      jj = (r < HALO) ? r - HALO : TJ + r - HALO;
-    }
-    const int gi = i0 + ii, gj = j0 + jj;
-    if (gi < -HALO || gi >= b.n[0] + HALO || gj < -HALO || gj >= b.n[1] + HALO) continue;
-    const long long off = gi + b.sy * (long long)gj + kofs;
-    const int s = pidx(ii, jj);
-#pragma unroll
-    for (int v = 0; v < 5; ++v) cp_async8(sw + v * PLANE + s, W[v] + off);
-  }
-}
-
-BF_DEV St load_st(const double* p, int stride) {
-  St s;
-  s.r = p[0];
-  s.u = p[stride];
-  s.v = p[2 * stride];
-  s.w = p[3 * stride];
-  s.p = p[4 * stride];
-  return s;
-}
 
 // psi+ / psi- of one cell from its three stencil values (solver.py:419-435):
 // psi+_c = phi(D_{c+1}, D_c), psi-_c = phi(D_c, D_{c+1}).
@@ -100,19 +79,19 @@ BF_DEV void cell_limiter(double wm, double w0, double wp, double& pp, double& pm
   const double lo = w0 - wm;
   const double hi = wp - w0;
   pp = limiter<LIM>(hi, lo);
-  pm = limiter<LIM>(lo, hi);
+  if constexpr (psi_count<LIM>() == 2) pm = limiter<LIM>(lo, hi);
+  else pm = pp;
 }
 
 // MUSCL face states (solver.py:437-474) + flux (physics.py) + area scaling
 // (solver.py:519) + boundary overwrite (solver.py:526-580) for one face.
-// c0..c3 point at var 0 of cells f-2, f-1, f, f+1 (var stride vs); pl/ml and
-// pr/mr at var 0 of psi+/psi- of cells f-1 and f (var stride ps).
-// Returns an error kind (0 ok).
-template <int FLUX>
-BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const double* c3,
-                     int vs, const double* pl, const double* ml, const double* pr,
-                     const double* mr, int ps, double nx, double ny, double nz, double A,
-                     int bkind, double side_sign, const Consts& c, double F[5]) {
+// c0..c3: var-0 pointers of cells f-2, f-1, f, f+1 (var stride vs).
+// ppl/pml: psi+/psi- of cell f-1, ppr/pmr: of cell f (var stride ps).
+template <int FLUX, int LIM>
+BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const double* c3, int vs,
+                     const double* ppl, const double* pml, const double* ppr, const double* pmr,
+                     int ps, double nx, double ny, double nz, double A, int bkind,
+                     double side_sign, const Consts& c, double F[5]) {
   double qL[5], qR[5];
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
@@ -125,8 +104,25 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
       const double dm = wl - c0[v * vs];
       const double d0 = wr - wl;
       const double dp = c3[v * vs] - wr;
-      qL[v] = wl + c.quarter * (c.omk * pl[v * ps] * dm + c.opk * ml[v * ps] * d0);
-      qR[v] = wr - c.quarter * (c.opk * pr[v * ps] * d0 + c.omk * mr[v * ps] * dp);
+      double a_pl = 1.0, a_ml = 1.0, a_pr = 1.0, a_mr = 1.0;
+      if constexpr (psi_count<LIM>() > 0) {
+        a_pl = ppl[v * ps];
+        a_pr = ppr[v * ps];
+        a_ml = pml[v * ps];
+        a_mr = pmr[v * ps];
+      }
+#if BF_EXACT
+      qL[v] = wl + c.quarter * (c.omk * a_pl * dm + c.opk * a_ml * d0);
+      qR[v] = wr - c.quarter * (c.opk * a_pr * d0 + c.omk * a_mr * dp);
+#else
+      if (c.kappa_m1) {
+        qL[v] = wl + c.quarter * (c.omk * a_pl * dm);
+        qR[v] = wr - c.quarter * (c.omk * a_mr * dp);
+      } else {
+        qL[v] = wl + c.quarter * (c.omk * a_pl * dm + c.opk * a_ml * d0);
+        qR[v] = wr - c.quarter * (c.opk * a_pr * d0 + c.omk * a_mr * dp);
+      }
+#endif
     }
   }
   int err = 0;
@@ -153,7 +149,7 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
       F[3] = nz * pw * A;
       F[4] = 0.0;
     } else {
-      const St s1 = load_st(in1, vs);
+      const St s1{in1[0], in1[vs], in1[2 * vs], in1[3 * vs], in1[4 * vs]};
       const St qb = farfield_state(s1, side_sign * nx, side_sign * ny, side_sign * nz, c);
       double Fb[5];
       euler_flux(qb, nx, ny, nz, c, Fb);
@@ -164,584 +160,456 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
   return err;
 }
 
+// Geometry and boundary code of one face, loaded early (ahead of its use).
+struct FaceGeo {
+  double nx, ny, nz, A;
+  int bk;
+  double sgn;
+};
+
+BF_DEV void load_geo(FaceGeo& g, const DevBlock& b, int d, long long off, bool on, int bface,
+                     int bk_side) {
+  if (on) {
+    const double* fn = b.base + (long long)ffn(d, 0) * b.fsz + off;
+    g.nx = __ldg(fn);
+    g.ny = __ldg(fn + b.fsz);
+    g.nz = __ldg(fn + 2 * b.fsz);
+    g.A = __ldg(fn + 3 * b.fsz);
+  } else {
+    g.nx = g.ny = g.nz = 0.0;
+    g.A = 0.0;
+  }
+  g.bk = BFACE_NONE;
+  g.sgn = 1.0;
+  if (on && bk_side >= 0) {
+    g.bk = b.bface[2 * d + bk_side][bface];
+    g.sgn = bk_side == 0 ? -1.0 : 1.0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the fused stage kernel
 // ---------------------------------------------------------------------------
 template <int NDIM, int FLUX, int LIM>
-__global__ void __launch_bounds__(NT, 1) stage_kernel(const StageArgs a) {
-  using S = Smem<NDIM>;
+__global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const StageArgs a) {
+  using K = Cfg<NDIM, LIM>;
+  constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW, PC = K::PC;
   extern __shared__ __align__(16) double smem[];
-  double* sW = smem + S::W;
-  double* sPX = smem + S::PX;
-  double* sPY = smem + S::PY;
-  double* sFX = smem + S::FX;
-  double* sFY = smem + S::FY;
-  constexpr int PXS = 5 * TJ * (TI + 2);      // plus->minus offset
-  constexpr int PYS = 5 * (TJ + 2) * TI;
+  double* const sW = smem + K::OW;
+  double* const sPX = smem + K::OPX;
+  double* const sPY = smem + K::OPY;
+  double* const sFX = smem + K::OFX;
+  double* const sFY = smem + K::OFY;
+  double* const sQ = smem + K::OQ;
 
   const Tile t = a.tiles[blockIdx.x];
-  const DevBlock& b = a.blocks[t.block];
+  const DevBlock b = a.blocks[t.block];     // local copy: no aliasing reloads
   const Consts& c = a.c;
-  const int tx = threadIdx.x % TI, ty = threadIdx.x / TI;
+  const int tid = threadIdx.x;
+  const int tx = tid % TI, ty = tid / TI;
   const int i0 = t.i0, j0 = t.j0, k0 = t.k0;
   const int ni = b.n[0], nj = b.n[1], nk = b.n[2];
+  const long long sy = b.sy, sz = b.sz, fsz = b.fsz;
   const int i = i0 + tx, j = j0 + ty;
   const bool col_on = (i < ni) && (j < nj);
-  const bool stage0 = a.flags & F_STAGE0;
-  const bool last = a.flags & F_LAST;
-  const bool psi_load = a.flags & F_PSI_LOAD;
-  const bool psi_store = a.flags & F_PSI_STORE;
-  const double* const* Win = b.W[a.cur];
-  double* const* Wout = b.W[a.cur ^ 1];
+  const int flags = a.flags;
+  const bool stage0 = flags & F_STAGE0;
+  const bool last = flags & F_LAST;
+  const bool psi_load = (PC > 0) && (flags & F_PSI_LOAD);
+  const bool psi_store = (PC > 0) && (flags & F_PSI_STORE);
   const int stage = a.stage;
+  const double* const Win = b.base + (long long)fw(a.cur, 0) * fsz;
+  double* const Wout = b.base + (long long)fw(a.cur ^ 1, 0) * fsz;
+  const long long colofs = i + sy * (long long)j;
+
+  auto slot = [&](int k) -> double* {
+    if constexpr (NDIM == 3) return sW + ((k - k0 + 4 * NSLOT) % NSLOT) * 5 * PLANE;
+    else return sW;
+  };
+  auto psi_ptr = [&](int d, int pm, int v) -> double* {
+    return b.base + (long long)(b.psi0 + 10 * d + 5 * pm + v) * fsz;
+  };
+
+  // issue the cp.async copies of one plane (tile + 2-cell i/j halo, cross shape)
+  auto load_plane = [&](int k) {
+    if (NDIM == 3 && (k < -HALO || k >= nk + HALO)) return;
+    double* dst = slot(k);
+    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
+    constexpr int ROWS_FULL = TJ * PW;
+    constexpr int ROWS_HALO = 2 * HALO * TI;
+    for (int q = tid; q < ROWS_FULL + ROWS_HALO; q += NT) {
+      int ii, jj;
+      if (q < ROWS_FULL) {
+        jj = q / PW;
+        ii = q % PW - HALO;
+      } else {
+        const int r = (q - ROWS_FULL) / TI;
+        ii = (q - ROWS_FULL) % TI;
+        jj = (r < HALO) ? r - HALO : TJ + r - HALO;
+      }
+      const int gi = i0 + ii, gj = j0 + jj;
+      if (gi < -HALO || gi >= ni + HALO || gj < -HALO || gj >= nj + HALO) continue;
+      const double* src = Win + gi + sy * (long long)gj + kofs;
+      const int s = K::pidx(ii, jj);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) cp_async8(dst + v * PLANE + s, src + v * fsz);
+    }
+  };
+  // Q0 (+ dt/V or V) of the own cell, staged per thread
+  auto load_q = [&](int k) {
+    if (!col_on) return;
+    const long long o = colofs + ((NDIM == 3) ? sz * (long long)k : 0);
+    const double* q = b.base + (long long)FQ * fsz + o;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) cp_async8(sQ + v * NT + tid, q + v * fsz);
+    const double* dv = b.base + (long long)(stage0 ? FVOL : FDTV) * fsz + o;
+    cp_async8(sQ + 5 * NT + tid, dv);
+  };
+
+  // ---- x/y face items of this thread (fixed for all k) ----------------------
+  // item q < NFX: x face (row = q / (TI+1), f = q % (TI+1)); else y face
+  int it_q[K::MAXIT];
+#pragma unroll
+  for (int r = 0; r < K::MAXIT; ++r) it_q[r] = tid + r * NT;
 
   double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
-  // plane slot of k (ring of NS planes)
-  auto slot = [&](int k) -> double* {
-    if constexpr (NDIM == 3) return sW + (((k - k0 + 2 * NSLOT) % NSLOT) * 5 * PLANE);
-    else return sW;
-  };
+  // ---- z-direction carried state (3D) -------------------------------------------
+  double wm1[5] = {0, 0, 0, 0, 0};  // W(k-1), own column
+  double pzp[5], pzm[5];            // psi+/psi- of cell k
+  double fz[5];                     // flux at face k
+#pragma unroll
+  for (int v = 0; v < 5; ++v) pzp[v] = pzm[v] = fz[v] = 0.0;
 
-  // z-direction carried state (NDIM == 3)
-  double pzp[5], pzm[5];    // psi+/psi- at cell k (own column)
-  double fz[5];             // flux at face k (own column)
-
-  const int kfirst = (NDIM == 3) ? -1 : 0;
   if constexpr (NDIM == 3) {
-    // prologue: planes k0-2 .. k0+1
-    for (int k = k0 - 2; k <= k0 + 1; ++k) load_plane<3>(slot(k), b, Win, i0, j0, k);
+    if (col_on) {
+      const long long o = colofs + sz * (long long)(k0 - 2);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) wm1[v] = Win[v * fsz + o];
+    }
+    load_plane(k0 - 1);
+    load_plane(k0);
+    load_plane(k0 + 1);
     cp_async_commit();
   } else {
-    load_plane<2>(sW, b, Win, i0, j0, 0);
+    load_plane(0);
+    load_q(0);
     cp_async_commit();
   }
 
+  const int kfirst = (NDIM == 3) ? -1 : 0;
   for (int kk = kfirst; kk < t.kc; ++kk) {
     const int k = k0 + kk;
+    const bool xy = kk >= 0;
+    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();   // B0: planes k..k+2 resident; everyone done with iteration k-1
     if constexpr (NDIM == 3) {
-      if (kk + 1 < t.kc) load_plane<3>(slot(k + 3), b, Win, i0, j0, k + 3);
+      if (xy) load_q(k);
+      cp_async_commit();
+      if (kk + 1 < t.kc) load_plane(k + 3);
       cp_async_commit();
     }
-    const bool xy = (kk >= 0);
-    const long long kofs = (NDIM == 3) ? b.sz * (long long)k : 0;
     const double* pk = slot(k);
+    const int s0 = K::pidx(tx, ty);
 
-    // ---- P1: limiters -------------------------------------------------------
+    // early geometry loads for this iteration's faces
+    FaceGeo gz;
     if constexpr (NDIM == 3) {
-      // psi_z of cell k+1 (and, in the prologue iteration, of cell k = k0-1)
-      const double* pm1 = slot(k - 1);
+      const int fk = k + 1;
+      load_geo(gz, b, 2, colofs + sz * (long long)fk, col_on, i + ni * j,
+               fk == 0 ? 0 : (fk == nk ? 1 : -1));
+    }
+    FaceGeo gi_[K::MAXIT];
+#pragma unroll
+    for (int r = 0; r < K::MAXIT; ++r) {
+      const int q = it_q[r];
+      if (!xy || q >= K::NITEM) {
+        gi_[r].A = 0.0;
+        continue;
+      }
+      if (q < K::NFX) {
+        const int row = q / (TI + 1), f = q % (TI + 1);
+        const int gi = i0 + f, gj = j0 + row;
+        const bool on = gi <= ni && gj < nj;
+        load_geo(gi_[r], b, 0, gi + sy * (long long)gj + kofs, on, gj + nj * (NDIM == 3 ? k : 0),
+                 gi == 0 ? 0 : (gi == ni ? 1 : -1));
+      } else {
+        const int q2 = q - K::NFX;
+        const int f = q2 / TI, col = q2 % TI;
+        const int gi = i0 + col, gj = j0 + f;
+        const bool on = gj <= nj && gi < ni;
+        load_geo(gi_[r], b, 1, gi + sy * (long long)gj + kofs, on, gi + ni * (NDIM == 3 ? k : 0),
+                 gj == 0 ? 0 : (gj == nj ? 1 : -1));
+      }
+    }
+
+    // ---- P1: x / y limiters of plane k -> smem -------------------------------------
+    if (xy && PC > 0) {
+      for (int q = tid; q < K::NLIM; q += NT) {
+        int gi, gj, d, o, sc, step;
+        if (q < K::NPX) {
+          const int row = q / (TI + 2), cc = q % (TI + 2) - 1;    // cell cc in [-1, TI]
+          gi = i0 + cc;
+          gj = j0 + row;
+          d = 0;
+          o = q;
+          sc = K::pidx(cc, row);
+          step = 1;
+        } else {
+          const int q2 = q - K::NPX;
+          const int row = q2 / TI - 1, cc = q2 % TI;             // row in [-1, TJ]
+          gi = i0 + cc;
+          gj = j0 + row;
+          d = 1;
+          o = q2;
+          sc = K::pidx(cc, row);
+          step = PW;
+        }
+        double* dstp = (d == 0) ? sPX + o : sPY + o;
+        const int vstride = (d == 0) ? K::NPX : K::NPY;
+        const bool in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
+                                       : (gj >= -1 && gj <= nj && gi < ni);
+        const long long go = gi + sy * (long long)gj + kofs;
+        if (psi_load) {
+          if (in_range) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) {
+              dstp[v * vstride] = psi_ptr(d, 0, v)[go];
+              if constexpr (PC == 2) dstp[(5 + v) * vstride] = psi_ptr(d, 1, v)[go];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            double pp, pm;
+            cell_limiter<LIM>(pk[v * PLANE + sc - step], pk[v * PLANE + sc],
+                              pk[v * PLANE + sc + step], pp, pm);
+            dstp[v * vstride] = pp;
+            if constexpr (PC == 2) dstp[(5 + v) * vstride] = pm;
+            if (psi_store && in_range) {
+              psi_ptr(d, 0, v)[go] = pp;
+              psi_ptr(d, 1, v)[go] = pm;
+            }
+          }
+        }
+      }
+    }
+
+    // ---- z limiter of cell k+1 and z face k+1 (own column, registers) ------------
+    double Fz[5] = {0, 0, 0, 0, 0};
+    if constexpr (NDIM == 3) {
       const double* p0 = slot(k);
       const double* p1 = slot(k + 1);
       const double* p2 = slot(k + 2);
-      const int s = pidx(tx, ty);
-      const long long cz = i + b.sy * (long long)j;
+      double nzp[5], nzm[5];
+      const long long cz = colofs + sz * (long long)(k + 1);
       if (kk == kfirst) {
+        // psi_z of cell k (= k0-1) from W(k-1) (regs), W(k), W(k+1)
+        const long long czk = colofs + sz * (long long)k;
         if (psi_load) {
-          if (col_on) {
 #pragma unroll
-            for (int v = 0; v < 5; ++v) {
-              pzp[v] = b.psi[2][0][v][cz + b.sz * (long long)k];
-              pzm[v] = b.psi[2][1][v][cz + b.sz * (long long)k];
-            }
+          for (int v = 0; v < 5; ++v) {
+            pzp[v] = col_on ? psi_ptr(2, 0, v)[czk] : 0.0;
+            pzm[v] = (PC == 2) ? (col_on ? psi_ptr(2, 1, v)[czk] : 0.0) : pzp[v];
           }
         } else {
 #pragma unroll
-          for (int v = 0; v < 5; ++v)
-            cell_limiter<LIM>(pm1[v * PLANE + s], p0[v * PLANE + s], p1[v * PLANE + s], pzp[v],
-                              pzm[v]);
-          if (psi_store && col_on && k >= -1) {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-              b.psi[2][0][v][cz + b.sz * (long long)k] = pzp[v];
-              b.psi[2][1][v][cz + b.sz * (long long)k] = pzm[v];
+          for (int v = 0; v < 5; ++v) {
+            cell_limiter<LIM>(wm1[v], p0[v * PLANE + s0], p1[v * PLANE + s0], pzp[v], pzm[v]);
+            if (psi_store && col_on && k >= -1) {
+              psi_ptr(2, 0, v)[czk] = pzp[v];
+              psi_ptr(2, 1, v)[czk] = pzm[v];
             }
           }
         }
       }
-      // psi of cell k+1 stored in registers as "next"
-      double nzp[5], nzm[5];
       if (psi_load) {
-        if (col_on) {
 #pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            nzp[v] = b.psi[2][0][v][cz + b.sz * (long long)(k + 1)];
-            nzm[v] = b.psi[2][1][v][cz + b.sz * (long long)(k + 1)];
-          }
+        for (int v = 0; v < 5; ++v) {
+          nzp[v] = col_on ? psi_ptr(2, 0, v)[cz] : 0.0;
+          nzm[v] = (PC == 2) ? (col_on ? psi_ptr(2, 1, v)[cz] : 0.0) : nzp[v];
         }
       } else {
 #pragma unroll
-        for (int v = 0; v < 5; ++v)
-          cell_limiter<LIM>(p0[v * PLANE + s], p1[v * PLANE + s], p2[v * PLANE + s], nzp[v],
+        for (int v = 0; v < 5; ++v) {
+          cell_limiter<LIM>(p0[v * PLANE + s0], p1[v * PLANE + s0], p2[v * PLANE + s0], nzp[v],
                             nzm[v]);
-        if (psi_store && col_on && k + 1 <= nk) {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            b.psi[2][0][v][cz + b.sz * (long long)(k + 1)] = nzp[v];
-            b.psi[2][1][v][cz + b.sz * (long long)(k + 1)] = nzm[v];
+          if (psi_store && col_on && k + 1 <= nk) {
+            psi_ptr(2, 0, v)[cz] = nzp[v];
+            psi_ptr(2, 1, v)[cz] = nzm[v];
           }
         }
       }
-      // z face k+1: cells k-1, k, k+1, k+2; psi of cells k and k+1
+      // z face k+1 from a unit-stride copy of the own-column stencil
       {
-        const int fk = k + 1;
-        double F[5];
-        const long long fo = cz + b.sz * (long long)fk;
-        double nx = 0, ny = 0, nz = 0, A = 0;
-        if (col_on) {
-          nx = b.fn[2][0][fo];
-          ny = b.fn[2][1][fo];
-          nz = b.fn[2][2][fo];
-          A = b.fn[2][3][fo];
+        double st[4][5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          st[0][v] = wm1[v];
+          st[1][v] = p0[v * PLANE + s0];
+          st[2][v] = p1[v * PLANE + s0];
+          st[3][v] = p2[v * PLANE + s0];
         }
-        int bk = BFACE_NONE;
-        double sgn = 1.0;
-        if (col_on && fk == 0) {
-          bk = b.bface[4][i + ni * j];
-          sgn = -1.0;
-        } else if (col_on && fk == nk) {
-          bk = b.bface[5][i + ni * j];
-        }
-        const int e = face_flux<FLUX>(pm1 + s, p0 + s, p1 + s, p2 + s, PLANE, pzp, pzm, nzp,
-                                      nzm, 1, nx, ny, nz, A, bk, sgn, c, F);
-        if (e && col_on) {
+        const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, pzp, pzm, nzp, nzm, 1,
+                                            gz.nx, gz.ny, gz.nz, gz.A, gz.bk, gz.sgn, c, Fz);
+        if (ez && col_on) {
+          const int fk = k + 1;
           const unsigned long long lin =
               ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
-          record_error(a.err, make_err_key(stage, 0, b.order, 2, e, lin));
+          record_error(a.err, make_err_key(stage, 0, b.order, 2, ez, lin));
         }
-        if (kk == kfirst) {
+      }
 #pragma unroll
-          for (int v = 0; v < 5; ++v) fz[v] = F[v];
-        }
-        // carry limiter state
+      for (int v = 0; v < 5; ++v) {
+        pzp[v] = nzp[v];
+        pzm[v] = nzm[v];
+      }
+      if (kk == kfirst) {
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          pzp[v] = nzp[v];
-          pzm[v] = nzm[v];
+          fz[v] = Fz[v];
+          wm1[v] = p0[v * PLANE + s0];
         }
-        if (kk == kfirst) continue;   // prologue iteration: z only
-        // x / y limiters for plane k
-        if (!psi_load) {
-          for (int q = threadIdx.x; q < TJ * (TI + 2) + (TJ + 2) * TI; q += NT) {
-            if (q < TJ * (TI + 2)) {
-              const int row = q / (TI + 2), cc = q % (TI + 2) - 1;   // cell cc in [-1, TI]
-              const int sc = pidx(cc, row);
-              const int o = row * (TI + 2) + (cc + 1);
-#pragma unroll
-              for (int v = 0; v < 5; ++v)
-                cell_limiter<LIM>(pk[v * PLANE + sc - 1], pk[v * PLANE + sc],
-                                  pk[v * PLANE + sc + 1], sPX[v * TJ * (TI + 2) + o],
-                                  sPX[PXS + v * TJ * (TI + 2) + o]);
-              const int gi = i0 + cc, gj = j0 + row;
-              if (psi_store && gi >= -1 && gi <= ni && gj < nj) {
-                const long long go = gi + b.sy * (long long)gj + kofs;
-#pragma unroll
-                for (int v = 0; v < 5; ++v) {
-                  b.psi[0][0][v][go] = sPX[v * TJ * (TI + 2) + o];
-                  b.psi[0][1][v][go] = sPX[PXS + v * TJ * (TI + 2) + o];
-                }
-              }
-            } else {
-              const int q2 = q - TJ * (TI + 2);
-              const int row = q2 / TI - 1, cc = q2 % TI;            // row in [-1, TJ]
-              const int sc = pidx(cc, row);
-              const int o = (row + 1) * TI + cc;
-#pragma unroll
-              for (int v = 0; v < 5; ++v)
-                cell_limiter<LIM>(pk[v * PLANE + sc - PW], pk[v * PLANE + sc],
-                                  pk[v * PLANE + sc + PW], sPY[v * (TJ + 2) * TI + o],
-                                  sPY[PYS + v * (TJ + 2) * TI + o]);
-              const int gi = i0 + cc, gj = j0 + row;
-              if (psi_store && gj >= -1 && gj <= nj && gi < ni) {
-                const long long go = gi + b.sy * (long long)gj + kofs;
-#pragma unroll
-                for (int v = 0; v < 5; ++v) {
-                  b.psi[1][0][v][go] = sPY[v * (TJ + 2) * TI + o];
-                  b.psi[1][1][v][go] = sPY[PYS + v * (TJ + 2) * TI + o];
-                }
-              }
-            }
-          }
-        } else {
-          for (int q = threadIdx.x; q < TJ * (TI + 2) + (TJ + 2) * TI; q += NT) {
-            int gi, gj, o, d;
-            if (q < TJ * (TI + 2)) {
-              const int row = q / (TI + 2), cc = q % (TI + 2) - 1;
-              gi = i0 + cc;
-              gj = j0 + row;
-              o = row * (TI + 2) + (cc + 1);
-              d = 0;
-              if (gi < -1 || gi > ni || gj >= nj) continue;
-            } else {
-              const int q2 = q - TJ * (TI + 2);
-              const int row = q2 / TI - 1, cc = q2 % TI;
-              gi = i0 + cc;
-              gj = j0 + row;
-              o = (row + 1) * TI + cc;
-              d = 1;
-              if (gj < -1 || gj > nj || gi >= ni) continue;
-            }
-            const long long go = gi + b.sy * (long long)gj + kofs;
-            double* dp = (d == 0) ? sPX : sPY;
-            const int stride = (d == 0) ? TJ * (TI + 2) : (TJ + 2) * TI;
-            const int ms = (d == 0) ? PXS : PYS;
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-              dp[v * stride + o] = b.psi[d][0][v][go];
-              dp[ms + v * stride + o] = b.psi[d][1][v][go];
-            }
-          }
-        }
-        __syncthreads();
-        // ---- P2: x / y face fluxes of plane k ------------------------------------
-        for (int q = threadIdx.x; q < TJ * (TI + 1) + (TJ + 1) * TI; q += NT) {
-          double Fq[5];
-          if (q < TJ * (TI + 1)) {
-            const int row = q / (TI + 1), f = q % (TI + 1);      // face f: cells f-1 | f
-            const int gi = i0 + f, gj = j0 + row;
-            const bool on = gi <= ni && gj < nj;
-            double nx = 0, ny = 0, nz = 0, A = 0;
-            int bk = BFACE_NONE;
-            double sgn = 1.0;
-            if (on) {
-              const long long fo = gi + b.sy * (long long)gj + kofs;
-              nx = b.fn[0][0][fo];
-              ny = b.fn[0][1][fo];
-              nz = b.fn[0][2][fo];
-              A = b.fn[0][3][fo];
-              if (gi == 0) {
-                bk = b.bface[0][gj + nj * (NDIM == 3 ? k : 0)];
-                sgn = -1.0;
-              } else if (gi == ni) {
-                bk = b.bface[1][gj + nj * (NDIM == 3 ? k : 0)];
-              }
-            }
-            const int sc = pidx(f, row);
-            const int po = row * (TI + 2) + f;      // psi cell f-1 at index (f-1)+1
-            const int e = face_flux<FLUX>(pk + sc - 2, pk + sc - 1, pk + sc, pk + sc + 1, PLANE,
-                                          sPX + po, sPX + PXS + po, sPX + po + 1,
-                                          sPX + PXS + po + 1, TJ * (TI + 2), nx, ny, nz, A, bk,
-                                          sgn, c, Fq);
-            if (e && on) {
-              const unsigned long long lin =
-                  ((unsigned long long)gi * nj + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
-                  (NDIM == 3 ? k : 0);
-              record_error(a.err, make_err_key(stage, 0, b.order, 0, e, lin));
-            }
-#pragma unroll
-            for (int v = 0; v < 5; ++v) sFX[v * TJ * (TI + 1) + row * (TI + 1) + f] = Fq[v];
-          } else {
-            const int q2 = q - TJ * (TI + 1);
-            const int f = q2 / TI, col = q2 % TI;          // face row f: cells f-1 | f
-            const int gi = i0 + col, gj = j0 + f;
-            const bool on = gj <= nj && gi < ni;
-            double nx = 0, ny = 0, nz = 0, A = 0;
-            int bk = BFACE_NONE;
-            double sgn = 1.0;
-            if (on) {
-              const long long fo = gi + b.sy * (long long)gj + kofs;
-              nx = b.fn[1][0][fo];
-              ny = b.fn[1][1][fo];
-              nz = b.fn[1][2][fo];
-              A = b.fn[1][3][fo];
-              if (gj == 0) {
-                bk = b.bface[2][gi + ni * (NDIM == 3 ? k : 0)];
-                sgn = -1.0;
-              } else if (gj == nj) {
-                bk = b.bface[3][gi + ni * (NDIM == 3 ? k : 0)];
-              }
-            }
-            const int sc = pidx(col, f);
-            const int po = f * TI + col;             // psi row f-1 at index ((f-1)+1)*TI
-            const int e = face_flux<FLUX>(pk + sc - 2 * PW, pk + sc - PW, pk + sc, pk + sc + PW,
-                                          PLANE, sPY + po, sPY + PYS + po, sPY + po + TI,
-                                          sPY + PYS + po + TI, (TJ + 2) * TI, nx, ny, nz, A, bk,
-                                          sgn, c, Fq);
-            if (e && on) {
-              const unsigned long long lin =
-                  ((unsigned long long)gi * (nj + 1) + gj) *
-                      (unsigned long long)(NDIM == 3 ? nk : 1) +
-                  (NDIM == 3 ? k : 0);
-              record_error(a.err, make_err_key(stage, 0, b.order, 1, e, lin));
-            }
-#pragma unroll
-            for (int v = 0; v < 5; ++v) sFY[v * (TJ + 1) * TI + f * TI + col] = Fq[v];
-          }
-        }
-        __syncthreads();
-        // ---- P3: residual, dt, update of cell (i, j, k) ----------------------------
-        if (col_on) {
-          double R[5];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            const double fxl = sFX[v * TJ * (TI + 1) + ty * (TI + 1) + tx];
-            const double fxh = sFX[v * TJ * (TI + 1) + ty * (TI + 1) + tx + 1];
-            const double fyl = sFY[v * (TJ + 1) * TI + ty * TI + tx];
-            const double fyh = sFY[v * (TJ + 1) * TI + (ty + 1) * TI + tx];
-            R[v] = ((0.0 + (fxh - fxl)) + (fyh - fyl)) + (F[v] - fz[v]);
-          }
-          const long long co = i + b.sy * (long long)j + kofs;
-          if (a.flags & F_SOURCE) {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) R[v] = R[v] - b.src[v][co];
-          }
-          double dtv;
-          const int s0 = pidx(tx, ty);
-          if (stage0) {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) rsum[v] += R[v] * R[v];
-            const double rho = pk[s0], u = pk[PLANE + s0], v = pk[2 * PLANE + s0],
-                         w = pk[3 * PLANE + s0], p = pk[4 * PLANE + s0];
-            const double snd = sqrt(c.gamma * p / rho);
-            double lam = 0.0;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-#pragma unroll
-              for (int hi = 0; hi < 2; ++hi) {
-                const long long fo = co + (hi ? (d == 0 ? 1 : (d == 1 ? b.sy : b.sz)) : 0);
-                const double nx = b.fn[d][0][fo], ny = b.fn[d][1][fo], nz = b.fn[d][2][fo],
-                             A = b.fn[d][3][fo];
-                lam = lam + (fabs(u * nx + v * ny + w * nz) + snd) * A;
-              }
-            }
-            const double vol = b.vol[co];
-            dtv = c.cfl * vol / lam / vol;
-            b.dtv[co] = dtv;
-          } else {
-            dtv = b.dtv[co];
-          }
-          double qn[5];
-          const double adt = a.alpha * dtv;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) qn[v] = b.Q[v][co] - adt * R[v];
-          const double uu = qn[1] / qn[0], vv = qn[2] / qn[0], ww = qn[3] / qn[0];
-          const double pp = c.gm1 * (qn[4] - 0.5 * (qn[1] * uu + qn[2] * vv + qn[3] * ww));
-          if (qn[0] <= 0.0 || pp <= 0.0) {
-            const unsigned long long lin = ((unsigned long long)i * nj + j) * nk + k;
-            record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
-          }
-          Wout[0][co] = qn[0];
-          Wout[1][co] = uu;
-          Wout[2][co] = vv;
-          Wout[3][co] = ww;
-          Wout[4][co] = pp;
-          if (last) {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) b.Q[v][co] = qn[v];
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) fz[v] = F[v];
+        continue;   // prologue iteration: z only
       }
-    } else {
-      // ------------------------------ 2D --------------------------------------
-      if (!psi_load) {
-        for (int q = threadIdx.x; q < TJ * (TI + 2) + (TJ + 2) * TI; q += NT) {
-          if (q < TJ * (TI + 2)) {
-            const int row = q / (TI + 2), cc = q % (TI + 2) - 1;
-            const int sc = pidx(cc, row);
-            const int o = row * (TI + 2) + (cc + 1);
+    }
+
+    __syncthreads();   // B1: psi of plane k complete
+
+    // ---- P2: x / y face fluxes of plane k -> smem ----------------------------------
 #pragma unroll
-            for (int v = 0; v < 5; ++v)
-              cell_limiter<LIM>(pk[v * PLANE + sc - 1], pk[v * PLANE + sc], pk[v * PLANE + sc + 1],
-                                sPX[v * TJ * (TI + 2) + o], sPX[PXS + v * TJ * (TI + 2) + o]);
-            const int gi = i0 + cc, gj = j0 + row;
-            if (psi_store && gi >= -1 && gi <= ni && gj < nj) {
-              const long long go = gi + b.sy * (long long)gj;
-#pragma unroll
-              for (int v = 0; v < 5; ++v) {
-                b.psi[0][0][v][go] = sPX[v * TJ * (TI + 2) + o];
-                b.psi[0][1][v][go] = sPX[PXS + v * TJ * (TI + 2) + o];
-              }
-            }
-          } else {
-            const int q2 = q - TJ * (TI + 2);
-            const int row = q2 / TI - 1, cc = q2 % TI;
-            const int sc = pidx(cc, row);
-            const int o = (row + 1) * TI + cc;
-#pragma unroll
-            for (int v = 0; v < 5; ++v)
-              cell_limiter<LIM>(pk[v * PLANE + sc - PW], pk[v * PLANE + sc],
-                                pk[v * PLANE + sc + PW], sPY[v * (TJ + 2) * TI + o],
-                                sPY[PYS + v * (TJ + 2) * TI + o]);
-            const int gi = i0 + cc, gj = j0 + row;
-            if (psi_store && gj >= -1 && gj <= nj && gi < ni) {
-              const long long go = gi + b.sy * (long long)gj;
-#pragma unroll
-              for (int v = 0; v < 5; ++v) {
-                b.psi[1][0][v][go] = sPY[v * (TJ + 2) * TI + o];
-                b.psi[1][1][v][go] = sPY[PYS + v * (TJ + 2) * TI + o];
-              }
-            }
-          }
+    for (int r = 0; r < K::MAXIT; ++r) {
+      const int q = it_q[r];
+      if (q >= K::NITEM) continue;
+      double Fq[5];
+      if (q < K::NFX) {
+        const int row = q / (TI + 1), f = q % (TI + 1);
+        const int sc = K::pidx(f, row);
+        const int po = row * (TI + 2) + f;          // psi of cell f-1 (index (f-1)+1)
+        const int e = face_flux<FLUX, LIM>(pk + sc - 2, pk + sc - 1, pk + sc, pk + sc + 1, PLANE,
+                                           sPX + po, sPX + (PC == 2 ? 5 * K::NPX : 0) + po,
+                                           sPX + po + 1, sPX + (PC == 2 ? 5 * K::NPX : 0) + po + 1,
+                                           K::NPX, gi_[r].nx, gi_[r].ny, gi_[r].nz, gi_[r].A,
+                                           gi_[r].bk, gi_[r].sgn, c, Fq);
+        const int gi = i0 + f, gj = j0 + row;
+        if (e && gi <= ni && gj < nj) {
+          const unsigned long long lin =
+              ((unsigned long long)gi * nj + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
+              (NDIM == 3 ? k : 0);
+          record_error(a.err, make_err_key(stage, 0, b.order, 0, e, lin));
         }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) sFX[v * K::NFX + q] = Fq[v];
       } else {
-        for (int q = threadIdx.x; q < TJ * (TI + 2) + (TJ + 2) * TI; q += NT) {
-          int gi, gj, o, d;
-          if (q < TJ * (TI + 2)) {
-            const int row = q / (TI + 2), cc = q % (TI + 2) - 1;
-            gi = i0 + cc;
-            gj = j0 + row;
-            o = row * (TI + 2) + (cc + 1);
-            d = 0;
-            if (gi < -1 || gi > ni || gj >= nj) continue;
-          } else {
-            const int q2 = q - TJ * (TI + 2);
-            const int row = q2 / TI - 1, cc = q2 % TI;
-            gi = i0 + cc;
-            gj = j0 + row;
-            o = (row + 1) * TI + cc;
-            d = 1;
-            if (gj < -1 || gj > nj || gi >= ni) continue;
-          }
-          const long long go = gi + b.sy * (long long)gj;
-          double* dp = (d == 0) ? sPX : sPY;
-          const int stride = (d == 0) ? TJ * (TI + 2) : (TJ + 2) * TI;
-          const int ms = (d == 0) ? PXS : PYS;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            dp[v * stride + o] = b.psi[d][0][v][go];
-            dp[ms + v * stride + o] = b.psi[d][1][v][go];
-          }
+        const int q2 = q - K::NFX;
+        const int f = q2 / TI, col = q2 % TI;
+        const int sc = K::pidx(col, f);
+        const int po = f * TI + col;                // psi of row f-1 (index (f-1)+1)
+        const int e = face_flux<FLUX, LIM>(pk + sc - 2 * PW, pk + sc - PW, pk + sc, pk + sc + PW,
+                                           PLANE, sPY + po, sPY + (PC == 2 ? 5 * K::NPY : 0) + po,
+                                           sPY + po + TI, sPY + (PC == 2 ? 5 * K::NPY : 0) + po + TI,
+                                           K::NPY, gi_[r].nx, gi_[r].ny, gi_[r].nz, gi_[r].A,
+                                           gi_[r].bk, gi_[r].sgn, c, Fq);
+        const int gi = i0 + col, gj = j0 + f;
+        if (e && gj <= nj && gi < ni) {
+          const unsigned long long lin =
+              ((unsigned long long)gi * (nj + 1) + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
+              (NDIM == 3 ? k : 0);
+          record_error(a.err, make_err_key(stage, 0, b.order, 1, e, lin));
         }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) sFY[v * K::NFY + q2] = Fq[v];
       }
-      __syncthreads();
-      for (int q = threadIdx.x; q < TJ * (TI + 1) + (TJ + 1) * TI; q += NT) {
-        double Fq[5];
-        if (q < TJ * (TI + 1)) {
-          const int row = q / (TI + 1), f = q % (TI + 1);
-          const int gi = i0 + f, gj = j0 + row;
-          const bool on = gi <= ni && gj < nj;
-          double nx = 0, ny = 0, nz = 0, A = 0;
-          int bk = BFACE_NONE;
-          double sgn = 1.0;
-          if (on) {
-            const long long fo = gi + b.sy * (long long)gj;
-            nx = b.fn[0][0][fo];
-            ny = b.fn[0][1][fo];
-            nz = b.fn[0][2][fo];
-            A = b.fn[0][3][fo];
-            if (gi == 0) {
-              bk = b.bface[0][gj];
-              sgn = -1.0;
-            } else if (gi == ni) {
-              bk = b.bface[1][gj];
-            }
-          }
-          const int sc = pidx(f, row);
-          const int po = row * (TI + 2) + f;
-          const int e = face_flux<FLUX>(pk + sc - 2, pk + sc - 1, pk + sc, pk + sc + 1, PLANE,
-                                        sPX + po, sPX + PXS + po, sPX + po + 1, sPX + PXS + po + 1,
-                                        TJ * (TI + 2), nx, ny, nz, A, bk, sgn, c, Fq);
-          if (e && on) {
-            const unsigned long long lin = (unsigned long long)gi * nj + gj;
-            record_error(a.err, make_err_key(stage, 0, b.order, 0, e, lin));
-          }
+    }
+    if constexpr (NDIM == 3) cp_async_wait_1();   // own Q0 / dt staging landed
+    else cp_async_wait_all();
+    __syncthreads();   // B2: face fluxes of plane k complete
+
+    // ---- P3: residual, dt, update of cell (i, j, k) --------------------------------
+    if (col_on) {
+      double R[5];
 #pragma unroll
-          for (int v = 0; v < 5; ++v) sFX[v * TJ * (TI + 1) + row * (TI + 1) + f] = Fq[v];
-        } else {
-          const int q2 = q - TJ * (TI + 1);
-          const int f = q2 / TI, col = q2 % TI;
-          const int gi = i0 + col, gj = j0 + f;
-          const bool on = gj <= nj && gi < ni;
-          double nx = 0, ny = 0, nz = 0, A = 0;
-          int bk = BFACE_NONE;
-          double sgn = 1.0;
-          if (on) {
-            const long long fo = gi + b.sy * (long long)gj;
-            nx = b.fn[1][0][fo];
-            ny = b.fn[1][1][fo];
-            nz = b.fn[1][2][fo];
-            A = b.fn[1][3][fo];
-            if (gj == 0) {
-              bk = b.bface[2][gi];
-              sgn = -1.0;
-            } else if (gj == nj) {
-              bk = b.bface[3][gi];
-            }
-          }
-          const int sc = pidx(col, f);
-          const int po = f * TI + col;
-          const int e = face_flux<FLUX>(pk + sc - 2 * PW, pk + sc - PW, pk + sc, pk + sc + PW,
-                                        PLANE, sPY + po, sPY + PYS + po, sPY + po + TI,
-                                        sPY + PYS + po + TI, (TJ + 2) * TI, nx, ny, nz, A, bk,
-                                        sgn, c, Fq);
-          if (e && on) {
-            const unsigned long long lin = (unsigned long long)gi * (nj + 1) + gj;
-            record_error(a.err, make_err_key(stage, 0, b.order, 1, e, lin));
-          }
-#pragma unroll
-          for (int v = 0; v < 5; ++v) sFY[v * (TJ + 1) * TI + f * TI + col] = Fq[v];
-        }
+      for (int v = 0; v < 5; ++v) {
+        const int ox = ty * (TI + 1) + tx;
+        const double dx = sFX[v * K::NFX + ox + 1] - sFX[v * K::NFX + ox];
+        const double dy = sFY[v * K::NFY + (ty + 1) * TI + tx] - sFY[v * K::NFY + ty * TI + tx];
+        if constexpr (NDIM == 3) R[v] = ((0.0 + dx) + dy) + (Fz[v] - fz[v]);
+        else R[v] = (0.0 + dx) + dy;
       }
-      __syncthreads();
-      if (col_on) {
-        double R[5];
+      const long long co = colofs + kofs;
+      if (flags & F_SOURCE) {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          const double fxl = sFX[v * TJ * (TI + 1) + ty * (TI + 1) + tx];
-          const double fxh = sFX[v * TJ * (TI + 1) + ty * (TI + 1) + tx + 1];
-          const double fyl = sFY[v * (TJ + 1) * TI + ty * TI + tx];
-          const double fyh = sFY[v * (TJ + 1) * TI + (ty + 1) * TI + tx];
-          R[v] = (0.0 + (fxh - fxl)) + (fyh - fyl);
-        }
-        const long long co = i + b.sy * (long long)j;
-        if (a.flags & F_SOURCE) {
+        for (int v = 0; v < 5; ++v) R[v] = R[v] - b.base[(long long)(FSRC + v) * fsz + co];
+      }
+      double dtv;
+      if (stage0) {
 #pragma unroll
-          for (int v = 0; v < 5; ++v) R[v] = R[v] - b.src[v][co];
-        }
-        double dtv;
-        const int s0 = pidx(tx, ty);
-        if (stage0) {
+        for (int v = 0; v < 5; ++v) rsum[v] += R[v] * R[v];
+        const double rho = pk[s0], u = pk[PLANE + s0], v = pk[2 * PLANE + s0],
+                     w = pk[3 * PLANE + s0], p = pk[4 * PLANE + s0];
+        const double snd = sqrt(c.gamma * p / rho);
+        double lam = 0.0;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) rsum[v] += R[v] * R[v];
-          const double rho = pk[s0], u = pk[PLANE + s0], v = pk[2 * PLANE + s0],
-                       w = pk[3 * PLANE + s0], p = pk[4 * PLANE + s0];
-          const double snd = sqrt(c.gamma * p / rho);
-          double lam = 0.0;
+        for (int d = 0; d < NDIM; ++d) {
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-#pragma unroll
-            for (int hi = 0; hi < 2; ++hi) {
-              const long long fo = co + (hi ? (d == 0 ? 1 : b.sy) : 0);
-              const double nx = b.fn[d][0][fo], ny = b.fn[d][1][fo], nz = b.fn[d][2][fo],
-                           A = b.fn[d][3][fo];
-              lam = lam + (fabs(u * nx + v * ny + w * nz) + snd) * A;
-            }
+          for (int hi = 0; hi < 2; ++hi) {
+            const long long fo = co + (hi ? (d == 0 ? 1 : (d == 1 ? sy : sz)) : 0);
+            const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
+            const double nx = __ldg(fn), ny = __ldg(fn + fsz), nz = __ldg(fn + 2 * fsz),
+                         A = __ldg(fn + 3 * fsz);
+            lam = lam + (fabs(u * nx + v * ny + w * nz) + snd) * A;
           }
-          const double vol = b.vol[co];
-          dtv = c.cfl * vol / lam / vol;
-          b.dtv[co] = dtv;
-        } else {
-          dtv = b.dtv[co];
         }
-        double qn[5];
-        const double adt = a.alpha * dtv;
+        const double vol = sQ[5 * NT + tid];
+#if BF_EXACT
+        dtv = c.cfl * vol / lam / vol;
+#else
+        dtv = c.cfl / lam;
+#endif
+        b.base[(long long)FDTV * fsz + co] = dtv;
+      } else {
+        dtv = sQ[5 * NT + tid];
+      }
+      double qn[5];
+      const double adt = a.alpha * dtv;
 #pragma unroll
-        for (int v = 0; v < 5; ++v) qn[v] = b.Q[v][co] - adt * R[v];
-        const double uu = qn[1] / qn[0], vv = qn[2] / qn[0], ww = qn[3] / qn[0];
-        const double pp = c.gm1 * (qn[4] - 0.5 * (qn[1] * uu + qn[2] * vv + qn[3] * ww));
-        if (qn[0] <= 0.0 || pp <= 0.0) {
-          const unsigned long long lin = (unsigned long long)i * nj + j;
-          record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
-        }
-        Wout[0][co] = qn[0];
-        Wout[1][co] = uu;
-        Wout[2][co] = vv;
-        Wout[3][co] = ww;
-        Wout[4][co] = pp;
-        if (last) {
+      for (int v = 0; v < 5; ++v) qn[v] = sQ[v * NT + tid] - adt * R[v];
+#if BF_EXACT
+      const double uu = qn[1] / qn[0], vv = qn[2] / qn[0], ww = qn[3] / qn[0];
+#else
+      const double rq = 1.0 / qn[0];
+      const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
+#endif
+      const double pp = c.gm1 * (qn[4] - 0.5 * (qn[1] * uu + qn[2] * vv + qn[3] * ww));
+      if (qn[0] <= 0.0 || pp <= 0.0) {
+        const unsigned long long lin =
+            ((unsigned long long)i * nj + j) * (unsigned long long)(NDIM == 3 ? nk : 1) +
+            (NDIM == 3 ? k : 0);
+        record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
+      }
+      Wout[co] = qn[0];
+      Wout[fsz + co] = uu;
+      Wout[2 * fsz + co] = vv;
+      Wout[3 * fsz + co] = ww;
+      Wout[4 * fsz + co] = pp;
+      if (last) {
 #pragma unroll
-          for (int v = 0; v < 5; ++v) b.Q[v][co] = qn[v];
-        }
+        for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
+      }
+    }
+    if constexpr (NDIM == 3) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        fz[v] = Fz[v];
+        wm1[v] = pk[v * PLANE + s0];
       }
     }
   }
 
   // ---- deterministic per-tile sum(R^2) ----------------------------------------
   if (stage0) {
+    cp_async_wait_all();
     __syncthreads();
     double* red = smem;   // reuse the plane ring: [NT/32][5]
 #pragma unroll
@@ -749,13 +617,13 @@ __global__ void __launch_bounds__(NT, 1) stage_kernel(const StageArgs a) {
       double x = rsum[v];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-      if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * 5 + v] = x;
+      if ((tid & 31) == 0) red[(tid >> 5) * 5 + v] = x;
     }
     __syncthreads();
-    if (threadIdx.x < 5) {
+    if (tid < 5) {
       double x = 0.0;
-      for (int w = 0; w < NT / 32; ++w) x += red[w * 5 + threadIdx.x];
-      a.partial[(long long)blockIdx.x * 5 + threadIdx.x] = x;
+      for (int w = 0; w < NT / 32; ++w) x += red[w * 5 + tid];
+      a.partial[(long long)blockIdx.x * 5 + tid] = x;
     }
   }
 }
@@ -763,9 +631,9 @@ __global__ void __launch_bounds__(NT, 1) stage_kernel(const StageArgs a) {
 // ---------------------------------------------------------------------------
 // ghost fill / pack / unpack (one launch per stage, all blocks)
 // ---------------------------------------------------------------------------
-BF_DEV double interior_T(const DevBlock& b, const double* const* W, long long o, int t_derived,
+BF_DEV double interior_T(const double* W, long long fsz, long long o, int t_derived,
                          const Consts& c) {
-  return t_derived ? W[4][o] / (W[0][o] * c.R) : W[5][o];
+  return t_derived ? W[4 * fsz + o] / (W[o] * c.R) : W[5 * fsz + o];
 }
 
 __global__ void __launch_bounds__(256) ghost_kernel(const GhostArgs a) {
@@ -791,30 +659,30 @@ __global__ void __launch_bounds__(256) ghost_kernel(const GhostArgs a) {
                            o2 * t.dst_stride[2];
     const long long soff = t.src_origin + o0 * t.src_stride[0] + o1 * t.src_stride[1] +
                            o2 * t.src_stride[2];
-    // field list: rho u v [w] p T
     double val[6];
     if (t.src_block >= 0) {
       const DevBlock& sb = a.blocks[t.src_block];
-      const double* const* W = sb.W[a.cur];
+      const double* W = sb.base + (long long)fw(a.cur, 0) * sb.fsz;
       int f = 0;
-      val[f++] = W[0][soff];
-      val[f++] = W[1][soff];
-      val[f++] = W[2][soff];
-      if (t.nfields == 6) val[f++] = W[3][soff];
-      val[f++] = W[4][soff];
-      val[f++] = interior_T(sb, W, soff, a.t_derived, c);
+      val[f++] = W[soff];
+      val[f++] = W[sb.fsz + soff];
+      val[f++] = W[2 * sb.fsz + soff];
+      if (t.nfields == 6) val[f++] = W[3 * sb.fsz + soff];
+      val[f++] = W[4 * sb.fsz + soff];
+      val[f++] = interior_T(W, sb.fsz, soff, a.t_derived, c);
     } else {
       for (int f = 0; f < t.nfields; ++f) val[f] = t.src_buf[f * t.buf_cells + soff];
     }
     if (t.block >= 0) {
-      double* const* W = a.blocks[t.block].W[a.cur];
+      const DevBlock& db = a.blocks[t.block];
+      double* W = db.base + (long long)fw(a.cur, 0) * db.fsz;
       int f = 0;
-      W[0][doff] = val[f++];
-      W[1][doff] = val[f++];
-      W[2][doff] = val[f++];
-      if (t.nfields == 6) W[3][doff] = val[f++];
-      W[4][doff] = val[f++];
-      W[5][doff] = val[f++];
+      W[doff] = val[f++];
+      W[db.fsz + doff] = val[f++];
+      W[2 * db.fsz + doff] = val[f++];
+      if (t.nfields == 6) W[3 * db.fsz + doff] = val[f++];
+      W[4 * db.fsz + doff] = val[f++];
+      W[5 * db.fsz + doff] = val[f++];
     } else {
       for (int f = 0; f < t.nfields; ++f) t.dst_buf[f * t.buf_cells + doff] = val[f];
     }
@@ -823,7 +691,8 @@ __global__ void __launch_bounds__(256) ghost_kernel(const GhostArgs a) {
 
   // ---- physical patch: one tangential position, all ghost layers ----------
   const DevBlock& b = a.blocks[t.block];
-  double* const* W = b.W[a.cur];
+  const long long fsz = b.fsz;
+  double* W = b.base + (long long)fw(a.cur, 0) * fsz;
   const int u0 = (int)(m % t.tn[0]), u1 = (int)(m / t.tn[0]);
   int cell[3] = {0, 0, 0};
   cell[t.ta] = t.tlo[0] + u0;
@@ -840,75 +709,77 @@ __global__ void __launch_bounds__(256) ghost_kernel(const GhostArgs a) {
   if (bc == BC_INFLOW) {
     for (int L = 0; L < t.depth; ++L) {
       const long long o = base + st[d] * gpos(L);
-      W[0][o] = c.fs_rho;
-      W[1][o] = c.fs_u;
-      W[2][o] = c.fs_v;
-      W[3][o] = c.fs_w;
-      W[4][o] = c.fs_p;
-      W[5][o] = c.fs_T;
+      W[o] = c.fs_rho;
+      W[fsz + o] = c.fs_u;
+      W[2 * fsz + o] = c.fs_v;
+      W[3 * fsz + o] = c.fs_w;
+      W[4 * fsz + o] = c.fs_p;
+      W[5 * fsz + o] = c.fs_T;
     }
   } else if (bc == BC_OUTFLOW) {
     const long long oi = base + st[d] * ipos(0);
-    const double v0 = W[0][oi], v1 = W[1][oi], v2 = W[2][oi], v3 = W[3][oi], v4 = W[4][oi];
-    const double v5 = interior_T(b, W, oi, a.t_derived, c);
+    const double v0 = W[oi], v1 = W[fsz + oi], v2 = W[2 * fsz + oi], v3 = W[3 * fsz + oi],
+                 v4 = W[4 * fsz + oi];
+    const double v5 = interior_T(W, fsz, oi, a.t_derived, c);
     for (int L = 0; L < t.depth; ++L) {
       const long long o = base + st[d] * gpos(L);
-      W[0][o] = v0;
-      W[1][o] = v1;
-      W[2][o] = v2;
-      W[3][o] = v3;
-      W[4][o] = v4;
-      W[5][o] = v5;
+      W[o] = v0;
+      W[fsz + o] = v1;
+      W[2 * fsz + o] = v2;
+      W[3 * fsz + o] = v3;
+      W[4 * fsz + o] = v4;
+      W[5 * fsz + o] = v5;
     }
   } else if (bc == BC_SLIP || bc == BC_NOSLIP) {
-    // outward unit normal on the boundary face plane
     const long long fo = base + st[d] * (t.side == 0 ? 0 : n);
     const double sg = t.side == 0 ? -1.0 : 1.0;
-    const double nx = sg * b.fn[d][0][fo], ny = sg * b.fn[d][1][fo], nz = sg * b.fn[d][2][fo];
+    const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
+    const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
     for (int L = 0; L < t.depth; ++L) {
       const long long og = base + st[d] * gpos(L);
       const long long oi = base + st[d] * ipos(L);
-      const double u = W[1][oi], v = W[2][oi], w = W[3][oi];
+      const double u = W[fsz + oi], v = W[2 * fsz + oi], w = W[3 * fsz + oi];
       if (bc == BC_SLIP) {
         const double vn = u * nx + v * ny + w * nz;
-        W[1][og] = u - 2.0 * vn * nx;
-        W[2][og] = v - 2.0 * vn * ny;
-        W[3][og] = w - 2.0 * vn * nz;
+        W[fsz + og] = u - 2.0 * vn * nx;
+        W[2 * fsz + og] = v - 2.0 * vn * ny;
+        W[3 * fsz + og] = w - 2.0 * vn * nz;
       } else {
-        W[1][og] = -u;
-        W[2][og] = -v;
-        W[3][og] = -w;
+        W[fsz + og] = -u;
+        W[2 * fsz + og] = -v;
+        W[3 * fsz + og] = -w;
       }
-      const double pg = W[4][oi];
-      W[4][og] = pg;
-      const double ti = interior_T(b, W, oi, a.t_derived, c);
+      const double pg = W[4 * fsz + oi];
+      W[4 * fsz + og] = pg;
+      const double ti = interior_T(W, fsz, oi, a.t_derived, c);
       const double tg = (bc == BC_NOSLIP && c.has_tw) ? 2.0 * c.tw - ti : ti;
-      W[5][og] = tg;
-      W[0][og] = pg / (c.R * tg);
+      W[5 * fsz + og] = tg;
+      W[og] = pg / (c.R * tg);
     }
   } else if (bc == BC_FARFIELD) {
     const long long fo = base + st[d] * (t.side == 0 ? 0 : n);
     const double sg = t.side == 0 ? -1.0 : 1.0;
-    const double nx = sg * b.fn[d][0][fo], ny = sg * b.fn[d][1][fo], nz = sg * b.fn[d][2][fo];
+    const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
+    const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
     const long long oi = base + st[d] * ipos(0);
-    const St s{W[0][oi], W[1][oi], W[2][oi], W[3][oi], W[4][oi]};
+    const St s{W[oi], W[fsz + oi], W[2 * fsz + oi], W[3 * fsz + oi], W[4 * fsz + oi]};
     const St q = farfield_state(s, nx, ny, nz, c);
     const double tb = q.p / (q.r * c.R);
     for (int L = 0; L < t.depth; ++L) {
       const long long o = base + st[d] * gpos(L);
-      W[0][o] = q.r;
-      W[1][o] = q.u;
-      W[2][o] = q.v;
-      W[3][o] = q.w;
-      W[4][o] = q.p;
-      W[5][o] = tb;
+      W[o] = q.r;
+      W[fsz + o] = q.u;
+      W[2 * fsz + o] = q.v;
+      W[3 * fsz + o] = q.w;
+      W[4 * fsz + o] = q.p;
+      W[5 * fsz + o] = tb;
     }
   } else {   // mms_dirichlet: cached exact values
     const long long nt = (long long)t.tn[0] * t.tn[1];
     for (int L = 0; L < t.depth; ++L) {
       const long long o = base + st[d] * gpos(L);
       const double* src = t.dirichlet + (long long)L * 6 * nt + m;
-      for (int f = 0; f < 6; ++f) W[f][o] = src[f * nt];
+      for (int f = 0; f < 6; ++f) W[f * fsz + o] = src[f * nt];
     }
   }
 }
@@ -943,19 +814,19 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double* partial, cons
 // ---------------------------------------------------------------------------
 template <int NDIM, int FLUX, int LIM>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
+  using K = Cfg<NDIM, LIM>;
   auto k = stage_kernel<NDIM, FLUX, LIM>;
-  const size_t bytes = Smem<NDIM>::BYTES;
   static unsigned long long attr_done = 0;   // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_done & (1ull << dev))) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+                                         (int)K::BYTES);
     if (e != cudaSuccess) return e;
     attr_done |= (1ull << dev);
   }
   if (a.ntiles == 0) return cudaSuccess;
-  k<<<a.ntiles, NT, bytes, s>>>(a);
+  k<<<a.ntiles, K::NT, K::BYTES, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -977,6 +848,13 @@ cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaSt
                           : launch_stage_l<2, FLUX_VAN_LEER>(lim, a, s);
 }
 
+// Tile rows used by the stage kernel for a (ndim, limiter) pair (the runtime
+// cuts tiles to match).
+int stage_tile_rows(int ndim, int lim) {
+  if (ndim == 2) return TJ_2D;
+  return lim == LIM_VAN_LEER || lim == LIM_MINMOD ? TJ_2D : TJ_3D;
+}
+
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s) {
   if (a.total_items == 0) return cudaSuccess;
   const long long nb = (a.total_items + 255) / 256;
@@ -990,8 +868,6 @@ cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblo
   reduce_kernel<<<nblocks, 256, 0, s>>>(partial, tile_begin, nblocks, out);
   return cudaGetLastError();
 }
-
-size_t stage_smem_bytes(int ndim) { return ndim == 3 ? Smem<3>::BYTES : Smem<2>::BYTES; }
 
 }  // namespace BF_NS
 }  // namespace bf

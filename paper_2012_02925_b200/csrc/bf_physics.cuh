@@ -1,10 +1,15 @@
 // bf_physics.cuh — point physics of the reference, as device functions.
 //
-// Each expression is written in the reference's left-to-right evaluation
-// order (C++ and Python associate + - * / identically), so the EXACT build
-// (-fmad=false: no a*b+c contraction; CUDA's double / and sqrt are IEEE
-// correctly rounded) reproduces numpy bit for bit.  The FAST build compiles
-// the same source with FMA contraction allowed.  Citations: blockflow/.
+// EXACT build (BF_EXACT=1, -fmad=false): every expression is written in the
+// reference's left-to-right evaluation order (C++ and Python associate
+// + - * / identically); CUDA's double / and sqrt are IEEE correctly rounded,
+// so the results are numpy's bit for bit.
+// FAST build (BF_EXACT=0): FMA contraction plus strength reduction — one
+// reciprocal per state instead of one division per use, rsqrt for 1/a,
+// multiplications by precomputed 1/gamma and 1/(2(g^2-1)), and the kappa=-1
+// zero terms dropped.  Each replacement changes a result by a few ulp; the
+// 1e-12 parity bar is checked in tests/test_gpu_parity.py.
+// Citations: blockflow/physics.py and blockflow/solver.py.
 #pragma once
 #include "bf_internal.h"
 
@@ -21,12 +26,17 @@ struct St {
 
 #define BF_DEV __device__ __forceinline__
 
-// physics.py:169-175
+// physics.py:169-175.  rinv = 1/rho (FAST only).
 BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Consts& c,
-                       double F[5]) {
+                       double F[5], double rinv) {
   const double vn = s.u * nx + s.v * ny + s.w * nz;
   const double ke = 0.5 * (s.u * s.u + s.v * s.v + s.w * s.w);
+#if BF_EXACT
+  (void)rinv;
   const double ht = c.gog1 * s.p / s.r + ke;
+#else
+  const double ht = c.gog1 * s.p * rinv + ke;
+#endif
   const double m = s.r * vn;
   F[0] = m;
   F[1] = m * s.u + nx * s.p;
@@ -35,23 +45,47 @@ BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Const
   F[4] = m * ht;
 }
 
-// physics.py:183-187
-BF_DEV double harten_abs(double lam, double delta) {
+BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Consts& c,
+                       double F[5]) {
+#if BF_EXACT
+  euler_flux(s, nx, ny, nz, c, F, 0.0);
+#else
+  euler_flux(s, nx, ny, nz, c, F, 1.0 / s.r);
+#endif
+}
+
+// physics.py:183-187.  half_inv = 1/(2*delta) (FAST only).
+BF_DEV double harten_abs(double lam, double delta, double half_inv) {
   const double mag = fabs(lam);
+#if BF_EXACT
+  (void)half_inv;
   const double safe = delta > 0.0 ? delta : 1.0;
   return mag < delta ? (lam * lam + delta * delta) / (2.0 * safe) : mag;
+#else
+  return mag < delta ? (lam * lam + delta * delta) * half_inv : mag;
+#endif
 }
 
 // physics.py:190-255.  Returns false when the Roe average has a2 <= 0.
 BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
                      const Consts& c, double F[5]) {
   double fl[5], fr[5];
-  euler_flux(L, nx, ny, nz, c, fl);
-  euler_flux(R, nx, ny, nz, c, fr);
+#if BF_EXACT
+  euler_flux(L, nx, ny, nz, c, fl, 0.0);
+  euler_flux(R, nx, ny, nz, c, fr, 0.0);
   const double hl = c.gog1 * L.p / L.r + 0.5 * (L.u * L.u + L.v * L.v + L.w * L.w);
   const double hr = c.gog1 * R.p / R.r + 0.5 * (R.u * R.u + R.v * R.v + R.w * R.w);
   const double rt = sqrt(R.r / L.r);
   const double wf = 1.0 / (1.0 + rt);
+#else
+  const double rli = 1.0 / L.r, rri = 1.0 / R.r;
+  euler_flux(L, nx, ny, nz, c, fl, rli);
+  euler_flux(R, nx, ny, nz, c, fr, rri);
+  const double hl = c.gog1 * L.p * rli + 0.5 * (L.u * L.u + L.v * L.v + L.w * L.w);
+  const double hr = c.gog1 * R.p * rri + 0.5 * (R.u * R.u + R.v * R.v + R.w * R.w);
+  const double rt = sqrt(R.r * rli);
+  const double wf = 1.0 / (1.0 + rt);
+#endif
   const double rho = rt * L.r;
   const double u = (L.u + rt * R.u) * wf;
   const double v = (L.v + rt * R.v) * wf;
@@ -68,12 +102,23 @@ BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
   const double dw = R.w - L.w;
   const double dvn = du * nx + dv * ny + dw * nz;
   const double delta = c.efix * (fabs(vn) + a);
-  const double l1 = harten_abs(vn - a, delta);
-  const double l2 = harten_abs(vn, delta);
-  const double l5 = harten_abs(vn + a, delta);
+#if BF_EXACT
+  const double l1 = harten_abs(vn - a, delta, 0.0);
+  const double l2 = harten_abs(vn, delta, 0.0);
+  const double l5 = harten_abs(vn + a, delta, 0.0);
   const double al1 = (dp - rho * a * dvn) / (2.0 * a2);
   const double al2 = dr - dp / a2;
   const double al5 = (dp + rho * a * dvn) / (2.0 * a2);
+#else
+  const double hinv = 0.5 / (delta > 0.0 ? delta : 1.0);
+  const double l1 = harten_abs(vn - a, delta, hinv);
+  const double l2 = harten_abs(vn, delta, hinv);
+  const double l5 = harten_abs(vn + a, delta, hinv);
+  const double ia2 = 1.0 / a2;
+  const double al1 = (dp - rho * a * dvn) * (0.5 * ia2);
+  const double al2 = dr - dp * ia2;
+  const double al5 = (dp + rho * a * dvn) * (0.5 * ia2);
+#endif
   const double su = du - dvn * nx;
   const double sv = dv - dvn * ny;
   const double sw = dw - dvn * nz;
@@ -97,11 +142,20 @@ BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
 // selected branch gives the same doubles.
 BF_DEV void van_leer_half(const St& s, double nx, double ny, double nz, const Consts& c,
                           double sign, double F[5]) {
-  const double a = sqrt(c.gamma * s.p / s.r);
   const double vn = s.u * nx + s.v * ny + s.w * nz;
+#if BF_EXACT
+  const double a = sqrt(c.gamma * s.p / s.r);
   const double mn = vn / a;
+  const double rinv = 0.0;
+#else
+  const double rinv = 1.0 / s.r;
+  const double a2 = c.gamma * s.p * rinv;
+  const double ainv = rsqrt(a2);
+  const double a = a2 * ainv;
+  const double mn = vn * ainv;
+#endif
   if (sign * mn >= 1.0) {
-    euler_flux(s, nx, ny, nz, c, F);
+    euler_flux(s, nx, ny, nz, c, F, rinv);
     return;
   }
   if (sign * mn <= -1.0) {
@@ -111,13 +165,19 @@ BF_DEV void van_leer_half(const St& s, double nx, double ny, double nz, const Co
   const double ke = 0.5 * (s.u * s.u + s.v * s.v + s.w * s.w);
   const double sh = mn + sign;
   const double fm = sign * 0.25 * s.r * a * (sh * sh);
-  const double fac = (-vn + sign * 2.0 * a) / c.gamma;
   const double et = c.gm1 * vn + sign * 2.0 * a;
+#if BF_EXACT
+  const double fac = (-vn + sign * 2.0 * a) / c.gamma;
+  const double ee = et * et / c.vl_c + ke - 0.5 * vn * vn;
+#else
+  const double fac = (-vn + sign * 2.0 * a) * c.inv_gamma;
+  const double ee = et * et * c.inv_vlc + ke - 0.5 * vn * vn;
+#endif
   F[0] = fm;
   F[1] = fm * (s.u + nx * fac);
   F[2] = fm * (s.v + ny * fac);
   F[3] = fm * (s.w + nz * fac);
-  F[4] = fm * (et * et / c.vl_c + ke - 0.5 * vn * vn);
+  F[4] = fm * ee;
 }
 
 // physics.py:293-297
@@ -130,7 +190,8 @@ BF_DEV void van_leer_flux(const St& L, const St& R, double nx, double ny, double
   for (int e = 0; e < 5; ++e) F[e] = fp[e] + fm[e];
 }
 
-// solver.py:138-171, (nx, ny, nz) is the OUTWARD unit normal.
+// solver.py:138-171, (nx, ny, nz) is the OUTWARD unit normal.  Boundary faces
+// only (a small fraction of the work): reference form in both builds.
 BF_DEV St farfield_state(const St& s, double nx, double ny, double nz, const Consts& c) {
   const double g = c.gamma;
   const double ai = sqrt(g * s.p / s.r);
@@ -174,6 +235,14 @@ BF_DEV double limiter(double a, double b) {
     const double val = 2.0 * r / (1.0 + r);
     return (a * b > 0.0) ? val : 0.0;
   }
+}
+
+// Number of stored limiter arrays per (cell, direction, var): Van Albada is
+// bitwise symmetric in (a, b) — (2a)b == (2b)a exactly, a*a+b*b commutes —
+// so psi+ == psi- and one evaluation serves both; "none" is identically 1.
+template <int LIM>
+__host__ __device__ constexpr int psi_count() {
+  return LIM == LIM_NONE ? 0 : (LIM == LIM_VAN_ALBADA ? 1 : 2);
 }
 
 }  // namespace BF_NS

@@ -27,6 +27,7 @@ cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaSt
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
+int stage_tile_rows(int ndim, int lim);
 }  // namespace bf_exact
 namespace bf_fast {
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
@@ -496,6 +497,7 @@ int build_tiles(bf_ctx* ctx) {
     hb.tile_begin = (int)tiles.size();
     tb.push_back(hb.tile_begin);
     const int kc = ctx->ndim == 3 ? ctx->kc : 1;
+    const int TJ = bf_exact::stage_tile_rows(ctx->ndim, ctx->sch.limiter);
     const int nk = ctx->ndim == 3 ? hb.n[2] : 1;
     for (int k0 = 0; k0 < nk; k0 += kc)
       for (int j0 = 0; j0 < hb.n[1]; j0 += TJ)
@@ -763,6 +765,9 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   c.ff_exp = 1.0 / (g - 1.0);
   c.two_over_gm1 = 2.0 / (g - 1.0);
   c.vl_c = 2.0 * (g * g - 1.0);
+  c.inv_gamma = 1.0 / g;
+  c.inv_vlc = 1.0 / c.vl_c;
+  c.kappa_m1 = scheme->kappa == -1.0;
   c.tw = scheme->wall_temperature;
   c.has_tw = scheme->has_wall_temperature;
   c.eps0 = scheme->epsilon == 0.0;
@@ -835,15 +840,15 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   hb.origin = hb.lead + hb.g + hb.sy * hb.g + hb.sz * hb.gk;
   hb.has_src = source != nullptr;
   const bool want_psi = ctx->sch.limiter_freeze_at > 0;
-  // arena: W 2x6, Q 5, dtv, vol, fn ndim x 4, src 5, psi ndim x 10
-  const int nfield = 12 + 5 + 2 + 4 * ndim + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0);
+  // arena slots (bf_internal.h): W 2x6 | Q 5 | dt/V | V | face geometry 3x4 |
+  // [S*V 5] | [limiters ndim x 2 x 5]
+  const int psi0 = want_psi ? FSRC + (hb.has_src ? 5 : 0) : -1;
+  const int nfield = FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0);
   int err = 0;
   hb.arena = dalloc(ctx, (size_t)nfield * hb.fsz, &err);
   if (err) return err;
   hb.owned.push_back(hb.arena);
   CK(cudaMemset(hb.arena, 0, sizeof(double) * (size_t)nfield * hb.fsz));
-  int slot = 0;
-  auto next = [&]() { return hb.arena + (size_t)(slot++) * hb.fsz + hb.origin; };
   DevBlock& d = hb.dev;
   for (int a = 0; a < 3; ++a) d.n[a] = hb.n[a];
   d.g = hb.g;
@@ -851,19 +856,9 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   d.id = block_id;
   d.sy = hb.sy;
   d.sz = hb.sz;
-  for (int b = 0; b < 2; ++b)
-    for (int f = 0; f < 6; ++f) d.W[b][f] = next();
-  for (int e = 0; e < 5; ++e) d.Q[e] = next();
-  d.dtv = next();
-  d.vol = next();
-  for (int dd = 0; dd < ndim; ++dd)
-    for (int cc = 0; cc < 4; ++cc) d.fn[dd][cc] = next();
-  if (hb.has_src)
-    for (int e = 0; e < 5; ++e) d.src[e] = next();
-  if (want_psi)
-    for (int dd = 0; dd < ndim; ++dd)
-      for (int pm = 0; pm < 2; ++pm)
-        for (int v = 0; v < 5; ++v) d.psi[dd][pm][v] = next();
+  d.fsz = hb.fsz;
+  d.base = hb.arena + hb.origin;
+  d.psi0 = psi0;
   ctx->have_psi = want_psi;
 
   // face unit normals and areas (solver.py:212-220), interior tangential
@@ -894,7 +889,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
           out[3][dst] = A;
         }
     for (int cc = 0; cc < 4; ++cc)
-      CK(cudaMemcpy(d.fn[dd][cc] - hb.origin, out[cc].data(), sizeof(double) * hb.fsz,
+      CK(cudaMemcpy(d.f(ffn(dd, cc)) - hb.origin, out[cc].data(), sizeof(double) * hb.fsz,
                     cudaMemcpyHostToDevice));
     ctx->bytes_h2d += 4LL * (long long)sizeof(double) * hb.fsz;
   }
@@ -911,11 +906,11 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
     ctx->bytes_h2d += (long long)sizeof(double) * hb.fsz;
     return BF_OK;
   };
-  int rc = put_interior(d.vol, volume);
+  int rc = put_interior(d.f(FVOL), volume);
   if (rc) return rc;
   if (hb.has_src)
     for (int e = 0; e < 5; ++e) {
-      rc = put_interior(d.src[e], source[e]);
+      rc = put_interior(d.f(FSRC + e), source[e]);
       if (rc) return rc;
     }
   d.order = (int)ctx->blocks.size();
@@ -1032,13 +1027,13 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
     return BF_OK;
   };
   for (int f = 0; f < 6; ++f) {
-    int rc = put(hb.dev.W[0][f], fields6[f]);
+    int rc = put(hb.dev.f(fw(0, f)), fields6[f]);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(hb.dev.W[1][f] - hb.origin, hb.dev.W[0][f] - hb.origin,
+    CK(cudaMemcpyAsync(hb.dev.f(fw(1, f)) - hb.origin, hb.dev.f(fw(0, f)) - hb.origin,
                        sizeof(double) * hb.fsz, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   for (int e = 0; e < 5; ++e) {
-    int rc = put(hb.dev.Q[e], q5[e]);
+    int rc = put(hb.dev.f(FQ + e), q5[e]);
     if (rc) return rc;
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1129,17 +1124,17 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
   };
   int rc;
   if (what >= BF_FIELD_RHO && what <= BF_FIELD_T) {
-    rc = get(hb.dev.W[ctx->cur][what], a);
+    rc = get(hb.dev.f(fw(ctx->cur, what)), a);
     if (rc) return rc;
-    rc = get(hb.dev.W[ctx->ghost_buf][what], b);
+    rc = get(hb.dev.f(fw(ctx->ghost_buf, what)), b);
     if (rc) return rc;
     std::vector<double> rho, p;
     if (what == BF_FIELD_T && ctx->t_derived) {
       rho.resize(hb.fsz);
       p.resize(hb.fsz);
-      rc = get(hb.dev.W[ctx->cur][0], rho);
+      rc = get(hb.dev.f(fw(ctx->cur, 0)), rho);
       if (rc) return rc;
-      rc = get(hb.dev.W[ctx->cur][4], p);
+      rc = get(hb.dev.f(fw(ctx->cur, 4)), p);
       if (rc) return rc;
     }
     for (long long k = 0; k < hb.P[2]; ++k)
@@ -1157,7 +1152,7 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
     return BF_OK;
   }
   if (what >= BF_FIELD_Q0 && what <= BF_FIELD_Q0 + 4) {
-    rc = get(hb.dev.Q[what - BF_FIELD_Q0], a);
+    rc = get(hb.dev.f(FQ + what - BF_FIELD_Q0), a);
     if (rc) return rc;
     for (long long k = 0; k < hb.P[2]; ++k)
       for (long long j = 0; j < hb.P[1]; ++j)
@@ -1166,7 +1161,7 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
     return BF_OK;
   }
   if (what == BF_FIELD_DTV) {
-    rc = get(hb.dev.dtv, a);
+    rc = get(hb.dev.f(FDTV), a);
     if (rc) return rc;
     for (long long k = 0; k < hb.n[2]; ++k)
       for (long long j = 0; j < hb.n[1]; ++j)
@@ -1179,7 +1174,7 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
     if (!ctx->have_psi) return fail(ctx, BF_EINVAL, "limiter arrays are kept only when freezing");
     const int r = what - BF_FIELD_PSI;
     const int d = r / 10, pm = (r % 10) / 5, v = r % 5;
-    rc = get(hb.dev.psi[d][pm][v], a);
+    rc = get(hb.dev.f(hb.dev.psi0 + 10 * d + 5 * pm + v), a);
     if (rc) return rc;
     long long ext[3] = {hb.n[0], hb.n[1], hb.n[2]};
     ext[d] += 2;
