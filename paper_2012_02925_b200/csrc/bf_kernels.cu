@@ -44,34 +44,6 @@ BF_DEV void record_error(unsigned long long* err, unsigned long long key) {
   if (key < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, key);
 }
 
-// Compile-time tile geometry and shared-memory layout (in doubles).
-template <int NDIM, int LIM>
-struct Cfg {
-  static constexpr int PC = psi_count<LIM>();
-  static constexpr int TJ = (NDIM == 3 && PC < 2) ? TJ_3D : TJ_2D;
-  static constexpr int NT = TI * TJ;
-  static constexpr int PW = TI + 2 * HALO;                // plane row pitch
-  static constexpr int PH = TJ + 2 * HALO;
-  static constexpr int PLANE = PW * PH;                   // cells per plane
-  static constexpr int NS = (NDIM == 3) ? NSLOT : 1;
-  static constexpr int NPX = (TI + 2) * TJ;               // psi_x cells: i = -1..TI
-  static constexpr int NPY = TI * (TJ + 2);               // psi_y cells: j = -1..TJ
-  static constexpr int NFX = (TI + 1) * TJ;               // x faces
-  static constexpr int NFY = TI * (TJ + 1);               // y faces
-  static constexpr int OW = 0;                            // [NS][5][PLANE]
-  static constexpr int OPX = OW + NS * 5 * PLANE;         // [PC][5][NPX]
-  static constexpr int OPY = OPX + PC * 5 * NPX;          // [PC][5][NPY]
-  static constexpr int OFX = OPY + PC * 5 * NPY;          // [5][NFX]
-  static constexpr int OFY = OFX + 5 * NFX;               // [5][NFY]
-  static constexpr int OQ = OFY + 5 * NFY;                // [6][NT] Q0 + dt/V (or V)
-  static constexpr int TOTAL = OQ + 6 * NT;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL;
-  static constexpr int NITEM = NFX + NFY;                 // x/y face items per plane
-  static constexpr int MAXIT = (NITEM + NT - 1) / NT;
-  static constexpr int NLIM = NPX + NPY;
-  BF_DEV static int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
-};
-
 // psi+ / psi- of one cell from its three stencil values (solver.py:419-435):
 // psi+_c = phi(D_{c+1}, D_c), psi-_c = phi(D_c, D_{c+1}).
 template <int LIM>
@@ -160,473 +132,7 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
   return err;
 }
 
-// Geometry and boundary code of one face, loaded early (ahead of its use).
-struct FaceGeo {
-  double nx, ny, nz, A;
-  int bk;
-  double sgn;
-};
-
-BF_DEV void load_geo(FaceGeo& g, const DevBlock& b, int d, long long off, bool on, int bface,
-                     int bk_side) {
-  if (on) {
-    const double* fn = b.base + (long long)ffn(d, 0) * b.fsz + off;
-    g.nx = __ldg(fn);
-    g.ny = __ldg(fn + b.fsz);
-    g.nz = __ldg(fn + 2 * b.fsz);
-    g.A = __ldg(fn + 3 * b.fsz);
-  } else {
-    g.nx = g.ny = g.nz = 0.0;
-    g.A = 0.0;
-  }
-  g.bk = BFACE_NONE;
-  g.sgn = 1.0;
-  if (on && bk_side >= 0) {
-    g.bk = b.bface[2 * d + bk_side][bface];
-    g.sgn = bk_side == 0 ? -1.0 : 1.0;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// the fused stage kernel
-// ---------------------------------------------------------------------------
-template <int NDIM, int FLUX, int LIM>
-__global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const StageArgs a) {
-  using K = Cfg<NDIM, LIM>;
-  constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW, PC = K::PC;
-  extern __shared__ __align__(16) double smem[];
-  double* const sW = smem + K::OW;
-  double* const sPX = smem + K::OPX;
-  double* const sPY = smem + K::OPY;
-  double* const sFX = smem + K::OFX;
-  double* const sFY = smem + K::OFY;
-  double* const sQ = smem + K::OQ;
-
-  const Tile t = a.tiles[blockIdx.x];
-  const DevBlock b = a.blocks[t.block];     // local copy: no aliasing reloads
-  const Consts& c = a.c;
-  const int tid = threadIdx.x;
-  const int tx = tid % TI, ty = tid / TI;
-  const int i0 = t.i0, j0 = t.j0, k0 = t.k0;
-  const int ni = b.n[0], nj = b.n[1], nk = b.n[2];
-  const long long sy = b.sy, sz = b.sz, fsz = b.fsz;
-  const int i = i0 + tx, j = j0 + ty;
-  const bool col_on = (i < ni) && (j < nj);
-  const int flags = a.flags;
-  const bool stage0 = flags & F_STAGE0;
-  const bool last = flags & F_LAST;
-  const bool psi_load = (PC > 0) && (flags & F_PSI_LOAD);
-  const bool psi_store = (PC > 0) && (flags & F_PSI_STORE);
-  const int stage = a.stage;
-  const double* const Win = b.base + (long long)fw(a.cur, 0) * fsz;
-  double* const Wout = b.base + (long long)fw(a.cur ^ 1, 0) * fsz;
-  const long long colofs = i + sy * (long long)j;
-
-  auto slot = [&](int k) -> double* {
-    if constexpr (NDIM == 3) return sW + ((k - k0 + 4 * NSLOT) % NSLOT) * 5 * PLANE;
-    else return sW;
-  };
-  auto psi_ptr = [&](int d, int pm, int v) -> double* {
-    return b.base + (long long)(b.psi0 + 10 * d + 5 * pm + v) * fsz;
-  };
-
-  // issue the cp.async copies of one plane (tile + 2-cell i/j halo, cross shape)
-  auto load_plane = [&](int k) {
-    if (NDIM == 3 && (k < -HALO || k >= nk + HALO)) return;
-    double* dst = slot(k);
-    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
-    constexpr int ROWS_FULL = TJ * PW;
-    constexpr int ROWS_HALO = 2 * HALO * TI;
-    for (int q = tid; q < ROWS_FULL + ROWS_HALO; q += NT) {
-      int ii, jj;
-      if (q < ROWS_FULL) {
-        jj = q / PW;
-        ii = q % PW - HALO;
-      } else {
-        const int r = (q - ROWS_FULL) / TI;
-        ii = (q - ROWS_FULL) % TI;
-        jj = (r < HALO) ? r - HALO : TJ + r - HALO;
-      }
-      const int gi = i0 + ii, gj = j0 + jj;
-      if (gi < -HALO || gi >= ni + HALO || gj < -HALO || gj >= nj + HALO) continue;
-      const double* src = Win + gi + sy * (long long)gj + kofs;
-      const int s = K::pidx(ii, jj);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) cp_async8(dst + v * PLANE + s, src + v * fsz);
-    }
-  };
-  // Q0 (+ dt/V or V) of the own cell, staged per thread
-  auto load_q = [&](int k) {
-    if (!col_on) return;
-    const long long o = colofs + ((NDIM == 3) ? sz * (long long)k : 0);
-    const double* q = b.base + (long long)FQ * fsz + o;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) cp_async8(sQ + v * NT + tid, q + v * fsz);
-    const double* dv = b.base + (long long)(stage0 ? FVOL : FDTV) * fsz + o;
-    cp_async8(sQ + 5 * NT + tid, dv);
-  };
-
-  // ---- x/y face items of this thread (fixed for all k) ----------------------
-  // item q < NFX: x face (row = q / (TI+1), f = q % (TI+1)); else y face
-  int it_q[K::MAXIT];
-#pragma unroll
-  for (int r = 0; r < K::MAXIT; ++r) it_q[r] = tid + r * NT;
-
-  double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-
-  // ---- z-direction carried state (3D) -------------------------------------------
-  double wm1[5] = {0, 0, 0, 0, 0};  // W(k-1), own column
-  double pzp[5], pzm[5];            // psi+/psi- of cell k
-  double fz[5];                     // flux at face k
-#pragma unroll
-  for (int v = 0; v < 5; ++v) pzp[v] = pzm[v] = fz[v] = 0.0;
-
-  if constexpr (NDIM == 3) {
-    if (col_on) {
-      const long long o = colofs + sz * (long long)(k0 - 2);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) wm1[v] = Win[v * fsz + o];
-    }
-    load_plane(k0 - 1);
-    load_plane(k0);
-    load_plane(k0 + 1);
-    cp_async_commit();
-  } else {
-    load_plane(0);
-    load_q(0);
-    cp_async_commit();
-  }
-
-  const int kfirst = (NDIM == 3) ? -1 : 0;
-  for (int kk = kfirst; kk < t.kc; ++kk) {
-    const int k = k0 + kk;
-    const bool xy = kk >= 0;
-    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
-    cp_async_wait_all();
-    __syncthreads();   // B0: planes k..k+2 resident; everyone done with iteration k-1
-    if constexpr (NDIM == 3) {
-      if (xy) load_q(k);
-      cp_async_commit();
-      if (kk + 1 < t.kc) load_plane(k + 3);
-      cp_async_commit();
-    }
-    const double* pk = slot(k);
-    const int s0 = K::pidx(tx, ty);
-
-    // early geometry loads for this iteration's faces
-    FaceGeo gz;
-    if constexpr (NDIM == 3) {
-      const int fk = k + 1;
-      load_geo(gz, b, 2, colofs + sz * (long long)fk, col_on, i + ni * j,
-               fk == 0 ? 0 : (fk == nk ? 1 : -1));
-    }
-    FaceGeo gi_[K::MAXIT];
-#pragma unroll
-    for (int r = 0; r < K::MAXIT; ++r) {
-      const int q = it_q[r];
-      if (!xy || q >= K::NITEM) {
-        gi_[r].A = 0.0;
-        continue;
-      }
-      if (q < K::NFX) {
-        const int row = q / (TI + 1), f = q % (TI + 1);
-        const int gi = i0 + f, gj = j0 + row;
-        const bool on = gi <= ni && gj < nj;
-        load_geo(gi_[r], b, 0, gi + sy * (long long)gj + kofs, on, gj + nj * (NDIM == 3 ? k : 0),
-                 gi == 0 ? 0 : (gi == ni ? 1 : -1));
-      } else {
-        const int q2 = q - K::NFX;
-        const int f = q2 / TI, col = q2 % TI;
-        const int gi = i0 + col, gj = j0 + f;
-        const bool on = gj <= nj && gi < ni;
-        load_geo(gi_[r], b, 1, gi + sy * (long long)gj + kofs, on, gi + ni * (NDIM == 3 ? k : 0),
-                 gj == 0 ? 0 : (gj == nj ? 1 : -1));
-      }
-    }
-
-    // ---- P1: x / y limiters of plane k -> smem -------------------------------------
-    if (xy && PC > 0) {
-      for (int q = tid; q < K::NLIM; q += NT) {
-        int gi, gj, d, o, sc, step;
-        if (q < K::NPX) {
-          const int row = q / (TI + 2), cc = q % (TI + 2) - 1;    // cell cc in [-1, TI]
-          gi = i0 + cc;
-          gj = j0 + row;
-          d = 0;
-          o = q;
-          sc = K::pidx(cc, row);
-          step = 1;
-        } else {
-          const int q2 = q - K::NPX;
-          const int row = q2 / TI - 1, cc = q2 % TI;             // row in [-1, TJ]
-          gi = i0 + cc;
-          gj = j0 + row;
-          d = 1;
-          o = q2;
-          sc = K::pidx(cc, row);
-          step = PW;
-        }
-        double* dstp = (d == 0) ? sPX + o : sPY + o;
-        const int vstride = (d == 0) ? K::NPX : K::NPY;
-        const bool in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
-                                       : (gj >= -1 && gj <= nj && gi < ni);
-        const long long go = gi + sy * (long long)gj + kofs;
-        if (psi_load) {
-          if (in_range) {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-              dstp[v * vstride] = psi_ptr(d, 0, v)[go];
-              if constexpr (PC == 2) dstp[(5 + v) * vstride] = psi_ptr(d, 1, v)[go];
-            }
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            double pp, pm;
-            cell_limiter<LIM>(pk[v * PLANE + sc - step], pk[v * PLANE + sc],
-                              pk[v * PLANE + sc + step], pp, pm);
-            dstp[v * vstride] = pp;
-            if constexpr (PC == 2) dstp[(5 + v) * vstride] = pm;
-            if (psi_store && in_range) {
-              psi_ptr(d, 0, v)[go] = pp;
-              psi_ptr(d, 1, v)[go] = pm;
-            }
-          }
-        }
-      }
-    }
-
-    // ---- z limiter of cell k+1 and z face k+1 (own column, registers) ------------
-    double Fz[5] = {0, 0, 0, 0, 0};
-    if constexpr (NDIM == 3) {
-      const double* p0 = slot(k);
-      const double* p1 = slot(k + 1);
-      const double* p2 = slot(k + 2);
-      double nzp[5], nzm[5];
-      const long long cz = colofs + sz * (long long)(k + 1);
-      if (kk == kfirst) {
-        // psi_z of cell k (= k0-1) from W(k-1) (regs), W(k), W(k+1)
-        const long long czk = colofs + sz * (long long)k;
-        if (psi_load) {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            pzp[v] = col_on ? psi_ptr(2, 0, v)[czk] : 0.0;
-            pzm[v] = (PC == 2) ? (col_on ? psi_ptr(2, 1, v)[czk] : 0.0) : pzp[v];
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            cell_limiter<LIM>(wm1[v], p0[v * PLANE + s0], p1[v * PLANE + s0], pzp[v], pzm[v]);
-            if (psi_store && col_on && k >= -1) {
-              psi_ptr(2, 0, v)[czk] = pzp[v];
-              psi_ptr(2, 1, v)[czk] = pzm[v];
-            }
-          }
-        }
-      }
-      if (psi_load) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          nzp[v] = col_on ? psi_ptr(2, 0, v)[cz] : 0.0;
-          nzm[v] = (PC == 2) ? (col_on ? psi_ptr(2, 1, v)[cz] : 0.0) : nzp[v];
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          cell_limiter<LIM>(p0[v * PLANE + s0], p1[v * PLANE + s0], p2[v * PLANE + s0], nzp[v],
-                            nzm[v]);
-          if (psi_store && col_on && k + 1 <= nk) {
-            psi_ptr(2, 0, v)[cz] = nzp[v];
-            psi_ptr(2, 1, v)[cz] = nzm[v];
-          }
-        }
-      }
-      // z face k+1 from a unit-stride copy of the own-column stencil
-      {
-        double st[4][5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          st[0][v] = wm1[v];
-          st[1][v] = p0[v * PLANE + s0];
-          st[2][v] = p1[v * PLANE + s0];
-          st[3][v] = p2[v * PLANE + s0];
-        }
-        const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, pzp, pzm, nzp, nzm, 1,
-                                            gz.nx, gz.ny, gz.nz, gz.A, gz.bk, gz.sgn, c, Fz);
-        if (ez && col_on) {
-          const int fk = k + 1;
-          const unsigned long long lin =
-              ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
-          record_error(a.err, make_err_key(stage, 0, b.order, 2, ez, lin));
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        pzp[v] = nzp[v];
-        pzm[v] = nzm[v];
-      }
-      if (kk == kfirst) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          fz[v] = Fz[v];
-          wm1[v] = p0[v * PLANE + s0];
-        }
-        continue;   // prologue iteration: z only
-      }
-    }
-
-    __syncthreads();   // B1: psi of plane k complete
-
-    // ---- P2: x / y face fluxes of plane k -> smem ----------------------------------
-#pragma unroll
-    for (int r = 0; r < K::MAXIT; ++r) {
-      const int q = it_q[r];
-      if (q >= K::NITEM) continue;
-      double Fq[5];
-      if (q < K::NFX) {
-        const int row = q / (TI + 1), f = q % (TI + 1);
-        const int sc = K::pidx(f, row);
-        const int po = row * (TI + 2) + f;          // psi of cell f-1 (index (f-1)+1)
-        const int e = face_flux<FLUX, LIM>(pk + sc - 2, pk + sc - 1, pk + sc, pk + sc + 1, PLANE,
-                                           sPX + po, sPX + (PC == 2 ? 5 * K::NPX : 0) + po,
-                                           sPX + po + 1, sPX + (PC == 2 ? 5 * K::NPX : 0) + po + 1,
-                                           K::NPX, gi_[r].nx, gi_[r].ny, gi_[r].nz, gi_[r].A,
-                                           gi_[r].bk, gi_[r].sgn, c, Fq);
-        const int gi = i0 + f, gj = j0 + row;
-        if (e && gi <= ni && gj < nj) {
-          const unsigned long long lin =
-              ((unsigned long long)gi * nj + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
-              (NDIM == 3 ? k : 0);
-          record_error(a.err, make_err_key(stage, 0, b.order, 0, e, lin));
-        }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) sFX[v * K::NFX + q] = Fq[v];
-      } else {
-        const int q2 = q - K::NFX;
-        const int f = q2 / TI, col = q2 % TI;
-        const int sc = K::pidx(col, f);
-        const int po = f * TI + col;                // psi of row f-1 (index (f-1)+1)
-        const int e = face_flux<FLUX, LIM>(pk + sc - 2 * PW, pk + sc - PW, pk + sc, pk + sc + PW,
-                                           PLANE, sPY + po, sPY + (PC == 2 ? 5 * K::NPY : 0) + po,
-                                           sPY + po + TI, sPY + (PC == 2 ? 5 * K::NPY : 0) + po + TI,
-                                           K::NPY, gi_[r].nx, gi_[r].ny, gi_[r].nz, gi_[r].A,
-                                           gi_[r].bk, gi_[r].sgn, c, Fq);
-        const int gi = i0 + col, gj = j0 + f;
-        if (e && gj <= nj && gi < ni) {
-          const unsigned long long lin =
-              ((unsigned long long)gi * (nj + 1) + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
-              (NDIM == 3 ? k : 0);
-          record_error(a.err, make_err_key(stage, 0, b.order, 1, e, lin));
-        }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) sFY[v * K::NFY + q2] = Fq[v];
-      }
-    }
-    if constexpr (NDIM == 3) cp_async_wait_1();   // own Q0 / dt staging landed
-    else cp_async_wait_all();
-    __syncthreads();   // B2: face fluxes of plane k complete
-
-    // ---- P3: residual, dt, update of cell (i, j, k) --------------------------------
-    if (col_on) {
-      double R[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        const int ox = ty * (TI + 1) + tx;
-        const double dx = sFX[v * K::NFX + ox + 1] - sFX[v * K::NFX + ox];
-        const double dy = sFY[v * K::NFY + (ty + 1) * TI + tx] - sFY[v * K::NFY + ty * TI + tx];
-        if constexpr (NDIM == 3) R[v] = ((0.0 + dx) + dy) + (Fz[v] - fz[v]);
-        else R[v] = (0.0 + dx) + dy;
-      }
-      const long long co = colofs + kofs;
-      if (flags & F_SOURCE) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) R[v] = R[v] - b.base[(long long)(FSRC + v) * fsz + co];
-      }
-      double dtv;
-      if (stage0) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) rsum[v] += R[v] * R[v];
-        const double rho = pk[s0], u = pk[PLANE + s0], v = pk[2 * PLANE + s0],
-                     w = pk[3 * PLANE + s0], p = pk[4 * PLANE + s0];
-        const double snd = sqrt(c.gamma * p / rho);
-        double lam = 0.0;
-#pragma unroll
-        for (int d = 0; d < NDIM; ++d) {
-#pragma unroll
-          for (int hi = 0; hi < 2; ++hi) {
-            const long long fo = co + (hi ? (d == 0 ? 1 : (d == 1 ? sy : sz)) : 0);
-            const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
-            const double nx = __ldg(fn), ny = __ldg(fn + fsz), nz = __ldg(fn + 2 * fsz),
-                         A = __ldg(fn + 3 * fsz);
-            lam = lam + (fabs(u * nx + v * ny + w * nz) + snd) * A;
-          }
-        }
-        const double vol = sQ[5 * NT + tid];
-#if BF_EXACT
-        dtv = c.cfl * vol / lam / vol;
-#else
-        dtv = c.cfl / lam;
-#endif
-        b.base[(long long)FDTV * fsz + co] = dtv;
-      } else {
-        dtv = sQ[5 * NT + tid];
-      }
-      double qn[5];
-      const double adt = a.alpha * dtv;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) qn[v] = sQ[v * NT + tid] - adt * R[v];
-#if BF_EXACT
-      const double uu = qn[1] / qn[0], vv = qn[2] / qn[0], ww = qn[3] / qn[0];
-#else
-      const double rq = 1.0 / qn[0];
-      const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
-#endif
-      const double pp = c.gm1 * (qn[4] - 0.5 * (qn[1] * uu + qn[2] * vv + qn[3] * ww));
-      if (qn[0] <= 0.0 || pp <= 0.0) {
-        const unsigned long long lin =
-            ((unsigned long long)i * nj + j) * (unsigned long long)(NDIM == 3 ? nk : 1) +
-            (NDIM == 3 ? k : 0);
-        record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
-      }
-      Wout[co] = qn[0];
-      Wout[fsz + co] = uu;
-      Wout[2 * fsz + co] = vv;
-      Wout[3 * fsz + co] = ww;
-      Wout[4 * fsz + co] = pp;
-      if (last) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
-      }
-    }
-    if constexpr (NDIM == 3) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        fz[v] = Fz[v];
-        wm1[v] = pk[v * PLANE + s0];
-      }
-    }
-  }
-
-  // ---- deterministic per-tile sum(R^2) ----------------------------------------
-  if (stage0) {
-    cp_async_wait_all();
-    __syncthreads();
-    double* red = smem;   // reuse the plane ring: [NT/32][5]
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      double x = rsum[v];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-      if ((tid & 31) == 0) red[(tid >> 5) * 5 + v] = x;
-    }
-    __syncthreads();
-    if (tid < 5) {
-      double x = 0.0;
-      for (int w = 0; w < NT / 32; ++w) x += red[w * 5 + tid];
-      a.partial[(long long)blockIdx.x * 5 + tid] = x;
-    }
-  }
-}
+#include "bf_stage.cuh"
 
 // ---------------------------------------------------------------------------
 // ghost fill / pack / unpack (one launch per stage, all blocks)

@@ -50,10 +50,25 @@ def run_pair(plan, cfg, fs, steps, init="uniform", precision="exact", gas=GAS):
     return ref, got
 
 
+def history_close(got, ref, tol=1e-12):
+    """SURVEY §8c residual-norm criterion: |dH_k| <= tol * H_1 per equation;
+    equations the reference's guard treats as inactive (H_1 <= 1e-12 max H_1,
+    solver.py:847-848, roundoff-level norms) against tol * max(H_1)."""
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert got.shape == ref.shape
+    base = ref[0]
+    scale = np.where(base > 1e-12 * base.max(), base, base.max())
+    err = np.abs(got - ref) / scale
+    assert err.max() <= tol, f"residual history differs: {err.max():.3e} > {tol}"
+
+
 def compare(ref, got, fs, bitwise, tol=1e-12, padded=True, check_q=True):
     # sum(R^2) is accumulated per tile on the device (numpy: pairwise over C
     # order), so even bitwise-equal residual fields give norms equal to ~1 ulp.
-    np.testing.assert_allclose(got.history, ref.history, rtol=1e-13 if bitwise else tol, atol=0)
+    if bitwise:
+        np.testing.assert_allclose(got.history, ref.history, rtol=1e-13, atol=0)
+    else:
+        history_close(got.history, ref.history, tol)
     scale = {n: max(abs(getattr(fs, n)), 1e-300) for n in FIELD_NAMES}
     speed = max(abs(fs.u), abs(fs.v), abs(fs.w))
     for n in ("u", "v", "w"):
@@ -262,7 +277,10 @@ def test_run_distributed_group_matches_serial(case, np_ranks):
         ost = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
         hist = [np.sqrt(ost.step(k + 1)[0]) for k in range(6)]
         ref = oracle.blockflow_oracle.OracleResult(blocks, np.array(hist), 6, False)
-    np.testing.assert_allclose(res.history, ref.history, rtol=1e-13 if bitwise else 1e-12)
+    if bitwise:
+        np.testing.assert_allclose(res.history, ref.history, rtol=1e-13)
+    else:
+        history_close(res.history, ref.history)
     for c in plan.children:
         (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
         for n in ("rho", "u", "v", "w", "p"):
