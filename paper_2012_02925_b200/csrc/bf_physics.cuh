@@ -26,6 +26,45 @@ struct St {
 
 #define BF_DEV __device__ __forceinline__
 
+#if !BF_EXACT
+// FAST build: branch-free reciprocal / reciprocal square root.  The MUFU
+// seed (rcp/rsqrt.approx.ftz.f64, ~2^-22 relative) is refined by two Newton
+// steps to ~1 ulp; no special-case slow path (all operands here are normal,
+// positive, finite numbers; non-physical states are flagged separately).
+BF_DEV double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+BF_DEV double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+BF_DEV double fsqrt(double x) {       // x * rsqrt(x), one residual correction
+  const double y = frsqrt(x);
+  const double s = x * y;
+  return fma(fma(-s, s, x), 0.5 * y, s);
+}
+BF_DEV double fdiv(double a, double b) {
+  const double r = frcp(b);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+#define BF_RCP(x) frcp(x)
+#define BF_DIV(a, b) fdiv((a), (b))
+#define BF_SQRT(x) fsqrt(x)
+#else
+#define BF_RCP(x) (1.0 / (x))
+#define BF_DIV(a, b) ((a) / (b))
+#define BF_SQRT(x) sqrt(x)
+#endif
+
 // physics.py:169-175.  rinv = 1/rho (FAST only).
 BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Consts& c,
                        double F[5], double rinv) {
@@ -50,7 +89,7 @@ BF_DEV void euler_flux(const St& s, double nx, double ny, double nz, const Const
 #if BF_EXACT
   euler_flux(s, nx, ny, nz, c, F, 0.0);
 #else
-  euler_flux(s, nx, ny, nz, c, F, 1.0 / s.r);
+  euler_flux(s, nx, ny, nz, c, F, frcp(s.r));
 #endif
 }
 
@@ -78,13 +117,13 @@ BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
   const double rt = sqrt(R.r / L.r);
   const double wf = 1.0 / (1.0 + rt);
 #else
-  const double rli = 1.0 / L.r, rri = 1.0 / R.r;
+  const double rli = frcp(L.r), rri = frcp(R.r);
   euler_flux(L, nx, ny, nz, c, fl, rli);
   euler_flux(R, nx, ny, nz, c, fr, rri);
   const double hl = c.gog1 * L.p * rli + 0.5 * (L.u * L.u + L.v * L.v + L.w * L.w);
   const double hr = c.gog1 * R.p * rri + 0.5 * (R.u * R.u + R.v * R.v + R.w * R.w);
-  const double rt = sqrt(R.r * rli);
-  const double wf = 1.0 / (1.0 + rt);
+  const double rt = fsqrt(R.r * rli);
+  const double wf = frcp(1.0 + rt);
 #endif
   const double rho = rt * L.r;
   const double u = (L.u + rt * R.u) * wf;
@@ -93,7 +132,7 @@ BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
   const double h = (hl + rt * hr) * wf;
   const double a2 = c.gm1 * (h - 0.5 * (u * u + v * v + w * w));
   const bool ok = !(a2 <= 0.0);
-  const double a = sqrt(a2);
+  const double a = BF_SQRT(a2);
   const double vn = u * nx + v * ny + w * nz;
   const double dr = R.r - L.r;
   const double dp = R.p - L.p;
@@ -110,11 +149,11 @@ BF_DEV bool roe_flux(const St& L, const St& R, double nx, double ny, double nz,
   const double al2 = dr - dp / a2;
   const double al5 = (dp + rho * a * dvn) / (2.0 * a2);
 #else
-  const double hinv = 0.5 / (delta > 0.0 ? delta : 1.0);
+  const double hinv = 0.5 * frcp(delta > 0.0 ? delta : 1.0);
   const double l1 = harten_abs(vn - a, delta, hinv);
   const double l2 = harten_abs(vn, delta, hinv);
   const double l5 = harten_abs(vn + a, delta, hinv);
-  const double ia2 = 1.0 / a2;
+  const double ia2 = frcp(a2);
   const double al1 = (dp - rho * a * dvn) * (0.5 * ia2);
   const double al2 = dr - dp * ia2;
   const double al5 = (dp + rho * a * dvn) * (0.5 * ia2);
@@ -148,9 +187,9 @@ BF_DEV void van_leer_half(const St& s, double nx, double ny, double nz, const Co
   const double mn = vn / a;
   const double rinv = 0.0;
 #else
-  const double rinv = 1.0 / s.r;
+  const double rinv = frcp(s.r);
   const double a2 = c.gamma * s.p * rinv;
-  const double ainv = rsqrt(a2);
+  const double ainv = frsqrt(a2);
   const double a = a2 * ainv;
   const double mn = vn * ainv;
 #endif
@@ -225,14 +264,14 @@ BF_DEV double limiter(double a, double b) {
   if constexpr (LIM == LIM_NONE) {
     return 1.0;
   } else if constexpr (LIM == LIM_VAN_ALBADA) {
-    const double x = (2.0 * a * b + 1e-12) / (a * a + b * b + 1e-12);
+    const double x = BF_DIV(2.0 * a * b + 1e-12, a * a + b * b + 1e-12);
     return (0.0 >= x) ? 0.0 : x;
   } else if constexpr (LIM == LIM_MINMOD) {
-    const double r = a / b;
+    const double r = BF_DIV(a, b);
     return (a * b > 0.0) ? ((1.0 <= r) ? 1.0 : r) : 0.0;
   } else {
-    const double r = a / b;
-    const double val = 2.0 * r / (1.0 + r);
+    const double r = BF_DIV(a, b);
+    const double val = BF_DIV(2.0 * r, 1.0 + r);
     return (a * b > 0.0) ? val : 0.0;
   }
 }

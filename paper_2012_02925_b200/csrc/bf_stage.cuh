@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
       if (col_on) {
         const double rho = pk[s0], u = pk[PLANE + s0], v = pk[2 * PLANE + s0],
                      w = pk[3 * PLANE + s0], p = pk[4 * PLANE + s0];
-        const double snd = sqrt(c.gamma * p / rho);
+        const double snd = BF_SQRT(BF_DIV(c.gamma * p, rho));
         double lam = 0.0;
         auto term = [&](double nx, double ny, double nz, double A) {
           lam = lam + (fabs(u * nx + v * ny + w * nz) + snd) * A;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
 #if BF_EXACT
         dtv = c.cfl * vol / lam / vol;
 #else
-        dtv = c.cfl / lam;
+        dtv = c.cfl * BF_RCP(lam);
 #endif
         b.base[(long long)FDTV * fsz + colofs + kofs] = dtv;
       }
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
 #if BF_EXACT
       const double uu = qn[1] / qn[0], vv = qn[2] / qn[0], ww = qn[3] / qn[0];
 #else
-      const double rq = 1.0 / qn[0];
+      const double rq = BF_RCP(qn[0]);
       const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
 #endif
       const double pp = c.gm1 * (qn[4] - 0.5 * (qn[1] * uu + qn[2] * vv + qn[3] * ww));
