@@ -59,7 +59,7 @@ def build(force=False, verbose=False):
     (OUT / "ptxas.log").write_text("\n".join(logs))
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *(str(o) for _, o, _ in jobs),
-          "-lnccl", "-cudart", "static"])
+          "-ldl", "-cudart", "static"])
     os.replace(tmp, LIB)
     if verbose:
         print(f"built {LIB}")

@@ -6,6 +6,7 @@
 // stream and moves halo messages with NCCL (one process per GPU) or with
 // device-to-device copies between contexts of one process (bf_group).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -40,6 +41,54 @@ cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblo
 using namespace bf;
 
 namespace {
+
+// NCCL is bound lazily with dlopen: the library has no load-time dependency on
+// libnccl, so whichever NCCL the process already holds (e.g. torch's bundled
+// one) is reused and importing libbfgpu first cannot shadow it.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi load_nccl() {
+  NcclApi a;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    a.err = dlerror() ? dlerror() : "libnccl.so.2 not found";
+    return a;
+  }
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+  a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+  a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+  a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+  a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+  a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+  a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+  a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+  a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart &&
+         a.GroupEnd && a.AllGather && a.GetErrorString;
+  if (!a.ok) a.err = "libnccl is missing required symbols";
+  return a;
+}
+
+NcclApi& nccl() {
+  static NcclApi api = load_nccl();
+  return api;
+}
 
 constexpr unsigned long long NO_ERROR = ~0ull;
 
@@ -174,7 +223,7 @@ int fail(bf_ctx* ctx, int code, const char* fmt, ...) {
   do {                                                                                        \
     ncclResult_t r_ = (call);                                                                 \
     if (r_ != ncclSuccess)                                                                    \
-      return fail(ctx, BF_ENCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_),     \
+      return fail(ctx, BF_ENCCL, "%s failed: %s (%s:%d)", #call, nccl().GetErrorString(r_), \
                   __FILE__, __LINE__);                                                        \
   } while (0)
 
@@ -558,13 +607,13 @@ std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx) {
 int nccl_exchange(bf_ctx* ctx) {
   auto rl = remote_links_sorted(ctx);
   if (rl.empty()) return BF_OK;
-  NK(ncclGroupStart());
+  NK(nccl().GroupStart());
   for (HostLink* L : rl) {
     const size_t cnt = (size_t)L->nfields * L->cells;
-    NK(ncclSend(L->send, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
-    NK(ncclRecv(L->recv, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    NK(nccl().Send(L->send, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    NK(nccl().Recv(L->recv, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
   }
-  NK(ncclGroupEnd());
+  NK(nccl().GroupEnd());
   return BF_OK;
 }
 
@@ -691,7 +740,7 @@ int rank_allgather(bf_ctx* ctx, double* sumsq, unsigned long long* key, int* bad
   for (int v = 0; v < 5; ++v) rec[v] = sumsq[v];
   std::memcpy(&rec[5], key, sizeof(double));
   CK(cudaMemcpyAsync(ctx->d_rank6, rec, sizeof rec, cudaMemcpyHostToDevice, ctx->stream));
-  NK(ncclAllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
+  NK(nccl().AllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
   std::vector<double> all((size_t)6 * ctx->nranks);
   CK(cudaMemcpyAsync(all.data(), ctx->d_gather, sizeof(double) * all.size(),
                      cudaMemcpyDeviceToHost, ctx->stream));
@@ -804,7 +853,7 @@ void bf_destroy(bf_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm) nccl().CommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -1203,7 +1252,7 @@ int bf_error_info(const bf_ctx* ctx, int* kind, int* block_id, int* stage, int* 
 
 int bf_nccl_unique_id(void* out128) {
   ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return BF_ENCCL;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return BF_ENCCL;
   std::memcpy(out128, &id, sizeof id);
   return BF_OK;
 }
@@ -1213,7 +1262,8 @@ int bf_nccl_init(bf_ctx* ctx, const void* id128) {
   CK(cudaSetDevice(ctx->device));
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof id);
-  NK(ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
+  if (!nccl().ok) return fail(ctx, BF_ENCCL, "NCCL unavailable: %s", nccl().err.c_str());
+  NK(nccl().CommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
   return BF_OK;
 }
 

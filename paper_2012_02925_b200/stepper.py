@@ -579,18 +579,10 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
                 converged = True
                 break
         solve = time.perf_counter() - t0
-        mine = {cid: {n: v.fields[n][v.block.interior()] for n in FIELD_NAMES}
-                for cid, v in stepper.solvers.items()}
+        from .distributed import assemble_parent_fields, local_interiors
         parts = [None] * nr
-        dist.all_gather_object(parts, mine)
-        fields = {b.id: {n: np.full(b.dims, np.nan) for n in FIELD_NAMES}
-                  for b in plan.grid.blocks}
-        for part in parts:
-            for cid, fl in part.items():
-                c = plan.child(cid)
-                (i0, i1), (j0, j1), (k0, k1) = c.cell_box()
-                for n in FIELD_NAMES:
-                    fields[c.parent][n][i0:i1, j0:j1, k0:k1] = fl[n]
+        dist.all_gather_object(parts, local_interiors(stepper.solvers))
+        fields = assemble_parent_fields(plan, parts)
         gpu.close()
         return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
                                  converged=converged, counters=native_counters(plan),
