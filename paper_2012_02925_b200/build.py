@@ -43,28 +43,43 @@ def up_to_date():
     return all(p.stat().st_mtime <= t for p in _sources())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, tile_rows=None, lib=None):
+    """tile_rows: 3D stage-kernel tile rows (16: 512-thread CTAs, 1 per SM;
+    8: 256-thread CTAs, 2 per SM); lib: output path (default libbfgpu.so)."""
+    global LIB
+    out_lib = Path(lib) if lib else LIB
+    if not force and lib is None and tile_rows is None and up_to_date():
         return LIB
     OUT.mkdir(exist_ok=True)
+    tag = f"_tj{tile_rows}" if tile_rows else ""
+    defs = [f"-DBF_TJ3={tile_rows}"] if tile_rows else []
     jobs = [
-        (CSRC / "bf_kernels.cu", OUT / "bf_kernels_exact.o", ["-DBF_EXACT=1", "-fmad=false"]),
-        (CSRC / "bf_kernels.cu", OUT / "bf_kernels_fast.o", ["-DBF_EXACT=0", "-fmad=true"]),
-        (CSRC / "bf_runtime.cu", OUT / "bf_runtime.o", []),
+        (CSRC / "bf_kernels.cu", OUT / f"bf_kernels_exact{tag}.o",
+         ["-DBF_EXACT=1", "-fmad=false", *defs]),
+        (CSRC / "bf_kernels.cu", OUT / f"bf_kernels_fast{tag}.o",
+         ["-DBF_EXACT=0", "-fmad=true", *defs]),
+        (CSRC / "bf_runtime.cu", OUT / f"bf_runtime{tag}.o", defs),
     ]
     cmds = [[NVCC, *COMMON, *extra, "-Xptxas", "-v", "-c", str(src), "-o", str(obj)]
             for src, obj, extra in jobs]
     with ThreadPoolExecutor(len(cmds)) as ex:
         logs = list(ex.map(_run, cmds))
-    (OUT / "ptxas.log").write_text("\n".join(logs))
-    tmp = LIB.with_suffix(".so.tmp")
+    (OUT / f"ptxas{tag}.log").write_text("\n".join(logs))
+    tmp = out_lib.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *(str(o) for _, o, _ in jobs),
           "-ldl", "-cudart", "static"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, out_lib)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {out_lib}")
+    return out_lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    rows = None
+    for a in sys.argv[1:]:
+        if a.startswith("--tile-rows="):
+            rows = int(a.split("=", 1)[1])
+    if rows:
+        build(force=True, verbose=True, tile_rows=rows, lib=PKG / f"libbfgpu_tj{rows}.so")
+    else:
+        build(force="--force" in sys.argv, verbose=True)

@@ -16,10 +16,16 @@ namespace bf {
 // marches KC cells along k (2.5-D streaming); 2D blocks use the same tile
 // with a single plane.
 constexpr int TI = 32;                   // tile width (one warp per row)
-constexpr int TJ_3D = 16;                // tile rows, 3D (512 threads, 1 CTA/SM)
+#ifndef BF_TJ3
+#define BF_TJ3 16
+#endif
+constexpr int TJ_3D = BF_TJ3;            // tile rows, 3D (16: 512 threads, 1 CTA/SM; 8: 2 CTAs/SM)
 constexpr int TJ_2D = 8;                 // tile rows, 2D
 constexpr int HALO = 2;                  // MUSCL stencil half-width
-constexpr int NSLOT = 4;                 // plane ring: k, k+1, k+2 resident + k+3 in flight
+constexpr int NSLOT = 3;                 // plane ring: k, k+1 resident, k+2 landing (TMA)
+constexpr int NTMAP = 6;                 // tensor maps per block: W plane, x/y face geometry,
+                                         // Q0, dt/V (or V), z face geometry
+constexpr int GXW = TI + 2;              // x-face geometry box width (16-byte multiple)
 
 // Scheme switches (bfgpu.h BF_FLUX_* / BF_LIM_*)
 constexpr int FLUX_ROE = 0;
@@ -91,6 +97,8 @@ struct DevBlock {
   int order;        // position of this block in the rank's id order
   int id;
   int psi0;         // first limiter slot (psi[d][pm][v] = psi0 + 10d + 5pm + v), -1: none
+  int ox, oy, oz;   // TMA coordinates of interior cell (0,0,0) in the arena tensor
+  int pad2_;
   long long sy, sz;
   long long fsz;    // doubles per slot
   double* base;     // arena base, pre-offset to the interior origin
@@ -153,6 +161,7 @@ struct StageArgs {
   double alpha;
   double* partial;      // [ntiles][5] sum(R^2) partials (stage 0)
   unsigned long long* err;   // [0] = min error key, [1..] unused
+  const unsigned char* tmaps;   // [nblocks][NTMAP] CUtensorMap (128 B each) in global memory
   Consts c;
 };
 

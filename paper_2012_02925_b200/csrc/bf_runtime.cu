@@ -5,6 +5,7 @@
 // the per-stage launches (RankStepper.step, solver.py:786-814) on one CUDA
 // stream and moves halo messages with NCCL (one process per GPU) or with
 // device-to-device copies between contexts of one process (bf_group).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -118,6 +119,7 @@ struct HostBlock {
   int g = 2, gk = 2;
   int P[3] = {0, 0, 0};      // padded dims
   long long lead = 0, sy = 0, sz = 0, origin = 0, fsz = 0;
+  int nslots = 0;
   double* arena = nullptr;
   std::vector<double*> owned;  // allocations to free
   DevBlock dev{};
@@ -152,6 +154,7 @@ struct bf_ctx {
   bool finalized = false;
   // device tables
   DevBlock* d_blocks = nullptr;
+  unsigned char* d_tmaps = nullptr;   // [nblocks][NTMAP] CUtensorMap
   Tile* d_tiles = nullptr;
   int ntiles = 0;
   int* d_tile_begin = nullptr;
@@ -538,6 +541,59 @@ int build_tables(bf_ctx* ctx) {
   return BF_OK;
 }
 
+// One 4-D tensor map per (block, box shape) over the block arena:
+// dims (pitch, P1, P2, field slot), strides (sy, sz, fsz) doubles.  Box shapes
+// follow the stage kernel's tile (bf_stage.cuh): the 5-variable haloed plane,
+// x / y face geometry, Q0, dt/V, z face geometry.
+int build_tensor_maps(bf_ctx* ctx) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(ctx, BF_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const int TJ = bf_exact::stage_tile_rows(ctx->ndim, ctx->sch.limiter);
+  const cuuint32_t boxes[NTMAP][4] = {
+      {(cuuint32_t)(TI + 2 * HALO), (cuuint32_t)(TJ + 2 * HALO), 1, 5},   // W plane
+      {(cuuint32_t)GXW, (cuuint32_t)TJ, 1, 4},                             // x-face geometry
+      {(cuuint32_t)TI, (cuuint32_t)(TJ + 1), 1, 4},                        // y-face geometry
+      {(cuuint32_t)TI, (cuuint32_t)TJ, 1, 5},                              // Q0
+      {(cuuint32_t)TI, (cuuint32_t)TJ, 1, 1},                              // dt/V or V
+      {(cuuint32_t)TI, (cuuint32_t)TJ, 1, 4}};                             // z-face geometry
+  std::vector<CUtensorMap> maps(ctx->blocks.size() * NTMAP);
+  for (size_t bi = 0; bi < ctx->blocks.size(); ++bi) {
+    const HostBlock& hb = ctx->blocks[bi];
+    const cuuint64_t dims[4] = {(cuuint64_t)hb.sy, (cuuint64_t)hb.P[1], (cuuint64_t)hb.P[2],
+                                (cuuint64_t)hb.nslots};
+    const cuuint64_t strides[3] = {(cuuint64_t)hb.sy * 8, (cuuint64_t)hb.sz * 8,
+                                   (cuuint64_t)hb.fsz * 8};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    for (int m = 0; m < NTMAP; ++m) {
+      const CUresult r = encode(&maps[bi * NTMAP + m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                hb.arena, dims, strides, boxes[m], estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(ctx, BF_ECUDA, "cuTensorMapEncodeTiled failed (%d) for block %d map %d",
+                    (int)r, hb.id, m);
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(maps.size(), 1) * sizeof(CUtensorMap)));
+  CK(cudaMemcpy(p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  ctx->d_tmaps = static_cast<unsigned char*>(p);
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap layout");
+  return BF_OK;
+}
+
 int build_tiles(bf_ctx* ctx) {
   std::vector<Tile> tiles;
   std::vector<int> tb;
@@ -664,6 +720,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.alpha = alpha;
   a.partial = ctx->d_partial;
   a.err = ctx->d_err;
+  a.tmaps = ctx->d_tmaps;
   a.c = ctx->c;
   {
     ProfScope ps(ctx, 0);
@@ -839,6 +896,7 @@ void bf_destroy(bf_ctx* ctx) {
   for (double* p : ctx->dirichlet_d) cudaFree(p);
   cudaFree(ctx->d_blocks);
   cudaFree(ctx->d_tiles);
+  cudaFree(ctx->d_tmaps);
   cudaFree(ctx->d_tile_begin);
   cudaFree(ctx->d_tasks_fill);
   cudaFree(ctx->d_tasks_unpack);
@@ -908,6 +966,10 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   d.fsz = hb.fsz;
   d.base = hb.arena + hb.origin;
   d.psi0 = psi0;
+  d.ox = (int)(hb.lead + hb.g);
+  d.oy = hb.g;
+  d.oz = hb.gk;
+  hb.nslots = nfield;
   ctx->have_psi = want_psi;
 
   // face unit normals and areas (solver.py:212-220), interior tangential
@@ -1031,6 +1093,8 @@ int bf_finalize(bf_ctx* ctx) {
   int rc = build_tables(ctx);
   if (rc) return rc;
   rc = build_tiles(ctx);
+  if (rc) return rc;
+  rc = build_tensor_maps(ctx);
   if (rc) return rc;
   std::vector<DevBlock> devs;
   for (auto& hb : ctx->blocks) devs.push_back(hb.dev);

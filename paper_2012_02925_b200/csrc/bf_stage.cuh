@@ -2,63 +2,113 @@
 // namespace bf::BF_NS).
 //
 // One CTA owns a TI x TJ column tile of one block and marches KC cells in k.
-// Per k-plane, three barrier-separated phases, each balanced across threads:
+// All global->shared traffic is TMA: each block has a 4-D tensor map over its
+// field arena (padded i, j, k, field slot), so ONE cp.async.bulk.tensor moves
+// the 5 primitive variables of a haloed (TI+4) x (TJ+4) plane, ONE moves the 4
+// geometry components of a face tile, ONE the 5 conserved variables; tiles at
+// block edges are zero-filled by the TMA unit.  One elected thread issues,
+// mbarriers carry completion.
+// Per k-plane, three barrier-separated phases:
 //   P1  every (cell, variable) limiter value of the plane's x and y stencils
-//       (a flat loop: each thread gets the same number +-1 of scalar items),
-//       stored to shared memory;
+//       (a flat loop: each thread gets the same number +-1 of scalar items);
 //   P2  face fluxes: own x-low face, own y-low face (+ one tile-edge face for
-//       TI+TJ threads), then the own-column z face k+1 and its limiter; each
-//       face's geometry was staged by cp.async into the very shared-memory
-//       slot its flux is written to;
+//       TI+TJ threads), then the own-column z limiter and z face k+1; a face's
+//       geometry sits in the shared-memory slot its flux is written to;
 //   P3  residual, stage-0 local dt / sum(R^2), RK update and decode.
-// Shared memory: a 4-slot ring of 5-variable primitive planes (k..k+2 resident,
-// k+3 in flight, cp.async), limiter arrays, face slots, and per-cell Q0 + dt/V
-// staging.  HBM is touched once per cell per stage for W, Q0, dt/V and the
-// face geometry (plus the 2-cell i/j halo reads, mostly L2 hits).
 #pragma once
+
+// ---- TMA / mbarrier primitives ------------------------------------------------
+BF_DEV unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+BF_DEV void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+BF_DEV void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+BF_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+BF_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+BF_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// 4-D tile load: box at coordinates (x, y, z, s) of the tensor map -> smem
+BF_DEV void tma_load4(void* dst, const void* tmap, int x, int y, int z, int s,
+                      unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(y), "r"(z), "r"(s),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 
 template <int NDIM, int LIM>
 struct Cfg {
   static constexpr int PC = psi_count<LIM>();
   static constexpr int TJ = (NDIM == 3 && PC < 2) ? TJ_3D : TJ_2D;
   static constexpr int NT = TI * TJ;
-  static constexpr int PW = TI + 2 * HALO;                // plane row pitch
+  static constexpr int MINB = (NT <= 256) ? 2 : 1;          // CTAs per SM targeted
+  static constexpr int PW = TI + 2 * HALO;                  // plane row pitch (36)
   static constexpr int PH = TJ + 2 * HALO;
-  static constexpr int PLANE = PW * PH;                   // cells per plane
+  static constexpr int PLANE = PW * PH;                     // cells per plane (full rectangle)
   static constexpr int NS = (NDIM == 3) ? NSLOT : 1;
-  static constexpr int NPX = (TI + 2) * TJ;               // psi_x cells: i = -1..TI
-  static constexpr int NPY = TI * (TJ + 2);               // psi_y cells: j = -1..TJ
+  static constexpr int NPX = (TI + 2) * TJ;                 // psi_x cells: i = -1..TI
+  static constexpr int NPY = TI * (TJ + 2);                 // psi_y cells: j = -1..TJ
   static constexpr int NLIM = NPX + NPY;
-  static constexpr int NFX = (TI + 1) * TJ;               // x faces: f = 0..TI per row
-  static constexpr int NFY = TI * (TJ + 1);               // y faces: rows f = 0..TJ
-  static constexpr int NEXTRA = TI + TJ;                  // tile-edge faces (f = TI, row TJ)
-  static constexpr int OW = 0;                            // [NS][5][PLANE]
-  static constexpr int OPX = OW + NS * 5 * PLANE;         // [PC][5][NPX]
-  static constexpr int OPY = OPX + PC * 5 * NPX;          // [PC][5][NPY]
-  static constexpr int OFX = OPY + PC * 5 * NPY;          // [5][NFX] geometry, then flux
-  static constexpr int OFY = OFX + 5 * NFX;               // [5][NFY]
-  static constexpr int OQ = OFY + 5 * NFY;                // [6][NT] Q0 + dt/V (or V)
-  static constexpr int TOTAL = OQ + 6 * NT;
+  static constexpr int NFX = GXW * TJ;                      // x-face slots [row][f], f = 0..33
+  static constexpr int NFY = TI * (TJ + 1);                 // y-face slots [f][col]
+  static constexpr bool ZG = (NDIM == 3) && (MINB == 1);    // z geometry staged in smem
+  static constexpr int r128(int x) { return (x + 15) / 16 * 16; }   // 128-byte alignment
+  static constexpr int OW = 0;                                      // [NS][5][PH][PW]
+  static constexpr int OPX = r128(OW + NS * 5 * PLANE);             // [PC][5][NPX]
+  static constexpr int OPY = r128(OPX + PC * 5 * NPX);              // [PC][5][NPY]
+  static constexpr int OFX = r128(OPY + PC * 5 * NPY);              // [5][TJ][GXW]
+  static constexpr int OFY = r128(OFX + 5 * NFX);                   // [5][TJ+1][TI]
+  static constexpr int OQ = r128(OFY + 5 * NFY);                    // [6][TJ][TI]
+  static constexpr int OZ = r128(OQ + 6 * NT);                      // [4][TJ][TI] (ZG)
+  static constexpr int OBAR = r128(OZ + (ZG ? 4 * NT : 0));         // mbarriers
+  static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
+  // TMA transaction sizes
+  static constexpr unsigned WBYTES = 5u * PLANE * 8u;
+  static constexpr unsigned GBYTES = (4u * NFX + 4u * NFY + 5u * NT + 1u * NT +
+                                      (ZG ? 4u * NT : 0u)) * 8u;
   BF_DEV static int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
 };
 
 template <int NDIM, int FLUX, int LIM>
-__global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
+    stage_kernel(const StageArgs a) {
   using K = Cfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW, PC = K::PC;
   constexpr int NFX = K::NFX, NFY = K::NFY, NPX = K::NPX, NPY = K::NPY;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   double* const sW = smem + K::OW;
   double* const sPX = smem + K::OPX;
   double* const sPY = smem + K::OPY;
   double* const sFX = smem + K::OFX;
   double* const sFY = smem + K::OFY;
   double* const sQ = smem + K::OQ;
+  double* const sZ = smem + K::OZ;
+  unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem + K::OBAR);
+  // bars[0..2]: plane ring slots, bars[3]: per-plane geometry/Q0 group
 
   const Tile t = a.tiles[blockIdx.x];
   const DevBlock b = a.blocks[t.block];     // by value: no aliasing reloads
   const Consts& c = a.c;
+  const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
   const int tid = threadIdx.x;
   const int tx = tid % TI, ty = tid / TI;
   const int i0 = t.i0, j0 = t.j0, k0 = t.k0;
@@ -72,103 +122,84 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
   const bool psi_load = (PC > 0) && (flags & F_PSI_LOAD);
   const bool psi_store = (PC > 0) && (flags & F_PSI_STORE);
   const int stage = a.stage;
-  const double* const Win = b.base + (long long)fw(a.cur, 0) * fsz;
   double* const Wout = b.base + (long long)fw(a.cur ^ 1, 0) * fsz;
   const long long colofs = i + sy * (long long)j;
+  const int s0 = K::pidx(tx, ty);
 
-  auto slot = [&](int k) -> double* {
-    if constexpr (NDIM == 3) return sW + ((k - k0 + 4 * NSLOT) % NSLOT) * 5 * PLANE;
+  // plane p (p = k - (k0 - 1)) lives in slot p % NS; its barrier parity is (p / NS) & 1
+  auto slot_of = [&](int k) -> double* {
+    if constexpr (NDIM == 3) return sW + ((k - k0 + 1) % NSLOT) * 5 * PLANE;
     else return sW;
   };
+  auto bar_of = [&](int k) { return bars + ((NDIM == 3) ? (k - k0 + 1) % NSLOT : 0); };
+  auto par_of = [&](int k) { return (unsigned)(((NDIM == 3) ? (k - k0 + 1) / NSLOT : 0) & 1); };
   auto psi_ptr = [&](int d, int pm, int v) -> double* {
     return b.base + (long long)(b.psi0 + 10 * d + 5 * pm + v) * fsz;
   };
 
-  // ---- cp.async producers -------------------------------------------------------
-  auto load_plane = [&](int k) {   // tile + 2-cell i/j halo (cross shape), 5 vars
-    if (NDIM == 3 && (k < -HALO || k >= nk + HALO)) return;
-    double* dst = slot(k);
-    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
-    constexpr int ROWS_FULL = TJ * PW;
-    constexpr int ROWS_HALO = 2 * HALO * TI;
-    for (int q = tid; q < ROWS_FULL + ROWS_HALO; q += NT) {
-      int ii, jj;
-      if (q < ROWS_FULL) {
-        jj = q / PW;
-        ii = q % PW - HALO;
-      } else {
-        const int r = (q - ROWS_FULL) / TI;
-        ii = (q - ROWS_FULL) % TI;
-        jj = (r < HALO) ? r - HALO : TJ + r - HALO;
-      }
-      const int gi = i0 + ii, gj = j0 + jj;
-      if (gi < -HALO || gi >= ni + HALO || gj < -HALO || gj >= nj + HALO) continue;
-      const double* src = Win + gi + sy * (long long)gj + kofs;
-      const int s = K::pidx(ii, jj);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) cp_async8(dst + v * PLANE + s, src + v * fsz);
-    }
+  // ---- producers (thread 0) -------------------------------------------------------
+  auto issue_plane = [&](int k) {
+    unsigned long long* bar = bar_of(k);
+    mbar_expect_tx(bar, K::WBYTES);
+    tma_load4(slot_of(k), tm + 0 * 128, b.ox + i0 - HALO, b.oy + j0 - HALO,
+              (NDIM == 3) ? b.oz + k : 0, fw(a.cur, 0), bar);
   };
-  // this thread's x/y faces of plane k: geometry (nx ny nz A) into their slots
-  // (slot components 0..3; the flux later overwrites components 0..4)
-  const int qx = ty * (TI + 1) + tx;                       // own x-low face
-  const int qy = ty * TI + tx;                             // own y-low face
+  auto issue_group = [&](int k) {   // geometry of plane k's faces, Q0, dt/V (or V), z geometry
+    unsigned long long* bar = bars + 3;
+    const int z = (NDIM == 3) ? b.oz + k : 0;
+    mbar_expect_tx(bar, K::GBYTES);
+    tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+    tma_load4(sFY, tm + 2 * 128, b.ox + i0, b.oy + j0, z, ffn(1, 0), bar);
+    tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
+    tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, stage0 ? FVOL : FDTV, bar);
+    if constexpr (K::ZG) tma_load4(sZ, tm + 5 * 128, b.ox + i0, b.oy + j0, z + 1, ffn(2, 0), bar);
+  };
+
+  const int qx = ty * GXW + tx;                            // own x-low face slot
+  const int qy = ty * TI + tx;                             // own y-low face slot
   const int ex = tid < TJ ? tid : -1;                      // extra x face f=TI, row tid
   const int ey = (tid >= TJ && tid < TJ + TI) ? tid - TJ : -1;   // extra y face row TJ
   auto face_on_x = [&](int f, int row) { return i0 + f <= ni && j0 + row < nj; };
   auto face_on_y = [&](int f, int col) { return j0 + f <= nj && i0 + col < ni; };
-  auto stage_geo = [&](int k) {
-    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
-    auto put = [&](double* slotbase, int q, int nq, int d, long long off) {
-      const double* src = b.base + (long long)ffn(d, 0) * fsz + off;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) cp_async8(slotbase + cc * nq + q, src + cc * fsz);
-    };
-    if (face_on_x(tx, ty)) put(sFX, qx, NFX, 0, colofs + kofs);
-    if (face_on_y(ty, tx)) put(sFY, qy, NFY, 1, colofs + kofs);
-    if (ex >= 0 && face_on_x(TI, ex))
-      put(sFX, ex * (TI + 1) + TI, NFX, 0, (i0 + TI) + sy * (long long)(j0 + ex) + kofs);
-    if (ey >= 0 && face_on_y(TJ, ey))
-      put(sFY, TJ * TI + ey, NFY, 1, (i0 + ey) + sy * (long long)(j0 + TJ) + kofs);
-  };
-  auto stage_q = [&](int k) {      // own cell's Q0 and dt/V (V at stage 0)
-    if (!col_on) return;
-    const long long o = colofs + ((NDIM == 3) ? sz * (long long)k : 0);
-    const double* q = b.base + (long long)FQ * fsz + o;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) cp_async8(sQ + v * NT + tid, q + v * fsz);
-    cp_async8(sQ + 5 * NT + tid, b.base + (long long)(stage0 ? FVOL : FDTV) * fsz + o);
-  };
 
   double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  // z-direction carried state (3D, own column)
-  double wm1[5] = {0, 0, 0, 0, 0};  // W(k-1)
+  double wm1[5] = {0, 0, 0, 0, 0};  // W(k-1), own column
   double pzp[5], pzm[5];            // psi+/psi- of cell k
   double fz[5];                     // flux at face k
 #pragma unroll
   for (int v = 0; v < 5; ++v) pzp[v] = pzm[v] = fz[v] = 0.0;
 
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(bars + q, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   if constexpr (NDIM == 3) {
     if (col_on) {
+      const double* Win = b.base + (long long)fw(a.cur, 0) * fsz;
       const long long o = colofs + sz * (long long)(k0 - 2);
 #pragma unroll
       for (int v = 0; v < 5; ++v) wm1[v] = Win[v * fsz + o];
     }
-    load_plane(k0 - 1);
-    load_plane(k0);
-    load_plane(k0 + 1);
-    cp_async_commit();
+    if (tid == 0) {
+      issue_plane(k0 - 1);
+      issue_plane(k0);
+      issue_plane(k0 + 1);
+    }
+    mbar_wait(bar_of(k0 - 1), par_of(k0 - 1));
+    mbar_wait(bar_of(k0), par_of(k0));
+    mbar_wait(bar_of(k0 + 1), par_of(k0 + 1));
   } else {
-    load_plane(0);
-    stage_geo(0);
-    stage_q(0);
-    cp_async_commit();
+    if (tid == 0) {
+      issue_plane(0);
+      issue_group(0);
+    }
+    mbar_wait(bar_of(0), 0);
   }
 
   // z limiter of cell kc from the own-column values of kc-1, kc, kc+1
-  auto z_limiter = [&](int kc, double wm_[5], const double* p0, const double* p1, double pp[5],
+  auto z_limiter = [&](int kc, const double* wa, const double* wb, const double* wc, double pp[5],
                        double pm[5]) {
-    const int s0 = K::pidx(tx, ty);
     const long long cz = colofs + sz * (long long)kc;
     if (psi_load) {
 #pragma unroll
@@ -180,12 +211,42 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
     }
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      cell_limiter<LIM>(wm_[v], p0[v * PLANE + s0], p1[v * PLANE + s0], pp[v], pm[v]);
+      cell_limiter<LIM>(wa[v], wb[v], wc[v], pp[v], pm[v]);
       if (psi_store && col_on && kc >= -1 && kc <= nk) {
         psi_ptr(2, 0, v)[cz] = pp[v];
         psi_ptr(2, 1, v)[cz] = pm[v];
       }
     }
+  };
+  // z face fk from own-column W(fk-2..fk+1) and psi of cells fk-1, fk
+  auto z_face = [&](int fk, const double st[4][5], const double* ppl, const double* pml,
+                    const double* ppr, const double* pmr, double g[4], double F[5]) {
+    int bk = BFACE_NONE;
+    double sg = 1.0;
+    if (col_on && fk == 0) {
+      bk = b.bface[4][i + ni * j];
+      sg = -1.0;
+    } else if (col_on && fk == nk) {
+      bk = b.bface[5][i + ni * j];
+    }
+    const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, ppl, pml, ppr, pmr, 1, g[0],
+                                        g[1], g[2], g[3], bk, sg, c, F);
+    if (ez && col_on) {
+      const unsigned long long lin =
+          ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
+      record_error(a.err, make_err_key(stage, 0, b.order, 2, ez, lin));
+    }
+  };
+  auto load_zgeo_global = [&](int fk, double g[4]) {
+    if (!col_on) {
+      g[0] = g[1] = g[2] = g[3] = 0.0;
+      return;
+    }
+    const double* fn = b.base + (long long)ffn(2, 0) * fsz + colofs + sz * (long long)fk;
+    g[0] = __ldg(fn);
+    g[1] = __ldg(fn + fsz);
+    g[2] = __ldg(fn + 2 * fsz);
+    g[3] = __ldg(fn + 3 * fsz);
   };
 
   const int kfirst = (NDIM == 3) ? -1 : 0;
@@ -193,81 +254,46 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
     const int k = k0 + kk;
     const bool xy = kk >= 0;
     const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
-    cp_async_wait_all();
-    __syncthreads();   // B0: planes k..k+2 resident; iteration k-1 fully retired
-    // producers for this iteration: [geometry + Q0 of plane k], [plane k+3]
-    if constexpr (NDIM == 3) {
-      if (xy) {
-        stage_geo(k);
-        stage_q(k);
-      }
-      cp_async_commit();
-      if (kk + 1 < t.kc) load_plane(k + 3);
-      cp_async_commit();
-    }
-    const double* pk = slot(k);
-    const int s0 = K::pidx(tx, ty);
+    const double* pk = slot_of(k);
 
     if constexpr (NDIM == 3) {
-      if (kk == kfirst) {
+      if (!xy) {
         // prologue: psi_z(k0-1), psi_z(k0) and the z face k0; no x/y work
-        double nzp[5], nzm[5], Fz[5];
-        z_limiter(k, wm1, slot(k), slot(k + 1), pzp, pzm);
-        double w0[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) w0[v] = slot(k)[v * PLANE + s0];
-        z_limiter(k + 1, w0, slot(k + 1), slot(k + 2), nzp, nzm);
-        double st[4][5];
+        double st[4][5], nzp[5], nzm[5], Fz[5], g[4];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           st[0][v] = wm1[v];
-          st[1][v] = w0[v];
-          st[2][v] = slot(k + 1)[v * PLANE + s0];
-          st[3][v] = slot(k + 2)[v * PLANE + s0];
+          st[1][v] = slot_of(k)[v * PLANE + s0];
+          st[2][v] = slot_of(k + 1)[v * PLANE + s0];
+          st[3][v] = slot_of(k + 2)[v * PLANE + s0];
         }
-        const int fk = k + 1;
-        const long long fo = colofs + sz * (long long)fk;
-        const double* fn = b.base + (long long)ffn(2, 0) * fsz + fo;
-        double gnx = 0, gny = 0, gnz = 0, gA = 0;
-        int bk = BFACE_NONE;
-        double sg = 1.0;
-        if (col_on) {
-          gnx = __ldg(fn);
-          gny = __ldg(fn + fsz);
-          gnz = __ldg(fn + 2 * fsz);
-          gA = __ldg(fn + 3 * fsz);
-          if (fk == 0) {
-            bk = b.bface[4][i + ni * j];
-            sg = -1.0;
-          } else if (fk == nk) {
-            bk = b.bface[5][i + ni * j];
-          }
-        }
-        const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, pzp, pzm, nzp, nzm, 1,
-                                            gnx, gny, gnz, gA, bk, sg, c, Fz);
-        if (ez && col_on) {
-          const unsigned long long lin =
-              ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
-          record_error(a.err, make_err_key(stage, 0, b.order, 2, ez, lin));
-        }
+        z_limiter(k, st[0], st[1], st[2], pzp, pzm);
+        z_limiter(k + 1, st[1], st[2], st[3], nzp, nzm);
+        load_zgeo_global(k + 1, g);
+        z_face(k + 1, st, pzp, pzm, nzp, nzm, g, Fz);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           pzp[v] = nzp[v];
           pzm[v] = nzm[v];
           fz[v] = Fz[v];
-          wm1[v] = w0[v];
+          wm1[v] = st[1][v];
         }
         continue;
+      }
+    }
+
+    __syncthreads();   // B0: iteration k-1 fully retired (smem slots free)
+    if (tid == 0) {
+      fence_async_smem();
+      if constexpr (NDIM == 3) {
+        issue_group(k);
+        issue_plane(k + 2);   // into the slot of plane k-1 (its own column is in wm1)
       }
     }
 
     // ---- P1: every (cell, var) limiter value of the x and y stencils of plane k --
     if constexpr (PC > 0) {
       int v = 0, q = tid;
-      while (q >= K::NLIM) {
-        q -= K::NLIM;
-        ++v;
-      }
       for (; v < 5;) {
         int gi, gj, d, sc, step;
         double* dst;
@@ -318,8 +344,9 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
         }
       }
     }
-    cp_async_wait_1();   // own geometry + Q0 staging landed (plane k+3 may be in flight)
-    __syncthreads();     // B1: limiters and staged geometry visible
+    if constexpr (NDIM == 3) mbar_wait(bars + 3, (unsigned)(kk & 1));
+    else mbar_wait(bars + 3, 0);
+    __syncthreads();     // B1: limiters complete; geometry / Q0 landed
 
     // ---- stage 0: local time step of the own cell (solver.py:696-731) -------------
     double dtv = 0.0;
@@ -337,10 +364,14 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
         term(sFY[qy], sFY[NFY + qy], sFY[2 * NFY + qy], sFY[3 * NFY + qy]);
         term(sFY[qy + TI], sFY[NFY + qy + TI], sFY[2 * NFY + qy + TI], sFY[3 * NFY + qy + TI]);
         if constexpr (NDIM == 3) {
-          const long long co = colofs + kofs;
-          for (int hi = 0; hi < 2; ++hi) {
-            const double* fn = b.base + (long long)ffn(2, 0) * fsz + co + (hi ? sz : 0);
-            term(__ldg(fn), __ldg(fn + fsz), __ldg(fn + 2 * fsz), __ldg(fn + 3 * fsz));
+          double g[4];
+          load_zgeo_global(k, g);
+          term(g[0], g[1], g[2], g[3]);
+          if constexpr (K::ZG) {
+            term(sZ[qy], sZ[NT + qy], sZ[2 * NT + qy], sZ[3 * NT + qy]);
+          } else {
+            load_zgeo_global(k + 1, g);
+            term(g[0], g[1], g[2], g[3]);
           }
         }
         const double vol = sQ[5 * NT + tid];
@@ -356,7 +387,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
 
     // ---- P2: x / y faces of plane k (geometry slot -> flux slot) --------------------
     auto x_face = [&](int f, int row) {
-      const int q = row * (TI + 1) + f;
+      const int q = row * GXW + f;
       const int gi = i0 + f, gj = j0 + row;
       const bool on = face_on_x(f, row);
       int bk = BFACE_NONE;
@@ -418,50 +449,35 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
     if (ex >= 0) x_face(TI, ex);
     if (ey >= 0) y_face(TJ, ey);
 
-    // z limiter of cell k+1 and the z face k+1 (own column, registers)
+    // own-column z limiter of cell k+1 and z face k+1 (plane k+2 must have landed)
     double Fz[5] = {0, 0, 0, 0, 0};
     if constexpr (NDIM == 3) {
-      double nzp[5], nzm[5];
-      double w0[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) w0[v] = pk[v * PLANE + s0];
-      z_limiter(k + 1, w0, slot(k + 1), slot(k + 2), nzp, nzm);
-      double st[4][5];
+      mbar_wait(bar_of(k + 2), par_of(k + 2));
+      double st[4][5], nzp[5], nzm[5], g[4];
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         st[0][v] = wm1[v];
-        st[1][v] = w0[v];
-        st[2][v] = slot(k + 1)[v * PLANE + s0];
-        st[3][v] = slot(k + 2)[v * PLANE + s0];
+        st[1][v] = pk[v * PLANE + s0];
+        st[2][v] = slot_of(k + 1)[v * PLANE + s0];
+        st[3][v] = slot_of(k + 2)[v * PLANE + s0];
       }
-      const int fk = k + 1;
-      const double* fn = b.base + (long long)ffn(2, 0) * fsz + colofs + sz * (long long)fk;
-      double gnx = 0, gny = 0, gnz = 0, gA = 0;
-      int bk = BFACE_NONE;
-      double sg = 1.0;
-      if (col_on) {
-        gnx = __ldg(fn);
-        gny = __ldg(fn + fsz);
-        gnz = __ldg(fn + 2 * fsz);
-        gA = __ldg(fn + 3 * fsz);
-        if (fk == nk) bk = b.bface[5][i + ni * j];
+      z_limiter(k + 1, st[1], st[2], st[3], nzp, nzm);
+      if constexpr (K::ZG) {
+        g[0] = sZ[qy];
+        g[1] = sZ[NT + qy];
+        g[2] = sZ[2 * NT + qy];
+        g[3] = sZ[3 * NT + qy];
+      } else {
+        load_zgeo_global(k + 1, g);
       }
-      (void)sg;
-      const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, pzp, pzm, nzp, nzm, 1,
-                                          gnx, gny, gnz, gA, bk, 1.0, c, Fz);
-      if (ez && col_on) {
-        const unsigned long long lin =
-            ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
-        record_error(a.err, make_err_key(stage, 0, b.order, 2, ez, lin));
-      }
+      z_face(k + 1, st, pzp, pzm, nzp, nzm, g, Fz);
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         pzp[v] = nzp[v];
         pzm[v] = nzm[v];
-        wm1[v] = w0[v];
+        wm1[v] = st[1][v];
       }
     }
-    if constexpr (NDIM == 2) cp_async_wait_all();
     __syncthreads();   // B2: face fluxes of plane k complete
 
     // ---- P3: residual, update of cell (i, j, k) ---------------------------------------
@@ -518,9 +534,8 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, 1) stage_kernel(const Stag
 
   // ---- deterministic per-tile sum(R^2) ----------------------------------------
   if (stage0) {
-    cp_async_wait_all();
     __syncthreads();
-    double* red = smem;   // reuse the plane ring: [NT/32][5]
+    double* red = sQ;   // free after the last P3: [NT/32][5]
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
       double x = rsum[v];
