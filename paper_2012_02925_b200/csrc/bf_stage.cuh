@@ -293,52 +293,63 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
 
     // ---- P1: every (cell, var) limiter value of the x and y stencils of plane k --
     if constexpr (PC > 0) {
+      // item q in [0, NLIM): [x cells i=0..TI-1 (TI*TJ)] [x edge cells i=-1,TI (2*TJ)]
+      // [y cells j=-1..TJ (TI*(TJ+2))]; all index maps are shifts/masks
+      static_assert(NT < K::NLIM, "one wrap per stride");
       int v = 0, q = tid;
       for (; v < 5;) {
-        int gi, gj, d, sc, step;
-        double* dst;
-        int vstride;
-        if (q < NPX) {
-          const int row = q / (TI + 2), cc = q % (TI + 2) - 1;    // cell cc in [-1, TI]
-          gi = i0 + cc;
-          gj = j0 + row;
+        int cc, row, d, o;
+        if (q < TI * TJ) {
+          cc = q & (TI - 1);
+          row = q >> 5;
           d = 0;
-          sc = K::pidx(cc, row);
-          step = 1;
-          dst = sPX + q;
-          vstride = NPX;
+          o = row * (TI + 2) + cc + 1;
+        } else if (q < TI * TJ + 2 * TJ) {
+          const int e = q - TI * TJ;
+          row = e >> 1;
+          cc = (e & 1) ? TI : -1;
+          d = 0;
+          o = row * (TI + 2) + cc + 1;
         } else {
           const int q2 = q - NPX;
-          const int row = q2 / TI - 1, cc = q2 % TI;             // row in [-1, TJ]
-          gi = i0 + cc;
-          gj = j0 + row;
+          cc = q2 & (TI - 1);
+          row = (q2 >> 5) - 1;
           d = 1;
-          sc = K::pidx(cc, row);
-          step = PW;
-          dst = sPY + q2;
-          vstride = NPY;
+          o = q2;
         }
-        const bool in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
-                                       : (gj >= -1 && gj <= nj && gi < ni);
-        const long long go = gi + sy * (long long)gj + kofs;
-        if (psi_load) {
-          if (in_range) {
-            dst[v * vstride] = psi_ptr(d, 0, v)[go];
-            if constexpr (PC == 2) dst[(5 + v) * vstride] = psi_ptr(d, 1, v)[go];
+        const int step = d == 0 ? 1 : PW;
+        double* dst = (d == 0 ? sPX : sPY) + o;
+        const int vstride = d == 0 ? NPX : NPY;
+        if (psi_load | psi_store) {
+          const int gi = i0 + cc, gj = j0 + row;
+          const bool in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
+                                         : (gj >= -1 && gj <= nj && gi < ni);
+          const long long go = gi + sy * (long long)gj + kofs;
+          if (psi_load) {
+            if (in_range) {
+              dst[v * vstride] = psi_ptr(d, 0, v)[go];
+              if constexpr (PC == 2) dst[(5 + v) * vstride] = psi_ptr(d, 1, v)[go];
+            }
+          } else {
+            double pp, pm;
+            const double* w = pk + v * PLANE + K::pidx(cc, row);
+            cell_limiter<LIM>(w[-step], w[0], w[step], pp, pm);
+            dst[v * vstride] = pp;
+            if constexpr (PC == 2) dst[(5 + v) * vstride] = pm;
+            if (in_range) {
+              psi_ptr(d, 0, v)[go] = pp;
+              psi_ptr(d, 1, v)[go] = pm;
+            }
           }
         } else {
           double pp, pm;
-          const double* w = pk + v * PLANE + sc;
+          const double* w = pk + v * PLANE + K::pidx(cc, row);
           cell_limiter<LIM>(w[-step], w[0], w[step], pp, pm);
           dst[v * vstride] = pp;
           if constexpr (PC == 2) dst[(5 + v) * vstride] = pm;
-          if (psi_store && in_range) {
-            psi_ptr(d, 0, v)[go] = pp;
-            psi_ptr(d, 1, v)[go] = pm;
-          }
         }
         q += NT;
-        while (q >= K::NLIM) {
+        if (q >= K::NLIM) {
           q -= K::NLIM;
           ++v;
         }
