@@ -44,6 +44,20 @@ def encode_primitive(rho, u, v, w, p, gamma):
     return rho, rho * u, rho * v, rho * w, p / (gamma - 1.0) + rho * ke
 
 
+def resolve_precision(precision, config):
+    """"exact": reference evaluation order, bitwise where no libm pow is involved.
+    "fast": FMA and strength reduction, within 1e-12 of the reference.
+    "auto" (default): fast, except exact when limiters are frozen — a frozen
+    non-smooth limiter pins O(1) limiter differences that roundoff-level state
+    differences produce in flat regions, which later multiply real gradients
+    (DESIGN.md §4), so freeze runs keep reference arithmetic."""
+    if precision == "auto":
+        return "exact" if getattr(config, "limiter_freeze_at", None) else "fast"
+    if precision not in ("exact", "fast"):
+        raise ConfigError(f"precision must be 'exact', 'fast' or 'auto', got {precision!r}")
+    return precision
+
+
 def host_setups(plan, child_ids, gas, config, freestream, metrics_fn=None):
     """Host-side setup (metrics, MMS data) of children, reusable across contexts."""
     return {cid: _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
@@ -116,8 +130,9 @@ class GpuContext:
     """One libbfgpu context: the children of one rank on one device."""
 
     def __init__(self, plan, child_ids, gas, config, freestream, device=0, rank=0, nranks=1,
-                 precision="exact", metrics_fn=None, setups=None):
+                 precision="auto", metrics_fn=None, setups=None):
         validate_scheme(config)
+        precision = resolve_precision(precision, config)
         if getattr(config, "viscous", False):
             raise ConfigError("the device path is inviscid; laminar NS is SURVEY §8f row 1")
         self.L = native.lib()
@@ -473,7 +488,7 @@ def write_residual_csv(result, path):
 
 
 def iterate_gpu(plan, schedule, gas, config, freestream, max_steps, residual_target=None,
-                init="uniform", residual_floor=None, device=0, precision="exact",
+                init="uniform", residual_floor=None, device=0, precision="auto",
                 metrics_fn=None):
     """solver.iterate on one GPU: every child of the plan in one context, all
     connected boundaries served by device copies (solver.py:914-936)."""
@@ -531,7 +546,7 @@ def native_counters(plan, rounds=1):
 
 def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, max_steps=100,
                         residual_target=None, init="uniform", timeout_s=5.0,
-                        residual_floor=None, precision="exact", devices=None, metrics_fn=None):
+                        residual_floor=None, precision="auto", devices=None, metrics_fn=None):
     """exchange.run_distributed on GPUs (exchange.py:599-682).
 
     * torch.distributed initialised with world_size == plan.np_ranks: this

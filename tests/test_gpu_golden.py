@@ -14,12 +14,16 @@ from paper_2012_02925_b200.model import FIELD_NAMES
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("precision", ["exact", "fast"])
+@pytest.mark.parametrize("precision", ["exact", "fast", "auto"])
 @pytest.mark.parametrize("name", gc.names())
 def test_gpu_matches_reference_golden(name, precision):
-    from paper_2012_02925_b200.stepper import iterate_gpu
+    from paper_2012_02925_b200.stepper import iterate_gpu, resolve_precision
     desc, z = gc.load(name)
     plan, sched, gas, cfg, fs = gc.build(desc)
+    if precision == "fast" and cfg.limiter_freeze_at:
+        pytest.skip("fast arithmetic + frozen limiters is outside the 1e-12 bar (DESIGN.md §4); "
+                    "'auto' runs such cases in exact arithmetic")
+    precision = resolve_precision(precision, cfg)
     res = iterate_gpu(plan, sched, gas, cfg, fs, desc["steps"], init=desc["init"],
                       precision=precision)
     bitwise = precision == "exact" and gc.bitwise_case(desc)
