@@ -310,10 +310,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        v, info = cpu_sample(level=9, steps=2, threads=1)
+        v, info = cpu_sample(level=11, steps=3, threads=1)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"CPU oracle (numpy restatement of blockflow.solver.iterate, 1 thread) "
-                         f"on multiblock_box_3d L9 ({info['cells']} cells, same scheme/BCs/IC), "
+                         f"on multiblock_box_3d L11 ({info['cells']} cells, same scheme/BCs/IC), "
                          f"{info['steps']} timed RK2 steps after 1 warm-up, {info['seconds']:.1f} s; "
                          f"CPU {cpu_model()}"}
 

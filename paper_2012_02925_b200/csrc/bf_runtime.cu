@@ -91,6 +91,85 @@ NcclApi& nccl() {
   return api;
 }
 
+// ---- device-side set-up kernels (replace host restriding loops) -----------------
+// Dense Fortran box (e0, e1, e2) -> arena slot at (o0, o1, o2) in padded-array
+// coordinates relative to the slot start.
+__global__ void scatter_box_kernel(double* dst, long long sy, long long sz, long long o0,
+                                   long long o1, long long o2, const double* src, int e0,
+                                   int e1, int e2) {
+  const long long n = (long long)e0 * e1 * e2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % e0, r = t / e0;
+    const long long j = r % e1, k = r / e1;
+    dst[(o0 + i) + sy * (o1 + j) + sz * (o2 + k)] = src[t];
+  }
+}
+
+// Arena slot -> dense Fortran box (inverse of scatter_box_kernel).
+__global__ void gather_box_kernel(double* dst, const double* src, long long sy, long long sz,
+                                  long long o0, long long o1, long long o2, int e0, int e1,
+                                  int e2) {
+  const long long n = (long long)e0 * e1 * e2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % e0, r = t / e0;
+    const long long j = r % e1, k = r / e1;
+    dst[t] = src[(o0 + i) + sy * (o1 + j) + sz * (o2 + k)];
+  }
+}
+
+// Unit normals and areas of one direction's faces (solver.py:212-220) with the
+// reference's IEEE operation order (explicit _rn intrinsics: no contraction).
+// sv: 3 component arrays of shape in (N_d+1 along d, padded tangential), Fortran.
+// Writes the interior-tangential faces f = 0..N_d into 4 slots (nx, ny, nz, A),
+// face f stored at interior cell index f.
+__global__ void face_normals_kernel(double* nx_slot, long long fsz, long long sy, long long sz,
+                                    long long origin, const double* sv, long long ncomp_stride,
+                                    int d, int e0, int e1, int e2, int in0, int in1, int g0,
+                                    int g1, int g2) {
+  const long long n = (long long)e0 * e1 * e2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % e0);
+    const long long r = t / e0;
+    const int j = (int)(r % e1), k = (int)(r / e1);
+    const long long ii = (d == 0) ? i : i + g0;
+    const long long jj = (d == 1) ? j : j + g1;
+    const long long kk = (d == 2) ? k : k + g2;
+    const long long s = ii + (long long)in0 * (jj + (long long)in1 * kk);
+    const double x = sv[s], y = sv[ncomp_stride + s], z = sv[2 * ncomp_stride + s];
+    const double A =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    const long long o = origin + i + sy * j + sz * k;
+    nx_slot[o] = A > 0.0 ? __ddiv_rn(x, A) : 0.0;
+    nx_slot[fsz + o] = A > 0.0 ? __ddiv_rn(y, A) : 0.0;
+    nx_slot[2 * fsz + o] = A > 0.0 ? __ddiv_rn(z, A) : 0.0;
+    nx_slot[3 * fsz + o] = A;
+  }
+}
+
+int grid_for(long long n) { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
+
+// One padded field as the reference holds it: interior from the current W
+// buffer (T derived as p/(rho R) once the state has been updated,
+// solver.py:753), ghost cells from the buffer the last ghost update filled.
+__global__ void merge_field_kernel(double* out, const double* cur, const double* ghost,
+                                   const double* rho, const double* p, int derived, double R,
+                                   long long sy, long long sz, long long lead, int g0, int g1,
+                                   int g2, int n0, int n1, int n2, int P0, int P1, int P2) {
+  const long long n = (long long)P0 * P1 * P2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % P0);
+    const long long r = t / P0;
+    const int j = (int)(r % P1), k = (int)(r / P1);
+    const long long s = lead + i + sy * j + sz * k;
+    const bool inner = i >= g0 && i < g0 + n0 && j >= g1 && j < g1 + n1 && k >= g2 && k < g2 + n2;
+    out[t] = inner ? (derived ? __ddiv_rn(p[s], __dmul_rn(rho[s], R)) : cur[s]) : ghost[s];
+  }
+}
+
 constexpr unsigned long long NO_ERROR = ~0ull;
 
 struct HostPatch {
@@ -972,49 +1051,40 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   hb.nslots = nfield;
   ctx->have_psi = want_psi;
 
-  // face unit normals and areas (solver.py:212-220), interior tangential
-  std::vector<double> host((size_t)hb.fsz);
+  // face unit normals and areas (solver.py:212-220): the reference's face-vector
+  // arrays go to the device as they are; a kernel normalises and scatters them.
+  cudaStream_t st = ctx->stream;
   for (int dd = 0; dd < ndim; ++dd) {
-    const double* sv[3] = {face_vectors[3 * dd], face_vectors[3 * dd + 1],
-                           face_vectors[3 * dd + 2]};
-    // input shape: (N_d+1 along d, padded along the others), Fortran
-    long long in_shape[3];
-    for (int a = 0; a < 3; ++a) in_shape[a] = (a == dd) ? hb.n[a] + 1 : hb.P[a];
-    std::vector<double> out[4];
-    for (auto& o : out) o.assign((size_t)hb.fsz, 0.0);
-    long long ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
-    for (long long k = 0; k < ext[2]; ++k)
-      for (long long j = 0; j < ext[1]; ++j)
-        for (long long i = 0; i < ext[0]; ++i) {
-          const long long ii = (dd == 0) ? i : i + gg[0];
-          const long long jj = (dd == 1) ? j : j + gg[1];
-          const long long kk = (dd == 2) ? k : k + gg[2];
-          const long long src = ii + in_shape[0] * (jj + in_shape[1] * kk);
-          const double x = sv[0][src], y = sv[1][src], z = sv[2][src];
-          const double A = std::sqrt((x * x + y * y) + z * z);
-          const long long dst = hb.origin + hb.off((int)i, (int)j, (int)k);
-          out[0][dst] = A > 0.0 ? x / A : 0.0;
-          out[1][dst] = A > 0.0 ? y / A : 0.0;
-          out[2][dst] = A > 0.0 ? z / A : 0.0;
-          out[3][dst] = A;
-        }
-    for (int cc = 0; cc < 4; ++cc)
-      CK(cudaMemcpy(d.f(ffn(dd, cc)) - hb.origin, out[cc].data(), sizeof(double) * hb.fsz,
-                    cudaMemcpyHostToDevice));
-    ctx->bytes_h2d += 4LL * (long long)sizeof(double) * hb.fsz;
+    long long in_shape[3], ext[3];
+    for (int a = 0; a < 3; ++a) {
+      in_shape[a] = (a == dd) ? hb.n[a] + 1 : hb.P[a];
+      ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+    }
+    const long long nin = in_shape[0] * in_shape[1] * in_shape[2];
+    double* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * 3 * nin, st));
+    for (int cc = 0; cc < 3; ++cc)
+      CK(cudaMemcpyAsync(tmp + cc * nin, face_vectors[3 * dd + cc], sizeof(double) * nin,
+                         cudaMemcpyHostToDevice, st));
+    const long long nout = ext[0] * ext[1] * ext[2];
+    face_normals_kernel<<<grid_for(nout), 256, 0, st>>>(
+        d.f(ffn(dd, 0)) - hb.origin, hb.fsz, hb.sy, hb.sz, hb.origin, tmp, nin, dd, (int)ext[0],
+        (int)ext[1], (int)ext[2], (int)in_shape[0], (int)in_shape[1], gg[0], gg[1], gg[2]);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, st));
+    ctx->bytes_h2d += 3LL * (long long)sizeof(double) * nin;
   }
   // volume + sources: interior Fortran (n0, n1, n2)
   auto put_interior = [&](double* dptr, const double* src) -> int {
-    std::fill(host.begin(), host.end(), 0.0);
-    for (long long k = 0; k < hb.n[2]; ++k)
-      for (long long j = 0; j < hb.n[1]; ++j)
-        for (long long i = 0; i < hb.n[0]; ++i)
-          host[hb.origin + hb.off((int)i, (int)j, (int)k)] =
-              src[i + (long long)hb.n[0] * (j + (long long)hb.n[1] * k)];
-    CK(cudaMemcpy(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
-                  cudaMemcpyHostToDevice));
-    ctx->bytes_h2d += (long long)sizeof(double) * hb.fsz;
+    const long long n = (long long)hb.n[0] * hb.n[1] * hb.n[2];
+    double* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * n, st));
+    CK(cudaMemcpyAsync(tmp, src, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    scatter_box_kernel<<<grid_for(n), 256, 0, st>>>(dptr, hb.sy, hb.sz, 0, 0, 0, tmp, hb.n[0],
+                                                    hb.n[1], hb.n[2]);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, st));
+    ctx->bytes_h2d += (long long)sizeof(double) * n;
     return BF_OK;
   };
   int rc = put_interior(d.f(FVOL), volume);
@@ -1024,6 +1094,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
       rc = put_interior(d.f(FSRC + e), source[e]);
       if (rc) return rc;
     }
+  CK(cudaStreamSynchronize(st));
   d.order = (int)ctx->blocks.size();
   ctx->index_of[block_id] = (int)ctx->blocks.size();
   ctx->blocks.push_back(std::move(hb));
@@ -1125,18 +1196,16 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
   if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
   CK(cudaSetDevice(ctx->device));
   HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
-  std::vector<double> host((size_t)hb.fsz, 0.0);
+  // padded Fortran arrays go to the device contiguously; a kernel restrides them
+  const long long np = (long long)hb.P[0] * hb.P[1] * hb.P[2];
+  double* tmp = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * np, ctx->stream));
   auto put = [&](double* dptr, const double* src) -> int {
-    for (long long k = 0; k < hb.P[2]; ++k)
-      for (long long j = 0; j < hb.P[1]; ++j) {
-        const double* row = src + (size_t)hb.P[0] * (j + (long long)hb.P[1] * k);
-        double* dst = host.data() + hb.lead + hb.sy * j + hb.sz * k;
-        std::memcpy(dst, row, sizeof(double) * hb.P[0]);
-      }
-    CK(cudaMemcpyAsync(dptr - hb.origin, host.data(), sizeof(double) * hb.fsz,
-                       cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->bytes_h2d += (long long)sizeof(double) * hb.fsz;
+    CK(cudaMemcpyAsync(tmp, src, sizeof(double) * np, cudaMemcpyHostToDevice, ctx->stream));
+    scatter_box_kernel<<<grid_for(np), 256, 0, ctx->stream>>>(
+        dptr - hb.origin + hb.lead, hb.sy, hb.sz, 0, 0, 0, tmp, hb.P[0], hb.P[1], hb.P[2]);
+    CK(cudaGetLastError());
+    ctx->bytes_h2d += (long long)sizeof(double) * np;
     return BF_OK;
   };
   for (int f = 0; f < 6; ++f) {
@@ -1149,6 +1218,7 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
     int rc = put(hb.dev.f(FQ + e), q5[e]);
     if (rc) return rc;
   }
+  CK(cudaFreeAsync(tmp, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->cur = 0;
   ctx->ghost_buf = 0;
@@ -1221,8 +1291,9 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   const HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
-  std::vector<double> a((size_t)hb.fsz), b((size_t)hb.fsz);
+  std::vector<double> a, b;
   auto get = [&](const double* dptr, std::vector<double>& h) -> int {
+    h.resize((size_t)hb.fsz);
     CK(cudaMemcpy(h.data(), dptr - hb.origin, sizeof(double) * hb.fsz, cudaMemcpyDeviceToHost));
     ctx->bytes_d2h += (long long)sizeof(double) * hb.fsz;
     return BF_OK;
@@ -1237,31 +1308,24 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
   };
   int rc;
   if (what >= BF_FIELD_RHO && what <= BF_FIELD_T) {
-    rc = get(hb.dev.f(fw(ctx->cur, what)), a);
-    if (rc) return rc;
-    rc = get(hb.dev.f(fw(ctx->ghost_buf, what)), b);
-    if (rc) return rc;
-    std::vector<double> rho, p;
-    if (what == BF_FIELD_T && ctx->t_derived) {
-      rho.resize(hb.fsz);
-      p.resize(hb.fsz);
-      rc = get(hb.dev.f(fw(ctx->cur, 0)), rho);
-      if (rc) return rc;
-      rc = get(hb.dev.f(fw(ctx->cur, 4)), p);
-      if (rc) return rc;
-    }
-    for (long long k = 0; k < hb.P[2]; ++k)
-      for (long long j = 0; j < hb.P[1]; ++j)
-        for (long long i = 0; i < hb.P[0]; ++i) {
-          const long long s = at(i, j, k);
-          double v;
-          if (interior(i, j, k)) {
-            v = (what == BF_FIELD_T && ctx->t_derived) ? p[s] / (rho[s] * ctx->gas.R) : a[s];
-          } else {
-            v = b[s];
-          }
-          out[i + hb.P[0] * (j + (long long)hb.P[1] * k)] = v;
-        }
+    const long long np = (long long)hb.P[0] * hb.P[1] * hb.P[2];
+    double* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * np, ctx->stream));
+    const int derived = (what == BF_FIELD_T && ctx->t_derived) ? 1 : 0;
+    merge_field_kernel<<<grid_for(np), 256, 0, ctx->stream>>>(
+        tmp, hb.dev.f(fw(ctx->cur, what)) - hb.origin,
+        hb.dev.f(fw(ctx->ghost_buf, what)) - hb.origin, hb.dev.f(fw(ctx->cur, 0)) - hb.origin,
+        hb.dev.f(fw(ctx->cur, 4)) - hb.origin, derived, ctx->gas.R, hb.sy, hb.sz, hb.lead, gg[0],
+        gg[1], gg[2], hb.n[0], hb.n[1], hb.n[2], hb.P[0], hb.P[1], hb.P[2]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp, sizeof(double) * np, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaFreeAsync(tmp, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->bytes_d2h += (long long)sizeof(double) * np;
+    (void)a;
+    (void)b;
+    (void)at;
+    (void)interior;
     return BF_OK;
   }
   if (what >= BF_FIELD_Q0 && what <= BF_FIELD_Q0 + 4) {
