@@ -268,7 +268,8 @@ def test_run_distributed_group_matches_serial(case, np_ranks):
     plan = planning.decompose(grid, np_ranks, grid.ndim)
     sched = planning.reorder_boundaries(plan)
     init = "uniform" if bitwise else "perturbed"
-    res = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=6, init=init)
+    res = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=6, init=init,
+                                 precision="exact")
     if bitwise:
         ref = oracle.iterate(plan, sched, GAS, cfg, fs, 6)
     else:
