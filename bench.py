@@ -347,7 +347,7 @@ def main():
 
 
 def gpu_kc():
-    return int(os.environ.get("BF_KC", "32"))
+    return int(os.environ.get("BF_KC", "16"))
 
 
 def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist, setups):

@@ -192,6 +192,24 @@ BF_DEV void van_leer_half(const St& s, double nx, double ny, double nz, const Co
   const double ainv = frsqrt(a2);
   const double a = a2 * ainv;
   const double mn = vn * ainv;
+  {
+    // branch-free: both forms, then select (lets the two halves of a face
+    // interleave instead of serialising behind data-dependent branches)
+    double full[5];
+    euler_flux(s, nx, ny, nz, c, full, rinv);
+    const double ke = 0.5 * (s.u * s.u + s.v * s.v + s.w * s.w);
+    const double sh = mn + sign;
+    const double fm = sign * 0.25 * s.r * a * (sh * sh);
+    const double et = c.gm1 * vn + sign * 2.0 * a;
+    const double fac = (-vn + sign * 2.0 * a) * c.inv_gamma;
+    const double ee = et * et * c.inv_vlc + ke - 0.5 * vn * vn;
+    const double part[5] = {fm, fm * (s.u + nx * fac), fm * (s.v + ny * fac),
+                            fm * (s.w + nz * fac), fm * ee};
+    const bool up = sign * mn >= 1.0, down = sign * mn <= -1.0;
+#pragma unroll
+    for (int e = 0; e < 5; ++e) F[e] = up ? full[e] : (down ? 0.0 : part[e]);
+    return;
+  }
 #endif
   if (sign * mn >= 1.0) {
     euler_flux(s, nx, ny, nz, c, F, rinv);

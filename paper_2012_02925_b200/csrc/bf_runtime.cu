@@ -257,7 +257,7 @@ struct bf_ctx {
   int t_derived = 0;
   bool psi_valid = false;
   bool have_psi = false;
-  int kc = 32;
+  int kc = 16;   // k-chunk per tile (measured: 16 > 32 > 64 on C4, profiles/r01_kc_*.json)
   // errors
   std::string msg;
   int e_kind = 0, e_block = -1, e_stage = 0, e_dir = 0;
