@@ -59,6 +59,58 @@ BF_DEV void cell_limiter(double wm, double w0, double wp, double& pp, double& pm
 // (solver.py:519) + boundary overwrite (solver.py:526-580) for one face.
 // c0..c3: var-0 pointers of cells f-2, f-1, f, f+1 (var stride vs).
 // ppl/pml: psi+/psi- of cell f-1, ppr/pmr: of cell f (var stride ps).
+// MUSCL left state at face f from cells f-2, f-1, f (solver.py:468-469):
+// qL = w_{f-1} + (eps/4)((1-k) psi+_{f-1} D_{f-1} + (1+k) psi-_{f-1} D_f)
+BF_DEV double muscl_left(double w0, double w1, double w2, double pp, double pm, const Consts& c) {
+  if (c.eps0) return w1;
+  const double dm = w1 - w0;
+  const double d0 = w2 - w1;
+#if BF_EXACT
+  return w1 + c.quarter * (c.omk * pp * dm + c.opk * pm * d0);
+#else
+  if (c.kappa_m1) return w1 + c.quarter * (c.omk * pp * dm);
+  return w1 + c.quarter * (c.omk * pp * dm + c.opk * pm * d0);
+#endif
+}
+// MUSCL right state at face f from cells f-1, f, f+1 (solver.py:470-471):
+// qR = w_f - (eps/4)((1+k) psi+_f D_f + (1-k) psi-_f D_{f+1})
+BF_DEV double muscl_right(double w1, double w2, double w3, double pp, double pm, const Consts& c) {
+  if (c.eps0) return w2;
+  const double d0 = w2 - w1;
+  const double dp = w3 - w2;
+#if BF_EXACT
+  return w2 - c.quarter * (c.opk * pp * d0 + c.omk * pm * dp);
+#else
+  if (c.kappa_m1) return w2 - c.quarter * (c.omk * pm * dp);
+  return w2 - c.quarter * (c.opk * pp * d0 + c.omk * pm * dp);
+#endif
+}
+
+// Wall / farfield face flux replacing the MUSCL one (solver.py:526-580).
+// c0..c3: var-0 pointers of cells f-2..f+1 (var stride vs); F already scaled by A.
+BF_DEV void boundary_overwrite(int bkind, double side_sign, const double* c0, const double* c1,
+                               const double* c2, const double* c3, int vs, double nx, double ny,
+                               double nz, double A, const Consts& c, double F[5]) {
+  // first / second interior cells next to the boundary plane
+  const double* in1 = (side_sign < 0.0) ? c2 : c1;
+  const double* in2 = (side_sign < 0.0) ? c3 : c0;
+  if (bkind == BFACE_WALL) {
+    const double pw = 1.5 * in1[4 * vs] - 0.5 * in2[4 * vs];
+    F[0] = 0.0;
+    F[1] = nx * pw * A;
+    F[2] = ny * pw * A;
+    F[3] = nz * pw * A;
+    F[4] = 0.0;
+  } else {
+    const St s1{in1[0], in1[vs], in1[2 * vs], in1[3 * vs], in1[4 * vs]};
+    const St qb = farfield_state(s1, side_sign * nx, side_sign * ny, side_sign * nz, c);
+    double Fb[5];
+    euler_flux(qb, nx, ny, nz, c, Fb);
+#pragma unroll
+    for (int e = 0; e < 5; ++e) F[e] = Fb[e] * A;
+  }
+}
+
 template <int FLUX, int LIM>
 BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const double* c3, int vs,
                      const double* ppl, const double* pml, const double* ppr, const double* pmr,
@@ -67,35 +119,15 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
   double qL[5], qR[5];
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    const double wl = c1[v * vs];
-    const double wr = c2[v * vs];
-    if (c.eps0) {
-      qL[v] = wl;
-      qR[v] = wr;
-    } else {
-      const double dm = wl - c0[v * vs];
-      const double d0 = wr - wl;
-      const double dp = c3[v * vs] - wr;
-      double a_pl = 1.0, a_ml = 1.0, a_pr = 1.0, a_mr = 1.0;
-      if constexpr (psi_count<LIM>() > 0) {
-        a_pl = ppl[v * ps];
-        a_pr = ppr[v * ps];
-        a_ml = pml[v * ps];
-        a_mr = pmr[v * ps];
-      }
-#if BF_EXACT
-      qL[v] = wl + c.quarter * (c.omk * a_pl * dm + c.opk * a_ml * d0);
-      qR[v] = wr - c.quarter * (c.opk * a_pr * d0 + c.omk * a_mr * dp);
-#else
-      if (c.kappa_m1) {
-        qL[v] = wl + c.quarter * (c.omk * a_pl * dm);
-        qR[v] = wr - c.quarter * (c.omk * a_mr * dp);
-      } else {
-        qL[v] = wl + c.quarter * (c.omk * a_pl * dm + c.opk * a_ml * d0);
-        qR[v] = wr - c.quarter * (c.opk * a_pr * d0 + c.omk * a_mr * dp);
-      }
-#endif
+    double a_pl = 1.0, a_ml = 1.0, a_pr = 1.0, a_mr = 1.0;
+    if constexpr (psi_count<LIM>() > 0) {
+      a_pl = ppl[v * ps];
+      a_pr = ppr[v * ps];
+      a_ml = pml[v * ps];
+      a_mr = pmr[v * ps];
     }
+    qL[v] = muscl_left(c0[v * vs], c1[v * vs], c2[v * vs], a_pl, a_ml, c);
+    qR[v] = muscl_right(c1[v * vs], c2[v * vs], c3[v * vs], a_pr, a_mr, c);
   }
   int err = 0;
   if (qL[0] <= 0.0 || qL[4] <= 0.0) err = ERR_FACE_LEFT;
@@ -109,26 +141,7 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
   }
 #pragma unroll
   for (int e = 0; e < 5; ++e) F[e] = F[e] * A;
-  if (bkind != BFACE_NONE) {
-    // first / second interior cells next to the boundary plane
-    const double* in1 = (side_sign < 0.0) ? c2 : c1;
-    const double* in2 = (side_sign < 0.0) ? c3 : c0;
-    if (bkind == BFACE_WALL) {
-      const double pw = 1.5 * in1[4 * vs] - 0.5 * in2[4 * vs];
-      F[0] = 0.0;
-      F[1] = nx * pw * A;
-      F[2] = ny * pw * A;
-      F[3] = nz * pw * A;
-      F[4] = 0.0;
-    } else {
-      const St s1{in1[0], in1[vs], in1[2 * vs], in1[3 * vs], in1[4 * vs]};
-      const St qb = farfield_state(s1, side_sign * nx, side_sign * ny, side_sign * nz, c);
-      double Fb[5];
-      euler_flux(qb, nx, ny, nz, c, Fb);
-#pragma unroll
-      for (int e = 0; e < 5; ++e) F[e] = Fb[e] * A;
-    }
-  }
+  if (bkind != BFACE_NONE) boundary_overwrite(bkind, side_sign, c0, c1, c2, c3, vs, nx, ny, nz, A, c, F);
   return err;
 }
 

@@ -78,7 +78,9 @@ struct Cfg {
   static constexpr int OFY = r128(OFX + 5 * NFX);                   // [5][TJ+1][TI]
   static constexpr int OQ = r128(OFY + 5 * NFY);                    // [6][TJ][TI]
   static constexpr int OZ = r128(OQ + 6 * NT);                      // [4][TJ][TI] (ZG)
-  static constexpr int OBAR = r128(OZ + (ZG ? 4 * NT : 0));         // mbarriers
+  static constexpr int NEDGE = TI + TJ;                             // tile-edge faces per plane
+  static constexpr int OH = r128(OZ + (ZG ? 4 * NT : 0));           // [NEDGE][2][5] half fluxes
+  static constexpr int OBAR = r128(OH + NEDGE * 10);                // mbarriers
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   // TMA transaction sizes
@@ -102,7 +104,14 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
   double* const sFY = smem + K::OFY;
   double* const sQ = smem + K::OQ;
   double* const sZ = smem + K::OZ;
+  double* const sH = smem + K::OH;
   unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem + K::OBAR);
+  // Van Leer faces split exactly into F+(qL) + F-(qR): the TI+TJ tile-edge
+  // faces become 2*(TI+TJ) half-face items done in the limiter phase by the
+  // last warps, so the flux phase has exactly three faces per thread.
+  constexpr bool SPLIT = FLUX == FLUX_VAN_LEER;
+  constexpr int NHALF = SPLIT ? 2 * K::NEDGE : 0;
+  constexpr int NFLAT = NT - NHALF;            // threads on the flat limiter loop
   // bars[0..2]: plane ring slots, bars[3]: per-plane geometry/Q0 group
 
   const Tile t = a.tiles[blockIdx.x];
@@ -291,8 +300,64 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
       }
     }
 
+    // ---- P1a (Van Leer): half fluxes of the tile-edge faces ---------------------------
+    if (SPLIT && tid >= NFLAT) {
+      const int hidx = tid - NFLAT;
+      const int e = hidx >> 1, h = hidx & 1;           // h = 0: F+(qL), h = 1: F-(qR)
+      const bool isx = e < TJ;
+      const int fcol = isx ? TI : e - TJ;              // the face's cell f (right of the face)
+      const int frow = isx ? e : TJ;
+      const int step = isx ? 1 : PW;
+      const int d = isx ? 0 : 1;
+      const int gi = i0 + fcol, gj = j0 + frow;
+      const bool on = isx ? face_on_x(TI, e) : face_on_y(TJ, fcol);
+      double g[3] = {0.0, 0.0, 0.0};
+      if (on) {
+        const double* fn = b.base + (long long)ffn(d, 0) * fsz + gi + sy * (long long)gj + kofs;
+        g[0] = __ldg(fn);
+        g[1] = __ldg(fn + fsz);
+        g[2] = __ldg(fn + 2 * fsz);
+      }
+      const double* wf = pk + K::pidx(fcol, frow);     // var-0 pointer of cell f
+      const double* wc = h == 0 ? wf - step : wf;      // cell whose limiter this side needs
+      const int lc = h == 0 ? -1 : 0;                  // its offset from f along the face normal
+      double q5[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double* w = wc + v * PLANE;
+        double pp = 1.0, pm = 1.0;
+        if constexpr (PC > 0) {
+          if (psi_load) {
+            const int ci = gi + (isx ? lc : 0), cj = gj + (isx ? 0 : lc);
+            const long long go = ci + sy * (long long)cj + kofs;
+            pp = on ? psi_ptr(d, 0, v)[go] : 0.0;
+            pm = (PC == 2) ? (on ? psi_ptr(d, 1, v)[go] : 0.0) : pp;
+          } else {
+            cell_limiter<LIM>(w[-step], w[0], w[step], pp, pm);
+          }
+        }
+        q5[v] = h == 0 ? muscl_left(w[-step], w[0], w[step], pp, pm, c)
+                       : muscl_right(w[-step], w[0], w[step], pp, pm, c);
+      }
+      if (on && (q5[0] <= 0.0 || q5[4] <= 0.0)) {
+        const unsigned long long lin =
+            isx ? ((unsigned long long)gi * nj + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
+                      (NDIM == 3 ? k : 0)
+                : ((unsigned long long)gi * (nj + 1) + gj) *
+                          (unsigned long long)(NDIM == 3 ? nk : 1) +
+                      (NDIM == 3 ? k : 0);
+        record_error(a.err, make_err_key(stage, 0, b.order, d,
+                                         h == 0 ? ERR_FACE_LEFT : ERR_FACE_RIGHT, lin));
+      }
+      double Fh[5];
+      van_leer_half(St{q5[0], q5[1], q5[2], q5[3], q5[4]}, g[0], g[1], g[2], c,
+                    h == 0 ? 1.0 : -1.0, Fh);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sH[(e * 2 + h) * 5 + v] = Fh[v];
+    }
+
     // ---- P1: every (cell, var) limiter value of the x and y stencils of plane k --
-    if constexpr (PC > 0) {
+    if (PC > 0 && tid < NFLAT) {
       // item q in [0, NLIM): [x cells i=0..TI-1 (TI*TJ)] [x edge cells i=-1,TI (2*TJ)]
       // [y cells j=-1..TJ (TI*(TJ+2))]; all index maps are shifts/masks
       static_assert(NT < K::NLIM, "one wrap per stride");
@@ -348,7 +413,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
           dst[v * vstride] = pp;
           if constexpr (PC == 2) dst[(5 + v) * vstride] = pm;
         }
-        q += NT;
+        q += NFLAT;
         if (q >= K::NLIM) {
           q -= K::NLIM;
           ++v;
@@ -457,8 +522,35 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
     };
     x_face(tx, ty);
     y_face(ty, tx);
-    if (ex >= 0) x_face(TI, ex);
-    if (ey >= 0) y_face(TJ, ey);
+    if constexpr (!SPLIT) {
+      if (ex >= 0) x_face(TI, ex);
+      if (ey >= 0) y_face(TJ, ey);
+    } else if (tid >= NFLAT && ((tid - NFLAT) & 1) == 0) {
+      // tile-edge face e = (F+ + F-) * A (+ wall / farfield overwrite)
+      const int e = (tid - NFLAT) >> 1;
+      const bool isx = e < TJ;
+      const int fcol = isx ? TI : e - TJ, frow = isx ? e : TJ;
+      const int q = isx ? e * GXW + TI : TJ * TI + fcol;
+      double* G = isx ? sFX : sFY;
+      const int nq = isx ? NFX : NFY;
+      const bool on = isx ? face_on_x(TI, e) : face_on_y(TJ, fcol);
+      const double nx = G[q], ny = G[nq + q], nz = G[2 * nq + q];
+      const double A = on ? G[3 * nq + q] : 0.0;
+      double F[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) F[v] = (sH[(e * 2) * 5 + v] + sH[(e * 2 + 1) * 5 + v]) * A;
+      int bk = BFACE_NONE;
+      if (on && isx && i0 + TI == ni) bk = b.bface[1][(j0 + frow) + nj * (NDIM == 3 ? k : 0)];
+      if (on && !isx && j0 + TJ == nj) bk = b.bface[3][(i0 + fcol) + ni * (NDIM == 3 ? k : 0)];
+      if (bk != BFACE_NONE) {
+        const int step = isx ? 1 : PW;
+        const double* wf = pk + K::pidx(fcol, frow);
+        boundary_overwrite(bk, 1.0, wf - 2 * step, wf - step, wf, wf + step, PLANE, nx, ny, nz,
+                           A, c, F);
+      }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) G[v * nq + q] = F[v];
+    }
 
     // own-column z limiter of cell k+1 and z face k+1 (plane k+2 must have landed)
     double Fz[5] = {0, 0, 0, 0, 0};
