@@ -17,8 +17,6 @@
 //   reduce_kernel  fixed-order per-block sum of the per-tile sum(R^2) partials.
 #include <cuda_runtime.h>
 
-#include <type_traits>
-
 #include "bf_internal.h"
 
 #if BF_EXACT

@@ -109,12 +109,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
   // Van Leer faces split exactly into F+(qL) + F-(qR): the TI+TJ tile-edge
   // faces become 2*(TI+TJ) half-face items done in the limiter phase by the
   // last warps, so the flux phase has exactly three faces per thread.
-  // Measured neutral on C4 (barrier stalls 16.5% -> 8.7% but +8% instructions,
-  // profiles/r01_stage_kernel_v9.ncu.json), so off unless BF_SPLIT_EDGE=1.
-#ifndef BF_SPLIT_EDGE
-#define BF_SPLIT_EDGE 0
-#endif
-  constexpr bool SPLIT = BF_SPLIT_EDGE && FLUX == FLUX_VAN_LEER;
+  constexpr bool SPLIT = FLUX == FLUX_VAN_LEER;
   constexpr int NHALF = SPLIT ? 2 * K::NEDGE : 0;
   constexpr int NFLAT = NT - NHALF;            // threads on the flat limiter loop
   // bars[0..2]: plane ring slots, bars[3]: per-plane geometry/Q0 group
@@ -363,11 +358,11 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
 
     // ---- P1: every (cell, var) limiter value of the x and y stencils of plane k --
     if (PC > 0 && tid < NFLAT) {
-      // cell item q in [0, NLIM): [x cells i=0..TI-1 (TI*TJ)] [x edge cells i=-1,TI
-      // (2*TJ)] [y cells j=-1..TJ (TI*(TJ+2))].  Each thread takes whole cells
-      // (all 5 variables, one index decode) for NLIM/NFLAT rounds; the leftover
-      // cells' (cell, var) scalars are spread flat, so per-thread work is equal +-1.
-      auto limit = [&](int q, int vlo, int vhi, auto mode) {
+      // item q in [0, NLIM): [x cells i=0..TI-1 (TI*TJ)] [x edge cells i=-1,TI (2*TJ)]
+      // [y cells j=-1..TJ (TI*(TJ+2))]; all index maps are shifts/masks
+      static_assert(NT < K::NLIM, "one wrap per stride");
+      int v = 0, q = tid;
+      for (; v < 5;) {
         int cc, row, d, o;
         if (q < TI * TJ) {
           cc = q & (TI - 1);
@@ -390,51 +385,40 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
         const int step = d == 0 ? 1 : PW;
         double* dst = (d == 0 ? sPX : sPY) + o;
         const int vstride = d == 0 ? NPX : NPY;
-        const double* w0 = pk + K::pidx(cc, row);
-        constexpr int MODE = decltype(mode)::value;   // 0 compute, 1 compute+store, 2 load
-        long long go = 0;
-        bool in_range = false;
-        if constexpr (MODE != 0) {
+        if (psi_load | psi_store) {
           const int gi = i0 + cc, gj = j0 + row;
-          in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
-                              : (gj >= -1 && gj <= nj && gi < ni);
-          go = gi + sy * (long long)gj + kofs;
-        }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          if (v < vlo || v >= vhi) continue;
-          if constexpr (MODE == 2) {
+          const bool in_range = (d == 0) ? (gi >= -1 && gi <= ni && gj < nj)
+                                         : (gj >= -1 && gj <= nj && gi < ni);
+          const long long go = gi + sy * (long long)gj + kofs;
+          if (psi_load) {
             if (in_range) {
               dst[v * vstride] = psi_ptr(d, 0, v)[go];
               if constexpr (PC == 2) dst[(5 + v) * vstride] = psi_ptr(d, 1, v)[go];
             }
           } else {
             double pp, pm;
-            const double* w = w0 + v * PLANE;
+            const double* w = pk + v * PLANE + K::pidx(cc, row);
             cell_limiter<LIM>(w[-step], w[0], w[step], pp, pm);
             dst[v * vstride] = pp;
             if constexpr (PC == 2) dst[(5 + v) * vstride] = pm;
-            if constexpr (MODE == 1) {
-              if (in_range) {
-                psi_ptr(d, 0, v)[go] = pp;
-                psi_ptr(d, 1, v)[go] = pm;
-              }
+            if (in_range) {
+              psi_ptr(d, 0, v)[go] = pp;
+              psi_ptr(d, 1, v)[go] = pm;
             }
           }
+        } else {
+          double pp, pm;
+          const double* w = pk + v * PLANE + K::pidx(cc, row);
+          cell_limiter<LIM>(w[-step], w[0], w[step], pp, pm);
+          dst[v * vstride] = pp;
+          if constexpr (PC == 2) dst[(5 + v) * vstride] = pm;
         }
-      };
-      auto run = [&](auto mode) {
-        constexpr int FULL = (K::NLIM / NFLAT) * NFLAT;
-        for (int q = tid; q < FULL; q += NFLAT) limit(q, 0, 5, mode);
-        constexpr int LEFT = K::NLIM - FULL;
-        for (int s = tid; s < 5 * LEFT; s += NFLAT) {
-          const int v = s / LEFT;
-          limit(FULL + (s - v * LEFT), v, v + 1, mode);
+        q += NFLAT;
+        if (q >= K::NLIM) {
+          q -= K::NLIM;
+          ++v;
         }
-      };
-      if (psi_load) run(std::integral_constant<int, 2>());
-      else if (psi_store) run(std::integral_constant<int, 1>());
-      else run(std::integral_constant<int, 0>());
+      }
     }
     if constexpr (NDIM == 3) mbar_wait(bars + 3, (unsigned)(kk & 1));
     else mbar_wait(bars + 3, 0);
