@@ -109,7 +109,12 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
   // Van Leer faces split exactly into F+(qL) + F-(qR): the TI+TJ tile-edge
   // faces become 2*(TI+TJ) half-face items done in the limiter phase by the
   // last warps, so the flux phase has exactly three faces per thread.
-  constexpr bool SPLIT = FLUX == FLUX_VAN_LEER;
+  // Measured neutral on C4 (barrier stalls 16.5% -> 8.7% but +8% instructions,
+  // profiles/r01_stage_kernel_v9.ncu.json), so off unless BF_SPLIT_EDGE=1.
+#ifndef BF_SPLIT_EDGE
+#define BF_SPLIT_EDGE 0
+#endif
+  constexpr bool SPLIT = BF_SPLIT_EDGE && FLUX == FLUX_VAN_LEER;
   constexpr int NHALF = SPLIT ? 2 * K::NEDGE : 0;
   constexpr int NFLAT = NT - NHALF;            // threads on the flat limiter loop
   // bars[0..2]: plane ring slots, bars[3]: per-plane geometry/Q0 group
