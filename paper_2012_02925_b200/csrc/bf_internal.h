@@ -77,7 +77,7 @@ struct Consts {
   int has_tw;
   int eps0;                                // epsilon == 0
   int kappa_m1;                            // kappa == -1 (fast mode drops the zero terms)
-  int pad_;
+  int muscl_k1;                            // epsilon == 1 and kappa == -1 (cell-split kernel)
 };
 
 // Field slots of a block arena (each slot fsz doubles, same padded layout).

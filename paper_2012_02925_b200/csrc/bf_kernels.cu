@@ -17,6 +17,8 @@
 //   reduce_kernel  fixed-order per-block sum of the per-tile sum(R^2) partials.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "bf_internal.h"
 
 #if BF_EXACT
@@ -146,6 +148,9 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
 }
 
 #include "bf_stage.cuh"
+#if !BF_EXACT
+#include "bf_vl.cuh"
+#endif
 
 // ---------------------------------------------------------------------------
 // ghost fill / pack / unpack (one launch per stage, all blocks)
@@ -330,6 +335,18 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double* partial, cons
 
 // ---------------------------------------------------------------------------
 // launchers (called by the runtime)
+#if !BF_EXACT
+// BF_VL=0 in the environment selects the reference-order kernel for FAST Van
+// Leer too (A/B measurements).
+static bool vl_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BF_VL");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+#endif
 // ---------------------------------------------------------------------------
 template <int NDIM, int FLUX, int LIM>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
@@ -360,6 +377,11 @@ static cudaError_t launch_stage_l(int lim, const StageArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s) {
+#if !BF_EXACT
+  // FAST Van Leer with limiters computed in-kernel: cell-split kernel (bf_vl.cuh)
+  if (flux == FLUX_VAN_LEER && !(a.flags & (F_PSI_LOAD | F_PSI_STORE)) && !vl_disabled())
+    return launch_vl(ndim, lim, a, s);
+#endif
   if (ndim == 3)
     return flux == FLUX_ROE ? launch_stage_l<3, FLUX_ROE>(lim, a, s)
                             : launch_stage_l<3, FLUX_VAN_LEER>(lim, a, s);

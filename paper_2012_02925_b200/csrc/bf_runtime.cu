@@ -956,6 +956,7 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   c.tw = scheme->wall_temperature;
   c.has_tw = scheme->has_wall_temperature;
   c.eps0 = scheme->epsilon == 0.0;
+  c.muscl_k1 = scheme->epsilon == 1.0 && scheme->kappa == -1.0;
   return ctx;
 }
 

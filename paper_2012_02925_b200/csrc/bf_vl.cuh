@@ -1,0 +1,699 @@
+// bf_vl.cuh — FAST-build Van Leer stage kernel in the cell-split form
+// (included by bf_kernels.cu inside namespace bf::bf_fast).
+//
+// Why a second kernel: with flux-vector splitting the face flux is
+//   F_{c+1/2} = F+(qL_{c+1/2}) + F-(qR_{c+1/2})        (physics.py:293-297)
+// and both MUSCL states are functions of ONE cell's stencil
+//   qL_{c+1/2} = w_c + (eps/4)[(1-k) Psi+_c D-_c + (1+k) Psi-_c D+_c]
+//   qR_{c-1/2} = w_c - (eps/4)[(1+k) Psi+_c D-_c + (1-k) Psi-_c D+_c]
+// (solver.py:437-474 with f = c+1 resp. f = c), where Psi+-_c are the cell's
+// limiters (solver.py:413-435).  So every cell computes, per direction, the
+// half flux F+ of its high face and F- of its low face (already times the
+// face area), and the residual needs only the neighbours' halves:
+//   R_c = sum_d [F+_c + F-_{c+1}]_d - [F+_{c-1} + F-_c]_d .
+// No limiter arrays, no face loop, no per-face load imbalance: x neighbours
+// are lanes of the same warp (shuffles), y neighbours go through shared
+// memory, z neighbours stay in registers while the CTA marches in k.
+// Tile-edge cells outside the tile (2*TJ in x, 2*TI in y per plane) are extra
+// half-flux items done by the first warps.
+//
+// Per k-plane: B0 barrier | phase A: halves of plane k (x, y) and the z halves
+// of cell k+1 (own column) | AB barrier | phase B: residual, stage-0 dt and
+// sum(R^2), RK update, decode.  TMA traffic: the haloed 5-variable plane k+2
+// and the geometry group of plane k+1 are issued at the AB barrier of plane k
+// (phase B needs no geometry: halves are pre-scaled and wall/farfield
+// overwrites are applied in phase A); Q0/dt of plane k at B0.
+//
+// Used for FAST precision, Van Leer flux, limiters computed (not frozen);
+// the reference-order kernel (bf_stage.cuh) covers EXACT, Roe and the
+// limiter-freeze steps.  Different FP association than the reference (area
+// scaling per half, FMA, Newton reciprocals): held to the 1e-12 bar.
+#pragma once
+
+BF_DEV void tma_prefetch4(const void* tmap, int x, int y, int z, int s) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<unsigned long long>(tmap)),
+               "r"(x), "r"(y), "r"(z), "r"(s)
+               : "memory");
+}
+
+// a / b with a single-Newton reciprocal and one quotient correction (~1 ulp)
+BF_DEV double fdiv1(double a, double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  r = fma(r, fma(-b, r, 1.0), r);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+
+template <int LIM>
+BF_DEV double vl_limiter(double a, double b) {
+  if constexpr (LIM == LIM_NONE) {
+    return 1.0;
+  } else if constexpr (LIM == LIM_VAN_ALBADA) {
+    const double x = fdiv1(fma(2.0 * a, b, 1e-12), fma(a, a, fma(b, b, 1e-12)));
+    return (0.0 >= x) ? 0.0 : x;
+  } else if constexpr (LIM == LIM_MINMOD) {
+    const double r = fdiv1(a, b);
+    return (a * b > 0.0) ? ((1.0 <= r) ? 1.0 : r) : 0.0;
+  } else {
+    const double r = fdiv1(a, b);
+    const double val = fdiv1(2.0 * r, 1.0 + r);
+    return (a * b > 0.0) ? val : 0.0;
+  }
+}
+
+// Both MUSCL states of one cell from its stencil (wm, w0, wp) along a direction:
+// qL at the cell's high face, qR at its low face.  K1: eps = 1, kappa = -1.
+template <int LIM, bool K1>
+BF_DEV void vl_recon(double wm, double w0, double wp, const Consts& c, double& qL, double& qR) {
+  const double dm = w0 - wm, dp = wp - w0;
+  const double pp = vl_limiter<LIM>(dp, dm);
+  const double pm = (psi_count<LIM>() == 2) ? vl_limiter<LIM>(dm, dp) : pp;
+  if constexpr (K1) {
+    qL = fma(0.5 * pp, dm, w0);
+    qR = fma(-0.5 * pm, dp, w0);
+  } else {
+    qL = w0 + c.quarter * fma(c.omk * pp, dm, c.opk * pm * dp);
+    qR = w0 - c.quarter * fma(c.opk * pp, dm, c.omk * pm * dp);
+  }
+}
+
+// One side of the Van Leer splitting (physics.py:267-290) times the face area.
+BF_DEV void vl_half(const double q[5], double nx, double ny, double nz, double A, double sign,
+                    const Consts& c, double F[5]) {
+  const double rinv = frcp(q[0]);
+  const double a2 = c.gamma * q[4] * rinv;
+  const double ainv = frsqrt(a2);
+  const double a = a2 * ainv;
+  const double vn = fma(q[1], nx, fma(q[2], ny, q[3] * nz));
+  const double mn = vn * ainv;
+  const double ke = 0.5 * fma(q[1], q[1], fma(q[2], q[2], q[3] * q[3]));
+  if (fabs(mn) < 1.0) {
+    const double sh = mn + sign;
+    const double fm = ((0.25 * sign) * q[0]) * (a * A) * (sh * sh);
+    const double ta = (2.0 * sign) * a;
+    const double et = fma(c.gm1, vn, ta);
+    const double fac = (ta - vn) * c.inv_gamma;
+    const double ee = fma(et * et, c.inv_vlc, fma(-0.5 * vn, vn, ke));
+    F[0] = fm;
+    F[1] = fm * fma(nx, fac, q[1]);
+    F[2] = fm * fma(ny, fac, q[2]);
+    F[3] = fm * fma(nz, fac, q[3]);
+    F[4] = fm * ee;
+  } else if (sign * mn >= 1.0) {
+    const double m = q[0] * vn * A;
+    const double pA = q[4] * A;
+    F[0] = m;
+    F[1] = fma(m, q[1], nx * pA);
+    F[2] = fma(m, q[2], ny * pA);
+    F[3] = fma(m, q[3], nz * pA);
+    F[4] = m * fma(c.gog1 * q[4], rinv, ke);
+  } else {
+    F[0] = F[1] = F[2] = F[3] = F[4] = 0.0;
+  }
+}
+
+// local-time-step term (solver.py:709-716) of one face
+BF_DEV double lam_term(double u, double v, double w, double snd, double nx, double ny, double nz,
+                       double A) {
+  return (fabs(fma(u, nx, fma(v, ny, w * nz))) + snd) * A;
+}
+
+template <int NDIM, int LIM>
+struct VCfg {
+  static constexpr int TJ = Cfg<NDIM, LIM>::TJ;   // same tiles as the reference-order kernel
+  static constexpr int NT = TI * TJ;
+  static constexpr int PW = TI + 2 * HALO;
+  static constexpr int PH = TJ + 2 * HALO;
+  static constexpr int PLANE = PW * PH;
+  static constexpr int NS = (NDIM == 3) ? NSLOT : 1;
+  static constexpr int NFX = GXW * TJ;             // x geometry [4][TJ][GXW]
+  static constexpr int NFY = TI * (TJ + 1);        // y geometry [4][TJ+1][TI]
+  static constexpr int NHY = TI * (TJ + 1);        // y halves  [5][TJ+1][TI]
+  static constexpr int NH = 2 * TJ + 2 * TI;       // tile-edge half-flux items per plane
+  static constexpr int r16(int x) { return (x + 15) / 16 * 16; }
+  static constexpr int OW = 0;
+  static constexpr int OHP = r16(OW + NS * 5 * PLANE);   // F+_y of rows -1..TJ-1 (index row+1)
+  static constexpr int OHM = r16(OHP + 5 * NHY);         // F-_y of rows 0..TJ   (index row)
+  static constexpr int OXH = r16(OHM + 5 * NHY);         // [2][5][TJ]: F+ of cell -1, F- of cell TI
+  static constexpr int OFX = r16(OXH + 10 * TJ);
+  static constexpr int OFY = r16(OFX + 4 * NFX);
+  static constexpr int OZG = r16(OFY + 4 * NFY);         // [2][4][TJ][TI] z faces (3D)
+  static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
+  static constexpr int OBAR = r16(OQ + 6 * NT);
+  static constexpr int TOTAL = OBAR + 8;
+  static constexpr size_t BYTES = sizeof(double) * TOTAL;
+  static constexpr unsigned WBYTES = 5u * PLANE * 8u;
+  static constexpr unsigned GBYTES = (4u * NFX + 4u * NFY + (NDIM == 3 ? 4u * NT : 0u)) * 8u;
+  BF_DEV static int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
+};
+
+template <int NDIM, int LIM, bool K1, bool S0>
+__global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const StageArgs a) {
+  using K = VCfg<NDIM, LIM>;
+  constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
+  constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
+  extern __shared__ __align__(128) double smem[];
+  double* const sW = smem + K::OW;
+  double* const sHP = smem + K::OHP;
+  double* const sHM = smem + K::OHM;
+  double* const sXH = smem + K::OXH;
+  double* const sFX = smem + K::OFX;
+  double* const sFY = smem + K::OFY;
+  double* const sZG = smem + K::OZG;
+  double* const sQ = smem + K::OQ;
+  unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem + K::OBAR);
+  // bars[0..2]: plane ring, bars[3]: geometry group, bars[4]: Q0 / dt group
+
+  const Tile t = a.tiles[blockIdx.x];
+  const DevBlock b = a.blocks[t.block];
+  const Consts& c = a.c;
+  const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
+  const int tid = threadIdx.x;
+  const int tx = tid % TI, ty = tid / TI;
+  const int i0 = t.i0, j0 = t.j0, k0 = t.k0, kc = t.kc;
+  const int ni = b.n[0], nj = b.n[1], nk = (NDIM == 3) ? b.n[2] : 1;
+  const long long sy = b.sy, sz = b.sz, fsz = b.fsz;
+  const int i = i0 + tx, j = j0 + ty;
+  const bool in_i = i < ni, in_j = j < nj;
+  const bool cell_on = in_i && in_j;
+  const int flags = a.flags;
+  constexpr bool stage0 = S0;   // first RK stage: dt/V and sum(R^2)
+  const bool last = flags & F_LAST;
+  const int stage = a.stage;
+  const double* const Win = b.base + (long long)fw(a.cur, 0) * fsz;
+  double* const Wout = b.base + (long long)fw(a.cur ^ 1, 0) * fsz;
+  const long long colofs = i + sy * (long long)j;
+  const int s0 = K::pidx(tx, ty);
+  const unsigned FULL = 0xffffffffu;
+
+  auto slot_of = [&](int k) -> double* {
+    if constexpr (NDIM == 3) return sW + ((k - k0 + 1) % NSLOT) * 5 * PLANE;
+    else return sW;
+  };
+  auto bar_of = [&](int k) { return bars + ((NDIM == 3) ? (k - k0 + 1) % NSLOT : 0); };
+  auto par_of = [&](int k) { return (unsigned)(((NDIM == 3) ? (k - k0 + 1) / NSLOT : 0) & 1); };
+  auto zslot = [&](int face) -> double* {   // z face `face` lives in slot (face - k0) & 1
+    return sZG + ((face - k0) & 1) * 4 * NT;
+  };
+
+  auto issue_plane = [&](int k) {
+    unsigned long long* bar = bar_of(k);
+    mbar_expect_tx(bar, K::WBYTES);
+    tma_load4(slot_of(k), tm + 0 * 128, b.ox + i0 - HALO, b.oy + j0 - HALO,
+              (NDIM == 3) ? b.oz + k : 0, fw(a.cur, 0), bar);
+  };
+  auto issue_geo = [&](int k) {   // x / y face geometry of plane k, z face k+2
+    unsigned long long* bar = bars + 3;
+    const int z = (NDIM == 3) ? b.oz + k : 0;
+    mbar_expect_tx(bar, K::GBYTES);
+    tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+    tma_load4(sFY, tm + 2 * 128, b.ox + i0, b.oy + j0, z, ffn(1, 0), bar);
+    if constexpr (NDIM == 3) tma_load4(zslot(k + 2), tm + 5 * 128, b.ox + i0, b.oy + j0, z + 2,
+                                       ffn(2, 0), bar);
+  };
+  auto prefetch_geo = [&](int k) {
+    const int z = (NDIM == 3) ? b.oz + k : 0;
+    tma_prefetch4(tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0));
+    tma_prefetch4(tm + 2 * 128, b.ox + i0, b.oy + j0, z, ffn(1, 0));
+    if constexpr (NDIM == 3) tma_prefetch4(tm + 5 * 128, b.ox + i0, b.oy + j0, z + 2, ffn(2, 0));
+    tma_prefetch4(tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ);
+  };
+  auto issue_q = [&](int k) {     // Q0 (and dt/V after stage 0) of plane k
+    unsigned long long* bar = bars + 4;
+    const int z = (NDIM == 3) ? b.oz + k : 0;
+    mbar_expect_tx(bar, (stage0 ? 5u : 6u) * NT * 8u);
+    tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
+    if (!stage0) tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV, bar);
+  };
+
+  auto face_err = [&](int d, int kind, unsigned long long lin) {
+    record_error(a.err, make_err_key(stage, 0, b.order, d, kind, lin));
+  };
+  // C-order linear face index of the reference's face arrays (solver.py:501-506)
+  auto lin_x = [&](int f, int jj, int k) {
+    return ((unsigned long long)f * nj + jj) * (unsigned long long)nk + (NDIM == 3 ? k : 0);
+  };
+  auto lin_y = [&](int ii, int f, int k) {
+    return ((unsigned long long)ii * (nj + 1) + f) * (unsigned long long)nk + (NDIM == 3 ? k : 0);
+  };
+  auto lin_z = [&](int ii, int jj, int f) {
+    return ((unsigned long long)ii * nj + jj) * (unsigned long long)(nk + 1) + f;
+  };
+  // wall / farfield flux of a boundary face (solver.py:526-580); wv[0..3] are
+  // the var-0 pointers of cells f-2..f+1 (stride vs)
+  auto overwrite = [&](int bk, double sg, const double* w0p, const double* w1p, const double* w2p,
+                       const double* w3p, int vs, const double* g, int gs, double F[5]) {
+    boundary_overwrite(bk, sg, w0p, w1p, w2p, w3p, vs, g[0], g[gs], g[2 * gs], g[3 * gs], c, F);
+  };
+
+  // ---- state carried along k (3D) ---------------------------------------------------
+  double hpz[5] = {0, 0, 0, 0, 0};   // F+_z of cell k (times A_{k+1/2})
+  double fzl[5] = {0, 0, 0, 0, 0};   // z flux of face k (times A), the low face of cell k
+  double lamz = 0.0;                 // z part of the stage-0 lambda of cell k
+  double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+
+  if (tid == 0) {
+    for (int q = 0; q < 5; ++q) mbar_init(bars + q, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if constexpr (NDIM == 3) {
+      issue_plane(k0 - 1);
+      issue_plane(k0);
+      issue_plane(k0 + 1);
+    } else {
+      issue_plane(0);
+    }
+    issue_geo(k0);
+  }
+
+  // z half fluxes of cell kc (own column): w[0..2] = W(kc-1), W(kc), W(kc+1);
+  // glo / ghi: geometry of faces kc, kc+1 (stride gs)
+  auto z_halves = [&](int kcell, const double wa[5], const double wb[5], const double wc[5],
+                      const double* glo, const double* ghi, int gs, double hp[5], double hm[5],
+                      bool want_hp) {
+    double qL[5], qR[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) vl_recon<LIM, K1>(wa[v], wb[v], wc[v], c, qL[v], qR[v]);
+    vl_half(qR, glo[0], glo[gs], glo[2 * gs], glo[3 * gs], -1.0, c, hm);
+    if (want_hp) vl_half(qL, ghi[0], ghi[gs], ghi[2 * gs], ghi[3 * gs], 1.0, c, hp);
+    const double mL = fmin(qL[0], qL[4]), mR = fmin(qR[0], qR[4]);
+    if (fmin(mL, mR) <= 0.0) {
+      // qL belongs to face kcell+1 (valid while kcell <= nk-1), qR to face kcell
+      if (want_hp && mL <= 0.0 && kcell <= nk - 1) face_err(2, ERR_FACE_LEFT, lin_z(i, j, kcell + 1));
+      if (mR <= 0.0 && kcell >= 0) face_err(2, ERR_FACE_RIGHT, lin_z(i, j, kcell));
+    }
+  };
+
+  if constexpr (NDIM == 3) {
+    // ---- prologue: F+_z(k0-1), F-_z(k0), F+_z(k0), z flux of face k0 ----------------
+    double wa[5], wb[5], wc[5], wd[5];
+    double g0[4] = {0, 0, 0, 0}, g1[4] = {0, 0, 0, 0};
+    if (cell_on) {
+      const long long o = colofs + sz * (long long)(k0 - 2);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) wa[v] = Win[v * fsz + o];
+      const double* fn = b.base + (long long)ffn(2, 0) * fsz + colofs + sz * (long long)k0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        g0[q] = __ldg(fn + q * fsz);
+        g1[q] = __ldg(fn + q * fsz + sz);
+      }
+    }
+    // face k0+1 geometry for iteration 0 (slot of face k0+1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) zslot(k0 + 1)[q * NT + tid] = g1[q];
+    mbar_wait(bar_of(k0 - 1), par_of(k0 - 1));
+    mbar_wait(bar_of(k0), par_of(k0));
+    mbar_wait(bar_of(k0 + 1), par_of(k0 + 1));
+    if (cell_on) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        wb[v] = slot_of(k0 - 1)[v * PLANE + s0];
+        wc[v] = slot_of(k0)[v * PLANE + s0];
+        wd[v] = slot_of(k0 + 1)[v * PLANE + s0];
+      }
+      double hp_prev[5], hm0[5];
+      {   // cell k0-1: only its F+ (face k0) is needed
+        double qL[5], qR[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) vl_recon<LIM, K1>(wa[v], wb[v], wc[v], c, qL[v], qR[v]);
+        vl_half(qL, g0[0], g0[1], g0[2], g0[3], 1.0, c, hp_prev);
+        if (fmin(qL[0], qL[4]) <= 0.0) face_err(2, ERR_FACE_LEFT, lin_z(i, j, k0));
+      }
+      z_halves(k0, wb, wc, wd, g0, g1, 1, hpz, hm0, true);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) fzl[v] = hp_prev[v] + hm0[v];
+      if (k0 == 0) {
+        const int bk = b.bface[4][i + ni * j];
+        if (bk != BFACE_NONE) {
+          const double st[4][5] = {{wa[0], wa[1], wa[2], wa[3], wa[4]},
+                                   {wb[0], wb[1], wb[2], wb[3], wb[4]},
+                                   {wc[0], wc[1], wc[2], wc[3], wc[4]},
+                                   {wd[0], wd[1], wd[2], wd[3], wd[4]}};
+          overwrite(bk, -1.0, st[0], st[1], st[2], st[3], 1, g0, 1, fzl);
+        }
+      }
+      if (stage0) {
+        const double snd = fsqrt(c.gamma * wc[4] * frcp(wc[0]));
+        lamz = lam_term(wc[1], wc[2], wc[3], snd, g0[0], g0[1], g0[2], g0[3]) +
+               lam_term(wc[1], wc[2], wc[3], snd, g1[0], g1[1], g1[2], g1[3]);
+      }
+    }
+  }
+
+  for (int kk = 0; kk < kc; ++kk) {
+    const int k = k0 + kk;
+    const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
+    const double* const pk = slot_of(k);
+
+    __syncthreads();   // B0: plane k-1 retired (y halves, Q0 slots free)
+    if (tid == 0) {
+      fence_async_smem();
+      issue_q(k);
+    }
+    // own-column W(k+2) for the z stencil of cell k+1 (latency hidden by phase A)
+    double wz2[5] = {0, 0, 0, 0, 0};
+    if constexpr (NDIM == 3) {
+      if (cell_on) {
+        const long long o = colofs + sz * (long long)(k + 2);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) wz2[v] = Win[v * fsz + o];
+      }
+    }
+    mbar_wait(bars + 3, (unsigned)(kk & 1));
+    mbar_wait(bar_of(k), par_of(k));
+
+    // ---- phase A1: tile-edge half fluxes --------------------------------------------
+    if (tid < K::NH) {
+      const int h = tid;
+      int cx, cy, st, d, fo;
+      double sg;
+      const double* g;
+      int gs;
+      double* out;
+      int os;
+      bool valid;
+      unsigned long long lin;
+      if (h < 2 * TJ) {                       // x: F+ of cell -1 (face 0), F- of cell TI (face TI)
+        const int row = h % TJ, hi = h / TJ;
+        cx = hi ? TI : -1;
+        cy = row;
+        st = 1;
+        d = 0;
+        sg = hi ? -1.0 : 1.0;
+        fo = hi ? TI : 0;
+        g = sFX + row * GXW + fo;
+        gs = NFX;
+        out = sXH + hi * 5 * TJ + row;
+        os = TJ;
+        valid = (j0 + row < nj) && (i0 + fo <= ni);
+        lin = lin_x(i0 + fo, j0 + row, k);
+      } else {                                // y: F+ of row -1 (face 0), F- of row TJ (face TJ)
+        const int e = h - 2 * TJ;
+        const int col = e % TI, hi = e / TI;
+        cx = col;
+        cy = hi ? TJ : -1;
+        st = PW;
+        d = 1;
+        sg = hi ? -1.0 : 1.0;
+        fo = hi ? TJ : 0;
+        g = sFY + fo * TI + col;
+        gs = NFY;
+        out = hi ? sHM + TJ * TI + col : sHP + col;
+        os = NHY;
+        valid = (i0 + col < ni) && (j0 + fo <= nj);
+        lin = lin_y(i0 + col, j0 + fo, k);
+      }
+      const double* w = pk + K::pidx(cx, cy);
+      double q5[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        double qL, qR;
+        vl_recon<LIM, K1>(w[v * PLANE - st], w[v * PLANE], w[v * PLANE + st], c, qL, qR);
+        q5[v] = sg > 0.0 ? qL : qR;
+      }
+      double F[5];
+      vl_half(q5, g[0], g[gs], g[2 * gs], g[3 * gs], sg, c, F);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) out[v * os] = F[v];
+      if (valid && fmin(q5[0], q5[4]) <= 0.0)
+        face_err(d, sg > 0.0 ? ERR_FACE_LEFT : ERR_FACE_RIGHT, lin);
+    }
+
+
+    // ---- phase A2: y halves -> shared memory ---------------------------------------
+    const double* const w = pk + s0;
+    bool ylo_ovw = false, yhi_ovw = false;
+    {
+      double qL[5], qR[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+        vl_recon<LIM, K1>(w[v * PLANE - PW], w[v * PLANE], w[v * PLANE + PW], c, qL[v], qR[v]);
+      const double* gl = sFY + ty * TI + tx;    // face j (low); face j+1 at gl + TI
+      double hp[5], hm[5];
+      vl_half(qL, gl[TI], gl[NFY + TI], gl[2 * NFY + TI], gl[3 * NFY + TI], 1.0, c, hp);
+      vl_half(qR, gl[0], gl[NFY], gl[2 * NFY], gl[3 * NFY], -1.0, c, hm);
+      const double mL = fmin(qL[0], qL[4]), mR = fmin(qR[0], qR[4]);
+      if (fmin(mL, mR) <= 0.0 && in_i) {
+        if (mL <= 0.0 && in_j) face_err(1, ERR_FACE_LEFT, lin_y(i, j + 1, k));
+        if (mR <= 0.0 && j <= nj) face_err(1, ERR_FACE_RIGHT, lin_y(i, j, k));
+      }
+      if (in_i && (j == 0 || j == nj - 1)) {
+        if (j == 0) {   // whole face flux into the F- slot; phase B drops the F+ half
+          const int bk = b.bface[2][i + ni * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, -1.0, w - 2 * PW, w - PW, w, w + PW, PLANE, gl, NFY, hm);
+            ylo_ovw = true;
+          }
+        }
+        if (j == nj - 1) {   // whole face flux into the F+ slot
+          const int bk = b.bface[3][i + ni * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, 1.0, w - PW, w, w + PW, w + 2 * PW, PLANE, gl + TI, NFY, hp);
+            yhi_ovw = true;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        sHP[v * NHY + (ty + 1) * TI + tx] = hp[v];
+        sHM[v * NHY + ty * TI + tx] = hm[v];
+      }
+    }
+
+    // ---- phase A3: x halves of cell (i, j, k); neighbours by shuffle ----------------
+    double R[5];              // residual being assembled (face fluxes already times A)
+    bool xlo_halo = tx == 0, xhi_halo = tx == TI - 1;
+    {
+      double qL[5], qR[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        vl_recon<LIM, K1>(w[v * PLANE - 1], w[v * PLANE], w[v * PLANE + 1], c, qL[v], qR[v]);
+      }
+      const double* gl = sFX + ty * GXW + tx;   // face i (low); face i+1 at gl + 1
+      double hp[5], hm[5];
+      vl_half(qL, gl[1], gl[NFX + 1], gl[2 * NFX + 1], gl[3 * NFX + 1], 1.0, c, hp);
+      vl_half(qR, gl[0], gl[NFX], gl[2 * NFX], gl[3 * NFX], -1.0, c, hm);
+      const double mL = fmin(qL[0], qL[4]), mR = fmin(qR[0], qR[4]);
+      if (fmin(mL, mR) <= 0.0 && in_j) {
+        if (mL <= 0.0 && in_i) face_err(0, ERR_FACE_LEFT, lin_x(i + 1, j, k));
+        if (mR <= 0.0 && i <= ni) face_err(0, ERR_FACE_RIGHT, lin_x(i, j, k));
+      }
+      double fhi[5], flo[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double hmn = __shfl_down_sync(FULL, hm[v], 1);
+        const double hpp = __shfl_up_sync(FULL, hp[v], 1);
+        // the tile-edge lanes complete these with the halo halves in phase B
+        fhi[v] = xhi_halo ? hp[v] : hp[v] + hmn;
+        flo[v] = xlo_halo ? hm[v] : hpp + hm[v];
+      }
+      if (in_j && (i == 0 || i == ni - 1)) {
+        if (i == 0) {
+          const int bk = b.bface[0][j + nj * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, -1.0, w - 2, w - 1, w, w + 1, PLANE, gl, NFX, flo);
+            xlo_halo = false;
+          }
+        }
+        if (i == ni - 1) {
+          const int bk = b.bface[1][j + nj * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, 1.0, w - 1, w, w + 1, w + 2, PLANE, gl + 1, NFX, fhi);
+            xhi_halo = false;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) R[v] = fhi[v] - flo[v];
+    }
+
+    // ---- stage 0: local time step of cell k (solver.py:696-731, dt/V = cfl/lambda) --
+    double dtv = 0.0;
+    if (stage0 && cell_on) {
+      double w0[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) w0[v] = w[v * PLANE];
+      const double snd = fsqrt(c.gamma * w0[4] * frcp(w0[0]));
+      const double* gx = sFX + ty * GXW + tx;
+      const double* gy = sFY + ty * TI + tx;
+      double lam = lam_term(w0[1], w0[2], w0[3], snd, gx[0], gx[NFX], gx[2 * NFX], gx[3 * NFX]) +
+                   lam_term(w0[1], w0[2], w0[3], snd, gx[1], gx[NFX + 1], gx[2 * NFX + 1],
+                            gx[3 * NFX + 1]) +
+                   lam_term(w0[1], w0[2], w0[3], snd, gy[0], gy[NFY], gy[2 * NFY], gy[3 * NFY]) +
+                   lam_term(w0[1], w0[2], w0[3], snd, gy[TI], gy[NFY + TI], gy[2 * NFY + TI],
+                            gy[3 * NFY + TI]);
+      if constexpr (NDIM == 3) lam += lamz;
+      dtv = c.cfl * frcp(lam);
+      b.base[(long long)FDTV * fsz + colofs + kofs] = dtv;
+    }
+
+    // ---- phase A4 (3D): z halves of cell k+1, z flux of face k+1 ---------------------
+    if constexpr (NDIM == 3) {
+      mbar_wait(bar_of(k + 1), par_of(k + 1));
+      if (cell_on) {
+        const double* p1 = slot_of(k + 1) + s0;
+        double w0[5], wc[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          w0[v] = w[v * PLANE];
+          wc[v] = p1[v * PLANE];
+        }
+        const double* glo = zslot(k + 1) + tid;
+        const double* ghi = zslot(k + 2) + tid;
+        double hp1[5], hm1[5], fhi[5];
+        z_halves(k + 1, w0, wc, wz2, glo, ghi, NT, hp1, hm1, true);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) fhi[v] = hpz[v] + hm1[v];
+        if (k == nk - 1) {
+          const int bk = b.bface[5][i + ni * j];
+          if (bk != BFACE_NONE) {
+            const double* pm1 = slot_of(k - 1) + s0;
+            double st[4][5];
+#pragma unroll
+            for (int v = 0; v < 5; ++v) {
+              st[0][v] = pm1[v * PLANE];
+              st[1][v] = w0[v];
+              st[2][v] = wc[v];
+              st[3][v] = wz2[v];
+            }
+            overwrite(bk, 1.0, st[0], st[1], st[2], st[3], 1, glo, NT, fhi);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          R[v] += fhi[v] - fzl[v];
+          fzl[v] = fhi[v];
+          hpz[v] = hp1[v];
+        }
+        if (stage0) {
+          const double snd = fsqrt(c.gamma * wc[4] * frcp(wc[0]));
+          lamz = lam_term(wc[1], wc[2], wc[3], snd, glo[0], glo[NT], glo[2 * NT], glo[3 * NT]) +
+                 lam_term(wc[1], wc[2], wc[3], snd, ghi[0], ghi[NT], ghi[2 * NT], ghi[3 * NT]);
+        }
+      }
+    }
+
+    __syncthreads();   // AB: y halves and tile-edge halves of plane k complete
+    if (tid == 0) {
+      fence_async_smem();
+      if (kk + 1 < kc) {
+        if constexpr (NDIM == 3) issue_plane(k + 2);
+        issue_geo(k + 1);
+      }
+      if (kk + 2 < kc) prefetch_geo(k + 2);
+    }
+
+    // ---- phase B: residual, update of cell (i, j, k) ----------------------------------
+    if (cell_on) {
+      const int hi = (ty + 1) * TI + tx, lo = ty * TI + tx;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double* HP = sHP + v * NHY;
+        const double* HM = sHM + v * NHY;
+        const double fyh = yhi_ovw ? HP[hi] : HP[hi] + HM[hi];
+        const double fyl = ylo_ovw ? HM[lo] : HP[lo] + HM[lo];
+        double r = R[v] + (fyh - fyl);
+        if (xlo_halo) r -= sXH[v * TJ + ty];
+        if (xhi_halo) r += sXH[5 * TJ + v * TJ + ty];
+        R[v] = r;
+      }
+      const long long co = colofs + kofs;
+      if (flags & F_SOURCE) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) R[v] = R[v] - b.base[(long long)(FSRC + v) * fsz + co];
+      }
+      mbar_wait(bars + 4, (unsigned)(kk & 1));
+      if (stage0) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) rsum[v] = fma(R[v], R[v], rsum[v]);
+      } else {
+        dtv = sQ[5 * NT + tid];
+      }
+      const double adt = a.alpha * dtv;
+      double qn[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) qn[v] = fma(-adt, R[v], sQ[v * NT + tid]);
+      const double rq = frcp(qn[0]);
+      const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
+      const double pp = c.gm1 * fma(-0.5, fma(qn[1], uu, fma(qn[2], vv, qn[3] * ww)), qn[4]);
+      if (qn[0] <= 0.0 || pp <= 0.0) {
+        const unsigned long long lin =
+            ((unsigned long long)i * nj + j) * (unsigned long long)nk + (NDIM == 3 ? k : 0);
+        record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
+      }
+      Wout[co] = qn[0];
+      Wout[fsz + co] = uu;
+      Wout[2 * fsz + co] = vv;
+      Wout[3 * fsz + co] = ww;
+      Wout[4 * fsz + co] = pp;
+      if (last) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
+      }
+    }
+  }
+
+  // ---- deterministic per-tile sum(R^2) ----------------------------------------
+  if (stage0) {
+    __syncthreads();
+    double* red = sQ;   // free after the last phase B: [NT/32][5]
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      double x = rsum[v];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
+      if ((tid & 31) == 0) red[(tid >> 5) * 5 + v] = x;
+    }
+    __syncthreads();
+    if (tid < 5) {
+      double x = 0.0;
+      for (int q = 0; q < NT / 32; ++q) x += red[q * 5 + tid];
+      a.partial[(long long)blockIdx.x * 5 + tid] = x;
+    }
+  }
+}
+
+template <int NDIM, int LIM, bool K1, bool S0>
+static cudaError_t launch_vl_s(const StageArgs& a, cudaStream_t s) {
+  using K = VCfg<NDIM, LIM>;
+  auto k = vl_stage_kernel<NDIM, LIM, K1, S0>;
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_done & (1ull << dev))) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done |= (1ull << dev);
+  }
+  if (a.ntiles == 0) return cudaSuccess;
+  k<<<a.ntiles, K::NT, K::BYTES, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NDIM, int LIM, bool K1>
+static cudaError_t launch_vl_t(const StageArgs& a, cudaStream_t s) {
+  return (a.flags & F_STAGE0) ? launch_vl_s<NDIM, LIM, K1, true>(a, s)
+                              : launch_vl_s<NDIM, LIM, K1, false>(a, s);
+}
+
+template <int NDIM, bool K1>
+static cudaError_t launch_vl_l(int lim, const StageArgs& a, cudaStream_t s) {
+  switch (lim) {
+    case LIM_NONE: return launch_vl_t<NDIM, LIM_NONE, K1>(a, s);
+    case LIM_VAN_LEER: return launch_vl_t<NDIM, LIM_VAN_LEER, K1>(a, s);
+    case LIM_VAN_ALBADA: return launch_vl_t<NDIM, LIM_VAN_ALBADA, K1>(a, s);
+    default: return launch_vl_t<NDIM, LIM_MINMOD, K1>(a, s);
+  }
+}
+
+static cudaError_t launch_vl(int ndim, int lim, const StageArgs& a, cudaStream_t s) {
+  const bool k1 = a.c.muscl_k1 != 0;
+  if (ndim == 3) return k1 ? launch_vl_l<3, true>(lim, a, s) : launch_vl_l<3, false>(lim, a, s);
+  return k1 ? launch_vl_l<2, true>(lim, a, s) : launch_vl_l<2, false>(lim, a, s);
+}
