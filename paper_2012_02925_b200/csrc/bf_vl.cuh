@@ -51,8 +51,7 @@ BF_DEV double vl_limiter(double a, double b) {
   if constexpr (LIM == LIM_NONE) {
     return 1.0;
   } else if constexpr (LIM == LIM_VAN_ALBADA) {
-    const double x = fdiv1(fma(2.0 * a, b, 1e-12), fma(a, a, fma(b, b, 1e-12)));
-    return (0.0 >= x) ? 0.0 : x;
+    return fmax(fdiv1(fma(2.0 * a, b, 1e-12), fma(a, a, fma(b, b, 1e-12))), 0.0);
   } else if constexpr (LIM == LIM_MINMOD) {
     const double r = fdiv1(a, b);
     return (a * b > 0.0) ? ((1.0 <= r) ? 1.0 : r) : 0.0;
@@ -189,11 +188,11 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   const unsigned FULL = 0xffffffffu;
 
   auto slot_of = [&](int k) -> double* {
-    if constexpr (NDIM == 3) return sW + ((k - k0 + 1) % NSLOT) * 5 * PLANE;
+    if constexpr (NDIM == 3) return sW + ((k - k0) % NSLOT) * 5 * PLANE;
     else return sW;
   };
-  auto bar_of = [&](int k) { return bars + ((NDIM == 3) ? (k - k0 + 1) % NSLOT : 0); };
-  auto par_of = [&](int k) { return (unsigned)(((NDIM == 3) ? (k - k0 + 1) / NSLOT : 0) & 1); };
+  auto bar_of = [&](int k) { return bars + ((NDIM == 3) ? (k - k0) % NSLOT : 0); };
+  auto par_of = [&](int k) { return (unsigned)(((NDIM == 3) ? (k - k0) / NSLOT : 0) & 1); };
   auto zslot = [&](int face) -> double* {   // z face `face` lives in slot (face - k0) & 1
     return sZG + ((face - k0) & 1) * 4 * NT;
   };
@@ -243,9 +242,27 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   };
   // wall / farfield flux of a boundary face (solver.py:526-580); wv[0..3] are
   // the var-0 pointers of cells f-2..f+1 (stride vs)
-  auto overwrite = [&](int bk, double sg, const double* w0p, const double* w1p, const double* w2p,
-                       const double* w3p, int vs, const double* g, int gs, double F[5]) {
-    boundary_overwrite(bk, sg, w0p, w1p, w2p, w3p, vs, g[0], g[gs], g[2 * gs], g[3 * gs], c, F);
+  // wall / farfield flux (times A) of a boundary face (solver.py:526-580).
+  // in1 / in2: first / second interior cell, gh: the ghost cell across the
+  // face.  For a farfield patch the ghost fill already stored
+  // farfield_state(in1, outward n) in every ghost layer (solver.py:138-171,
+  // ghost_kernel BC_FARFIELD), so the overwrite flux is its Euler flux.
+  auto overwrite = [&](int bk, const double* in1, const double* in2, const double* gh, int vs,
+                       const double* g, int gs, double F[5]) {
+    const double nx = g[0], ny = g[gs], nz = g[2 * gs], A = g[3 * gs];
+    if (bk == BFACE_WALL) {
+      const double pw = fma(1.5, in1[4 * vs], -0.5 * in2[4 * vs]) * A;
+      F[0] = 0.0;
+      F[1] = nx * pw;
+      F[2] = ny * pw;
+      F[3] = nz * pw;
+      F[4] = 0.0;
+    } else {
+      const St q{gh[0], gh[vs], gh[2 * vs], gh[3 * vs], gh[4 * vs]};
+      euler_flux(q, nx, ny, nz, c, F);
+#pragma unroll
+      for (int e = 0; e < 5; ++e) F[e] = F[e] * A;
+    }
   };
 
   // ---- state carried along k (3D) ---------------------------------------------------
@@ -261,9 +278,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   __syncthreads();
   if (tid == 0) {
     if constexpr (NDIM == 3) {
-      issue_plane(k0 - 1);
       issue_plane(k0);
       issue_plane(k0 + 1);
+      issue_plane(k0 + 2);
     } else {
       issue_plane(0);
     }
@@ -295,7 +312,10 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     if (cell_on) {
       const long long o = colofs + sz * (long long)(k0 - 2);
 #pragma unroll
-      for (int v = 0; v < 5; ++v) wa[v] = Win[v * fsz + o];
+      for (int v = 0; v < 5; ++v) {
+        wa[v] = Win[v * fsz + o];
+        wb[v] = Win[v * fsz + o + sz];
+      }
       const double* fn = b.base + (long long)ffn(2, 0) * fsz + colofs + sz * (long long)k0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -306,13 +326,11 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     // face k0+1 geometry for iteration 0 (slot of face k0+1)
 #pragma unroll
     for (int q = 0; q < 4; ++q) zslot(k0 + 1)[q * NT + tid] = g1[q];
-    mbar_wait(bar_of(k0 - 1), par_of(k0 - 1));
     mbar_wait(bar_of(k0), par_of(k0));
     mbar_wait(bar_of(k0 + 1), par_of(k0 + 1));
     if (cell_on) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
-        wb[v] = slot_of(k0 - 1)[v * PLANE + s0];
         wc[v] = slot_of(k0)[v * PLANE + s0];
         wd[v] = slot_of(k0 + 1)[v * PLANE + s0];
       }
@@ -330,11 +348,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
       if (k0 == 0) {
         const int bk = b.bface[4][i + ni * j];
         if (bk != BFACE_NONE) {
-          const double st[4][5] = {{wa[0], wa[1], wa[2], wa[3], wa[4]},
-                                   {wb[0], wb[1], wb[2], wb[3], wb[4]},
-                                   {wc[0], wc[1], wc[2], wc[3], wc[4]},
-                                   {wd[0], wd[1], wd[2], wd[3], wd[4]}};
-          overwrite(bk, -1.0, st[0], st[1], st[2], st[3], 1, g0, 1, fzl);
+          overwrite(bk, wc, wd, wb, 1, g0, 1, fzl);
         }
       }
       if (stage0) {
@@ -354,15 +368,6 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     if (tid == 0) {
       fence_async_smem();
       issue_q(k);
-    }
-    // own-column W(k+2) for the z stencil of cell k+1 (latency hidden by phase A)
-    double wz2[5] = {0, 0, 0, 0, 0};
-    if constexpr (NDIM == 3) {
-      if (cell_on) {
-        const long long o = colofs + sz * (long long)(k + 2);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) wz2[v] = Win[v * fsz + o];
-      }
     }
     mbar_wait(bars + 3, (unsigned)(kk & 1));
     mbar_wait(bar_of(k), par_of(k));
@@ -446,14 +451,14 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         if (j == 0) {   // whole face flux into the F- slot; phase B drops the F+ half
           const int bk = b.bface[2][i + ni * (NDIM == 3 ? k : 0)];
           if (bk != BFACE_NONE) {
-            overwrite(bk, -1.0, w - 2 * PW, w - PW, w, w + PW, PLANE, gl, NFY, hm);
+            overwrite(bk, w, w + PW, w - PW, PLANE, gl, NFY, hm);
             ylo_ovw = true;
           }
         }
         if (j == nj - 1) {   // whole face flux into the F+ slot
           const int bk = b.bface[3][i + ni * (NDIM == 3 ? k : 0)];
           if (bk != BFACE_NONE) {
-            overwrite(bk, 1.0, w - PW, w, w + PW, w + 2 * PW, PLANE, gl + TI, NFY, hp);
+            overwrite(bk, w, w - PW, w + PW, PLANE, gl + TI, NFY, hp);
             yhi_ovw = true;
           }
         }
@@ -496,14 +501,14 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         if (i == 0) {
           const int bk = b.bface[0][j + nj * (NDIM == 3 ? k : 0)];
           if (bk != BFACE_NONE) {
-            overwrite(bk, -1.0, w - 2, w - 1, w, w + 1, PLANE, gl, NFX, flo);
+            overwrite(bk, w, w + 1, w - 1, PLANE, gl, NFX, flo);
             xlo_halo = false;
           }
         }
         if (i == ni - 1) {
           const int bk = b.bface[1][j + nj * (NDIM == 3 ? k : 0)];
           if (bk != BFACE_NONE) {
-            overwrite(bk, 1.0, w - 1, w, w + 1, w + 2, PLANE, gl + 1, NFX, fhi);
+            overwrite(bk, w, w - 1, w + 1, PLANE, gl + 1, NFX, fhi);
             xhi_halo = false;
           }
         }
@@ -534,14 +539,16 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
 
     // ---- phase A4 (3D): z halves of cell k+1, z flux of face k+1 ---------------------
     if constexpr (NDIM == 3) {
-      mbar_wait(bar_of(k + 1), par_of(k + 1));
+      mbar_wait(bar_of(k + 2), par_of(k + 2));
       if (cell_on) {
         const double* p1 = slot_of(k + 1) + s0;
-        double w0[5], wc[5];
+        const double* p2 = slot_of(k + 2) + s0;
+        double w0[5], wc[5], wz2[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           w0[v] = w[v * PLANE];
           wc[v] = p1[v * PLANE];
+          wz2[v] = p2[v * PLANE];
         }
         const double* glo = zslot(k + 1) + tid;
         const double* ghi = zslot(k + 2) + tid;
@@ -552,16 +559,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         if (k == nk - 1) {
           const int bk = b.bface[5][i + ni * j];
           if (bk != BFACE_NONE) {
-            const double* pm1 = slot_of(k - 1) + s0;
-            double st[4][5];
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-              st[0][v] = pm1[v * PLANE];
-              st[1][v] = w0[v];
-              st[2][v] = wc[v];
-              st[3][v] = wz2[v];
-            }
-            overwrite(bk, 1.0, st[0], st[1], st[2], st[3], 1, glo, NT, fhi);
+            double wm1[5] = {0, 0, 0, 0, 0};   // W(k-1): walls only (plane k-1 has left the ring)
+            if (bk == BFACE_WALL) wm1[4] = Win[4 * fsz + colofs + sz * (long long)(k - 1)];
+            overwrite(bk, w0, wm1, wc, 1, glo, NT, fhi);
           }
         }
 #pragma unroll
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     if (tid == 0) {
       fence_async_smem();
       if (kk + 1 < kc) {
-        if constexpr (NDIM == 3) issue_plane(k + 2);
+        if constexpr (NDIM == 3) issue_plane(k + 3);   // into the slot of plane k
         issue_geo(k + 1);
       }
       if (kk + 2 < kc) prefetch_geo(k + 2);
