@@ -144,7 +144,8 @@ struct VCfg {
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr unsigned WBYTES = 5u * PLANE * 8u;
-  static constexpr unsigned GBYTES = (4u * NFX + 4u * NFY + (NDIM == 3 ? 4u * NT : 0u)) * 8u;
+  static constexpr unsigned GYZBYTES = (4u * NFY + (NDIM == 3 ? 4u * NT : 0u)) * 8u;
+  static constexpr unsigned GXBYTES = 4u * NFX * 8u;
   BF_DEV static int pidx(int ii, int jj) { return (jj + HALO) * PW + (ii + HALO); }
 };
 
@@ -203,28 +204,28 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     tma_load4(slot_of(k), tm + 0 * 128, b.ox + i0 - HALO, b.oy + j0 - HALO,
               (NDIM == 3) ? b.oz + k : 0, fw(a.cur, 0), bar);
   };
-  auto issue_geo = [&](int k) {   // x / y face geometry of plane k, z face k+2
+  auto issue_geo_yz = [&](int k) {   // y face geometry of plane k, z face k+2 (phase A)
     unsigned long long* bar = bars + 3;
     const int z = (NDIM == 3) ? b.oz + k : 0;
-    mbar_expect_tx(bar, K::GBYTES);
-    tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+    mbar_expect_tx(bar, K::GYZBYTES);
     tma_load4(sFY, tm + 2 * 128, b.ox + i0, b.oy + j0, z, ffn(1, 0), bar);
     if constexpr (NDIM == 3) tma_load4(zslot(k + 2), tm + 5 * 128, b.ox + i0, b.oy + j0, z + 2,
                                        ffn(2, 0), bar);
   };
-  auto prefetch_geo = [&](int k) {
+  auto issue_b = [&](int k) {        // x face geometry, Q0 (and dt/V) of plane k (phase B)
+    unsigned long long* bar = bars + 4;
+    const int z = (NDIM == 3) ? b.oz + k : 0;
+    mbar_expect_tx(bar, K::GXBYTES + (stage0 ? 5u : 6u) * NT * 8u);
+    tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+    tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
+    if (!stage0) tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV, bar);
+  };
+  auto prefetch_l2 = [&](int k) {    // geometry and Q0 of plane k into L2
     const int z = (NDIM == 3) ? b.oz + k : 0;
     tma_prefetch4(tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0));
     tma_prefetch4(tm + 2 * 128, b.ox + i0, b.oy + j0, z, ffn(1, 0));
     if constexpr (NDIM == 3) tma_prefetch4(tm + 5 * 128, b.ox + i0, b.oy + j0, z + 2, ffn(2, 0));
     tma_prefetch4(tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ);
-  };
-  auto issue_q = [&](int k) {     // Q0 (and dt/V after stage 0) of plane k
-    unsigned long long* bar = bars + 4;
-    const int z = (NDIM == 3) ? b.oz + k : 0;
-    mbar_expect_tx(bar, (stage0 ? 5u : 6u) * NT * 8u);
-    tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
-    if (!stage0) tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV, bar);
   };
 
   auto face_err = [&](int d, int kind, unsigned long long lin) {
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     } else {
       issue_plane(0);
     }
-    issue_geo(k0);
+    issue_geo_yz(k0);
   }
 
   // z half fluxes of cell kc (own column): w[0..2] = W(kc-1), W(kc), W(kc+1);
@@ -363,27 +364,30 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     const int k = k0 + kk;
     const long long kofs = (NDIM == 3) ? sz * (long long)k : 0;
     const double* const pk = slot_of(k);
+    const double* const w = pk + s0;
 
-    __syncthreads();   // B0: plane k-1 retired (y halves, Q0 slots free)
+    __syncthreads();   // B0: plane k-1 retired (its ring slot, x geometry, y halves, Q0)
     if (tid == 0) {
       fence_async_smem();
-      issue_q(k);
+      issue_b(k);
+      if constexpr (NDIM == 3) {
+        if (kk > 0) issue_plane(k + 2);   // into the slot of plane k-1
+      }
     }
     mbar_wait(bars + 3, (unsigned)(kk & 1));
     mbar_wait(bar_of(k), par_of(k));
 
-    // ---- phase A1: tile-edge half fluxes --------------------------------------------
+    // ---- phase A1: tile-edge half fluxes ----------------------------------------------
     if (tid < K::NH) {
       const int h = tid;
       int cx, cy, st, d, fo;
       double sg;
-      const double* g;
-      int gs;
+      double g[4];
       double* out;
       int os;
       bool valid;
       unsigned long long lin;
-      if (h < 2 * TJ) {                       // x: F+ of cell -1 (face 0), F- of cell TI (face TI)
+      if (h < 2 * TJ) {   // x: F+ of cell -1 (face i0), F- of cell TI (face i0+TI)
         const int row = h % TJ, hi = h / TJ;
         cx = hi ? TI : -1;
         cy = row;
@@ -391,13 +395,16 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         d = 0;
         sg = hi ? -1.0 : 1.0;
         fo = hi ? TI : 0;
-        g = sFX + row * GXW + fo;
-        gs = NFX;
         out = sXH + hi * 5 * TJ + row;
         os = TJ;
         valid = (j0 + row < nj) && (i0 + fo <= ni);
         lin = lin_x(i0 + fo, j0 + row, k);
-      } else {                                // y: F+ of row -1 (face 0), F- of row TJ (face TJ)
+        // x geometry of plane k is staged only for phase B: read these two faces directly
+        const double* fn =
+            b.base + (long long)ffn(0, 0) * fsz + (i0 + fo) + sy * (long long)(j0 + row) + kofs;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = valid ? __ldg(fn + q * fsz) : 0.0;
+      } else {            // y: F+ of row -1 (face j0), F- of row TJ (face j0+TJ)
         const int e = h - 2 * TJ;
         const int col = e % TI, hi = e / TI;
         cx = col;
@@ -406,39 +413,39 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         d = 1;
         sg = hi ? -1.0 : 1.0;
         fo = hi ? TJ : 0;
-        g = sFY + fo * TI + col;
-        gs = NFY;
         out = hi ? sHM + TJ * TI + col : sHP + col;
         os = NHY;
         valid = (i0 + col < ni) && (j0 + fo <= nj);
         lin = lin_y(i0 + col, j0 + fo, k);
+        const double* gy = sFY + fo * TI + col;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = gy[q * NFY];
       }
-      const double* w = pk + K::pidx(cx, cy);
+      const double* wh = pk + K::pidx(cx, cy);
       double q5[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         double qL, qR;
-        vl_recon<LIM, K1>(w[v * PLANE - st], w[v * PLANE], w[v * PLANE + st], c, qL, qR);
+        vl_recon<LIM, K1>(wh[v * PLANE - st], wh[v * PLANE], wh[v * PLANE + st], c, qL, qR);
         q5[v] = sg > 0.0 ? qL : qR;
       }
       double F[5];
-      vl_half(q5, g[0], g[gs], g[2 * gs], g[3 * gs], sg, c, F);
+      vl_half(q5, g[0], g[1], g[2], g[3], sg, c, F);
 #pragma unroll
       for (int v = 0; v < 5; ++v) out[v * os] = F[v];
       if (valid && fmin(q5[0], q5[4]) <= 0.0)
         face_err(d, sg > 0.0 ? ERR_FACE_LEFT : ERR_FACE_RIGHT, lin);
     }
 
-
-    // ---- phase A2: y halves -> shared memory ---------------------------------------
-    const double* const w = pk + s0;
+    // ---- phase A2: y halves -> shared memory -------------------------------------------
     bool ylo_ovw = false, yhi_ovw = false;
+    double lam = 0.0;   // stage 0: y and z parts of lambda of cell k
     {
       double qL[5], qR[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v)
         vl_recon<LIM, K1>(w[v * PLANE - PW], w[v * PLANE], w[v * PLANE + PW], c, qL[v], qR[v]);
-      const double* gl = sFY + ty * TI + tx;    // face j (low); face j+1 at gl + TI
+      const double* gl = sFY + ty * TI + tx;   // face j (low); face j+1 at gl + TI
       double hp[5], hm[5];
       vl_half(qL, gl[TI], gl[NFY + TI], gl[2 * NFY + TI], gl[3 * NFY + TI], 1.0, c, hp);
       vl_half(qR, gl[0], gl[NFY], gl[2 * NFY], gl[3 * NFY], -1.0, c, hm);
@@ -468,76 +475,18 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         sHP[v * NHY + (ty + 1) * TI + tx] = hp[v];
         sHM[v * NHY + ty * TI + tx] = hm[v];
       }
+      if (stage0 && cell_on) {
+        const double snd = fsqrt(c.gamma * w[4 * PLANE] * frcp(w[0]));
+        lam = lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[0], gl[NFY], gl[2 * NFY],
+                       gl[3 * NFY]) +
+              lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[TI], gl[NFY + TI],
+                       gl[2 * NFY + TI], gl[3 * NFY + TI]);
+        if constexpr (NDIM == 3) lam += lamz;
+      }
     }
 
-    // ---- phase A3: x halves of cell (i, j, k); neighbours by shuffle ----------------
-    double R[5];              // residual being assembled (face fluxes already times A)
-    bool xlo_halo = tx == 0, xhi_halo = tx == TI - 1;
-    {
-      double qL[5], qR[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        vl_recon<LIM, K1>(w[v * PLANE - 1], w[v * PLANE], w[v * PLANE + 1], c, qL[v], qR[v]);
-      }
-      const double* gl = sFX + ty * GXW + tx;   // face i (low); face i+1 at gl + 1
-      double hp[5], hm[5];
-      vl_half(qL, gl[1], gl[NFX + 1], gl[2 * NFX + 1], gl[3 * NFX + 1], 1.0, c, hp);
-      vl_half(qR, gl[0], gl[NFX], gl[2 * NFX], gl[3 * NFX], -1.0, c, hm);
-      const double mL = fmin(qL[0], qL[4]), mR = fmin(qR[0], qR[4]);
-      if (fmin(mL, mR) <= 0.0 && in_j) {
-        if (mL <= 0.0 && in_i) face_err(0, ERR_FACE_LEFT, lin_x(i + 1, j, k));
-        if (mR <= 0.0 && i <= ni) face_err(0, ERR_FACE_RIGHT, lin_x(i, j, k));
-      }
-      double fhi[5], flo[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        const double hmn = __shfl_down_sync(FULL, hm[v], 1);
-        const double hpp = __shfl_up_sync(FULL, hp[v], 1);
-        // the tile-edge lanes complete these with the halo halves in phase B
-        fhi[v] = xhi_halo ? hp[v] : hp[v] + hmn;
-        flo[v] = xlo_halo ? hm[v] : hpp + hm[v];
-      }
-      if (in_j && (i == 0 || i == ni - 1)) {
-        if (i == 0) {
-          const int bk = b.bface[0][j + nj * (NDIM == 3 ? k : 0)];
-          if (bk != BFACE_NONE) {
-            overwrite(bk, w, w + 1, w - 1, PLANE, gl, NFX, flo);
-            xlo_halo = false;
-          }
-        }
-        if (i == ni - 1) {
-          const int bk = b.bface[1][j + nj * (NDIM == 3 ? k : 0)];
-          if (bk != BFACE_NONE) {
-            overwrite(bk, w, w - 1, w + 1, PLANE, gl + 1, NFX, fhi);
-            xhi_halo = false;
-          }
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 5; ++v) R[v] = fhi[v] - flo[v];
-    }
-
-    // ---- stage 0: local time step of cell k (solver.py:696-731, dt/V = cfl/lambda) --
-    double dtv = 0.0;
-    if (stage0 && cell_on) {
-      double w0[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) w0[v] = w[v * PLANE];
-      const double snd = fsqrt(c.gamma * w0[4] * frcp(w0[0]));
-      const double* gx = sFX + ty * GXW + tx;
-      const double* gy = sFY + ty * TI + tx;
-      double lam = lam_term(w0[1], w0[2], w0[3], snd, gx[0], gx[NFX], gx[2 * NFX], gx[3 * NFX]) +
-                   lam_term(w0[1], w0[2], w0[3], snd, gx[1], gx[NFX + 1], gx[2 * NFX + 1],
-                            gx[3 * NFX + 1]) +
-                   lam_term(w0[1], w0[2], w0[3], snd, gy[0], gy[NFY], gy[2 * NFY], gy[3 * NFY]) +
-                   lam_term(w0[1], w0[2], w0[3], snd, gy[TI], gy[NFY + TI], gy[2 * NFY + TI],
-                            gy[3 * NFY + TI]);
-      if constexpr (NDIM == 3) lam += lamz;
-      dtv = c.cfl * frcp(lam);
-      b.base[(long long)FDTV * fsz + colofs + kofs] = dtv;
-    }
-
-    // ---- phase A4 (3D): z halves of cell k+1, z flux of face k+1 ---------------------
+    // ---- phase A3 (3D): z halves of cell k+1, z flux of face k+1 ----------------------
+    double R[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // residual (face fluxes already times A)
     if constexpr (NDIM == 3) {
       mbar_wait(bar_of(k + 2), par_of(k + 2));
       if (cell_on) {
@@ -566,7 +515,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         }
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          R[v] += fhi[v] - fzl[v];
+          R[v] = fhi[v] - fzl[v];
           fzl[v] = fhi[v];
           hpz[v] = hp1[v];
         }
@@ -581,14 +530,64 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     __syncthreads();   // AB: y halves and tile-edge halves of plane k complete
     if (tid == 0) {
       fence_async_smem();
-      if (kk + 1 < kc) {
-        if constexpr (NDIM == 3) issue_plane(k + 3);   // into the slot of plane k
-        issue_geo(k + 1);
-      }
-      if (kk + 2 < kc) prefetch_geo(k + 2);
+      if (kk + 1 < kc) issue_geo_yz(k + 1);
+      if (kk + 2 < kc) prefetch_l2(k + 2);
     }
 
-    // ---- phase B: residual, update of cell (i, j, k) ----------------------------------
+    // ---- phase B1: x halves of cell (i, j, k); neighbours by shuffle --------------------
+    mbar_wait(bars + 4, (unsigned)(kk & 1));   // x geometry, Q0 (dt/V) of plane k
+    bool xlo_halo = tx == 0, xhi_halo = tx == TI - 1;
+    {
+      double qL[5], qR[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+        vl_recon<LIM, K1>(w[v * PLANE - 1], w[v * PLANE], w[v * PLANE + 1], c, qL[v], qR[v]);
+      const double* gl = sFX + ty * GXW + tx;   // face i (low); face i+1 at gl + 1
+      double hp[5], hm[5];
+      vl_half(qL, gl[1], gl[NFX + 1], gl[2 * NFX + 1], gl[3 * NFX + 1], 1.0, c, hp);
+      vl_half(qR, gl[0], gl[NFX], gl[2 * NFX], gl[3 * NFX], -1.0, c, hm);
+      const double mL = fmin(qL[0], qL[4]), mR = fmin(qR[0], qR[4]);
+      if (fmin(mL, mR) <= 0.0 && in_j) {
+        if (mL <= 0.0 && in_i) face_err(0, ERR_FACE_LEFT, lin_x(i + 1, j, k));
+        if (mR <= 0.0 && i <= ni) face_err(0, ERR_FACE_RIGHT, lin_x(i, j, k));
+      }
+      double fhi[5], flo[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double hmn = __shfl_down_sync(FULL, hm[v], 1);
+        const double hpp = __shfl_up_sync(FULL, hp[v], 1);
+        // the tile-edge lanes complete these with the tile-edge halves below
+        fhi[v] = xhi_halo ? hp[v] : hp[v] + hmn;
+        flo[v] = xlo_halo ? hm[v] : hpp + hm[v];
+      }
+      if (in_j && (i == 0 || i == ni - 1)) {
+        if (i == 0) {
+          const int bk = b.bface[0][j + nj * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, w, w + 1, w - 1, PLANE, gl, NFX, flo);
+            xlo_halo = false;
+          }
+        }
+        if (i == ni - 1) {
+          const int bk = b.bface[1][j + nj * (NDIM == 3 ? k : 0)];
+          if (bk != BFACE_NONE) {
+            overwrite(bk, w, w - 1, w + 1, PLANE, gl + 1, NFX, fhi);
+            xhi_halo = false;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) R[v] += fhi[v] - flo[v];
+      if (stage0 && cell_on) {
+        const double snd = fsqrt(c.gamma * w[4 * PLANE] * frcp(w[0]));
+        lam += lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[0], gl[NFX], gl[2 * NFX],
+                        gl[3 * NFX]) +
+               lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[1], gl[NFX + 1],
+                        gl[2 * NFX + 1], gl[3 * NFX + 1]);
+      }
+    }
+
+    // ---- phase B2: residual, update of cell (i, j, k) -----------------------------------
     if (cell_on) {
       const int hi = (ty + 1) * TI + tx, lo = ty * TI + tx;
 #pragma unroll
@@ -607,10 +606,12 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
 #pragma unroll
         for (int v = 0; v < 5; ++v) R[v] = R[v] - b.base[(long long)(FSRC + v) * fsz + co];
       }
-      mbar_wait(bars + 4, (unsigned)(kk & 1));
+      double dtv;
       if (stage0) {
 #pragma unroll
         for (int v = 0; v < 5; ++v) rsum[v] = fma(R[v], R[v], rsum[v]);
+        dtv = c.cfl * frcp(lam);
+        b.base[(long long)FDTV * fsz + co] = dtv;
       } else {
         dtv = sQ[5 * NT + tid];
       }
