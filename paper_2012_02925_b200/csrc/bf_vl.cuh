@@ -67,6 +67,13 @@ BF_DEV double vl_limiter(double a, double b) {
 template <int LIM, bool K1>
 BF_DEV void vl_recon(double wm, double w0, double wp, const Consts& c, double& qL, double& qR) {
   const double dm = w0 - wm, dp = wp - w0;
+  if constexpr (K1 && LIM == LIM_VAN_ALBADA) {
+    // (eps/4)(1-k) Psi = Psi/2 = (ab + 1e-12/2) / (a^2 + b^2 + 1e-12), a = D+, b = D-
+    const double t = fmax(fdiv1(fma(dp, dm, 0.5e-12), fma(dp, dp, fma(dm, dm, 1e-12))), 0.0);
+    qL = fma(t, dm, w0);
+    qR = fma(-t, dp, w0);
+    return;
+  }
   const double pp = vl_limiter<LIM>(dp, dm);
   const double pm = (psi_count<LIM>() == 2) ? vl_limiter<LIM>(dm, dp) : pp;
   if constexpr (K1) {
@@ -81,20 +88,22 @@ BF_DEV void vl_recon(double wm, double w0, double wp, const Consts& c, double& q
 // One side of the Van Leer splitting (physics.py:267-290) times the face area.
 BF_DEV void vl_half(const double q[5], double nx, double ny, double nz, double A, double sign,
                     const Consts& c, double F[5]) {
-  const double rinv = frcp(q[0]);
-  const double a2 = c.gamma * q[4] * rinv;
-  const double ainv = frsqrt(a2);
-  const double a = a2 * ainv;
+  // a = sqrt(g p / rho) and 1/a from one reciprocal square root of g p rho
+  const double gp = c.gamma * q[4];
+  const double y = frsqrt(gp * q[0]);
+  const double a = gp * y;
+  const double ainv = q[0] * y;
   const double vn = fma(q[1], nx, fma(q[2], ny, q[3] * nz));
   const double mn = vn * ainv;
-  const double ke = 0.5 * fma(q[1], q[1], fma(q[2], q[2], q[3] * q[3]));
   if (fabs(mn) < 1.0) {
     const double sh = mn + sign;
-    const double fm = ((0.25 * sign) * q[0]) * (a * A) * (sh * sh);
+    const double fm = q[0] * (a * ((0.25 * sign) * A)) * (sh * sh);
     const double ta = (2.0 * sign) * a;
     const double et = fma(c.gm1, vn, ta);
     const double fac = (ta - vn) * c.inv_gamma;
-    const double ee = fma(et * et, c.inv_vlc, fma(-0.5 * vn, vn, ke));
+    // e = et^2 / (2 (g^2-1)) + ke - vn^2 / 2
+    const double s2 = fma(q[1], q[1], fma(q[2], q[2], fma(q[3], q[3], -vn * vn)));
+    const double ee = fma(et * et, c.inv_vlc, 0.5 * s2);
     F[0] = fm;
     F[1] = fm * fma(nx, fac, q[1]);
     F[2] = fm * fma(ny, fac, q[2]);
@@ -107,7 +116,8 @@ BF_DEV void vl_half(const double q[5], double nx, double ny, double nz, double A
     F[1] = fma(m, q[1], nx * pA);
     F[2] = fma(m, q[2], ny * pA);
     F[3] = fma(m, q[3], nz * pA);
-    F[4] = m * fma(c.gog1 * q[4], rinv, ke);
+    const double ke = 0.5 * fma(q[1], q[1], fma(q[2], q[2], q[3] * q[3]));
+    F[4] = m * fma(c.gog1 * q[4], frcp(q[0]), ke);
   } else {
     F[0] = F[1] = F[2] = F[3] = F[4] = 0.0;
   }
