@@ -381,21 +381,33 @@ def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist,
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    marks = {}
+
+    def mark(name):
+        torch.cuda.synchronize()
+        marks[name] = time.perf_counter()
+
+    mark("start")
+    t0 = marks["start"]
     # device registration: geometry host->device, tables, buffers
     gpu = stepper.GpuContext(plan, children, gas, cfg, fs, device=device, rank=rank,
                              nranks=world, precision=args.precision, setups=setups)
     if uid is not None:
         gpu._check(gpu.L.bf_nccl_init(gpu.ctx, uid))
     gpu.finalize()
+    mark("context")
     for cid, (f6, q5) in host.items():
         gpu.upload(cid, f6, q5)
+    mark("upload")
     st = stepper.GpuRankStepper(gpu, cfg)
     for k in range(args.steps):
         st.step(k + 1)       # each step ends with the D2H of its residual norms
+    mark("steps")
     out = {cid: [gpu.download(cid, n) for n in FIELD_NAMES] for cid in host}
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    mark("download")
+    dt = marks["download"] - t0
+    names = list(marks)
+    phases = {n: marks[n] - marks[p] for p, n in zip(names, names[1:])}
     if dist:
         t = torch.tensor([dt], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -408,6 +420,7 @@ def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist,
             "h2d_bytes_per_step": h2d / args.steps,
             "d2h_bytes_per_step": d2h / args.steps + 48,
             "seconds": dt,
+            "phases_s": phases,
             "note": "context creation with geometry host->device, upload of the initial padded "
                     "state (6 fields + 5 conserved), K RK steps each returning its residual "
                     "norms to the host, download of the 6 final padded fields; host-side "

@@ -140,9 +140,15 @@ struct GhostTask {
   const double* dirichlet;   // GK_BC mms: [layer][6][tn0*tn1]
 };
 
+// Ghost launches are block-aligned: CUDA block b covers items
+// [block_map[b].y, +GHOST_BLOCK) of task block_map[b].x (one task per block).
+constexpr int GHOST_BLOCK = 128;
+
 struct GhostArgs {
   const DevBlock* blocks;
   const GhostTask* tasks;
+  const int2* block_map;
+  int nlaunch;          // CUDA blocks in the launch
   int ntasks;
   int cur;              // W buffer being filled
   int t_derived;        // interior T is p/(rho R) (after the first update)

@@ -160,17 +160,21 @@ BF_DEV double interior_T(const double* W, long long fsz, long long o, int t_deri
   return t_derived ? W[4 * fsz + o] / (W[o] * c.R) : W[5 * fsz + o];
 }
 
-__global__ void __launch_bounds__(256) ghost_kernel(const GhostArgs a) {
-  const long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= a.total_items) return;
-  int lo = 0, hi = a.ntasks - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.tasks[mid].begin <= item) lo = mid;
-    else hi = mid - 1;
+__global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
+  // one task per CUDA block: the task record is staged in shared memory once
+  __shared__ __align__(16) GhostTask ts;
+  const int2 bm = a.block_map[blockIdx.x];
+  {
+    static_assert(sizeof(GhostTask) % 8 == 0, "GhostTask words");
+    constexpr int NW = (int)(sizeof(GhostTask) / 8);
+    const unsigned long long* src =
+        reinterpret_cast<const unsigned long long*>(a.tasks + bm.x);
+    for (int w = threadIdx.x; w < NW; w += blockDim.x)
+      reinterpret_cast<unsigned long long*>(&ts)[w] = src[w];
   }
-  const GhostTask& t = a.tasks[lo];
-  const long long m = item - t.begin;
+  __syncthreads();
+  const GhostTask& t = ts;
+  const long long m = (long long)bm.y + threadIdx.x;
   if (m >= t.items) return;
   const Consts& c = a.c;
 
@@ -397,9 +401,8 @@ int stage_tile_rows(int ndim, int lim) {
 }
 
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s) {
-  if (a.total_items == 0) return cudaSuccess;
-  const long long nb = (a.total_items + 255) / 256;
-  ghost_kernel<<<(unsigned)nb, 256, 0, s>>>(a);
+  if (a.total_items == 0 || a.nlaunch == 0) return cudaSuccess;
+  ghost_kernel<<<(unsigned)a.nlaunch, GHOST_BLOCK, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -241,6 +241,9 @@ struct bf_ctx {
   int n_fill = 0;
   long long items_fill = 0;
   GhostTask* d_tasks_unpack = nullptr;
+  int2* d_map_fill = nullptr;      // ghost launch block -> (task, first item)
+  int2* d_map_unpack = nullptr;
+  int nmap_fill = 0, nmap_unpack = 0;
   int n_unpack = 0;
   long long items_unpack = 0;
   std::vector<GhostTask> h_tasks_fill, h_tasks_unpack;
@@ -605,6 +608,21 @@ int build_tables(bf_ctx* ctx) {
   ctx->items_unpack = acc;
   ctx->n_fill = (int)fill.size();
   ctx->n_unpack = (int)unp.size();
+  auto block_map = [&](const std::vector<GhostTask>& ts, int2** dst, int* n) -> int {
+    std::vector<int2> m;
+    for (size_t ti = 0; ti < ts.size(); ++ti)
+      for (long long it = 0; it < ts[ti].items; it += GHOST_BLOCK)
+        m.push_back(make_int2((int)ti, (int)it));
+    *n = (int)m.size();
+    if (m.empty()) return BF_OK;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, m.size() * sizeof(int2)));
+    CK(cudaMemcpy(p, m.data(), m.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    *dst = static_cast<int2*>(p);
+    return BF_OK;
+  };
+  if (int rc = block_map(fill, &ctx->d_map_fill, &ctx->nmap_fill)) return rc;
+  if (int rc = block_map(unp, &ctx->d_map_unpack, &ctx->nmap_unpack)) return rc;
   if (!fill.empty()) {
     void* p = nullptr;
     CK(cudaMalloc(&p, fill.size() * sizeof(GhostTask)));
@@ -707,6 +725,8 @@ GhostArgs ghost_args(bf_ctx* ctx, bool unpack) {
   GhostArgs g{};
   g.blocks = ctx->d_blocks;
   g.tasks = unpack ? ctx->d_tasks_unpack : ctx->d_tasks_fill;
+  g.block_map = unpack ? ctx->d_map_unpack : ctx->d_map_fill;
+  g.nlaunch = unpack ? ctx->nmap_unpack : ctx->nmap_fill;
   g.ntasks = unpack ? ctx->n_unpack : ctx->n_fill;
   g.total_items = unpack ? ctx->items_unpack : ctx->items_fill;
   g.cur = ctx->cur;
@@ -980,6 +1000,8 @@ void bf_destroy(bf_ctx* ctx) {
   cudaFree(ctx->d_tile_begin);
   cudaFree(ctx->d_tasks_fill);
   cudaFree(ctx->d_tasks_unpack);
+  cudaFree(ctx->d_map_fill);
+  cudaFree(ctx->d_map_unpack);
   cudaFree(ctx->d_partial);
   cudaFree(ctx->d_blocksum);
   cudaFree(ctx->d_err);
