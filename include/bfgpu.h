@@ -31,6 +31,7 @@ extern "C" {
 #define BF_ECUDA 2           /* CUDA runtime failure                                    */
 #define BF_ENONPHYSICAL 3    /* NonPhysicalStateError: see bf_error_info()              */
 #define BF_ENCCL 4           /* NCCL failure                                            */
+#define BF_EMETRIC 5         /* MetricError: inverted cell (mesh.py compute_metrics)     */
 
 /* solver.py:31-32 */
 #define BF_FLUX_ROE 0
@@ -60,6 +61,9 @@ extern "C" {
 #define BF_FIELD_Q0 6        /* Q0..Q4 = 6..10: conserved variables */
 #define BF_FIELD_DTV 11      /* dt / V of the last step, interior only */
 #define BF_FIELD_PSI 12      /* limiter arrays: 12 + 10*d + 5*minus + var */
+#define BF_FIELD_VOL 50      /* cell volumes, interior only (Fortran dims) */
+#define BF_FIELD_FACE 51     /* face geometry: 51 + 4*d + (nx, ny, nz, A), faces 0..N_d along d,
+                                interior tangential (solver.py:212-220 _nhat / _area) */
 
 /* arithmetic modes */
 #define BF_PRECISION_EXACT 0 /* reference evaluation order, no FMA contraction: bitwise  */
@@ -116,6 +120,16 @@ int bf_api_version(void);
 int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
                  const double* const* face_vectors, const double* volume,
                  const double* const* source);
+
+/* Same, from the block's padded node coordinates (Block.nodes, mesh.py:44-119):
+   nodes[c], c < ndim, Fortran arrays of shape (P0+1, P1+1[, P2+1]) with
+   P = dims + 2*ghost.  Face geometry and volumes are computed on the device
+   with compute_metrics' operation order (mesh.py:250-331), bitwise equal to
+   the host metrics; an inverted interior cell returns BF_EMETRIC with the
+   reference's MetricError text.  Moves ndim/9 of bf_add_block's geometry
+   bytes (one node triple per cell instead of nine face-vector components). */
+int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
+                       const double* const* nodes, const double* const* source);
 
 /* One physical patch (solver.py:281-403, 526-580).  box[6] = (i0,i1,j0,j1,k0,k1)
    in the block's interior cell indices (BoundarySpec.box).  dirichlet: for

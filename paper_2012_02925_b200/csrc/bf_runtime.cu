@@ -149,6 +149,133 @@ __global__ void face_normals_kernel(double* nx_slot, long long fsz, long long sy
   }
 }
 
+// ---- device metrics (geometry.py / mesh.py:250-331), reference operation order ----------
+// Nodes: 3 padded component arrays (Fortran, (P0+1) x (P1+1) [x (P2+1)]).  Explicit
+// _rn intrinsics keep numpy's rounding (no contraction), so the face geometry and the
+// volumes are bitwise those of compute_metrics on the host.
+struct V3 {
+  double x, y, z;
+};
+__device__ __forceinline__ V3 v_sub(V3 a, V3 b) {
+  return {__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y), __dsub_rn(a.z, b.z)};
+}
+__device__ __forceinline__ V3 v_cross(V3 a, V3 b) {   // numpy.cross component order
+  return {__dsub_rn(__dmul_rn(a.y, b.z), __dmul_rn(a.z, b.y)),
+          __dsub_rn(__dmul_rn(a.z, b.x), __dmul_rn(a.x, b.z)),
+          __dsub_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))};
+}
+__device__ __forceinline__ V3 v_scale(double s, V3 a) {
+  return {__dmul_rn(s, a.x), __dmul_rn(s, a.y), __dmul_rn(s, a.z)};
+}
+__device__ __forceinline__ double v_sum3_mul(V3 g, V3 t) {   // (g0 t0 + g1 t1) + g2 t2
+  return __dadd_rn(__dadd_rn(__dmul_rn(g.x, t.x), __dmul_rn(g.y, t.y)), __dmul_rn(g.z, t.z));
+}
+struct NodeView {
+  const double* x;
+  const double* y;
+  const double* z;   // null in 2D
+  long long s1, s2;  // node strides along j, k
+  __device__ V3 at(long long a, long long b, long long c) const {
+    const long long o = a + s1 * b + s2 * c;
+    return {x[o], y[o], z ? z[o] : 0.0};
+  }
+};
+// Corner orderings per face direction, normals toward +axis (mesh.py:294-298)
+__constant__ int kFaceCorners[3][4][3] = {
+    {{0, 0, 0}, {0, 1, 0}, {0, 1, 1}, {0, 0, 1}},
+    {{0, 0, 0}, {0, 0, 1}, {1, 0, 1}, {1, 0, 0}},
+    {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}}};
+
+// Faces f = 0..N_d of direction d over the interior tangential range: face vector,
+// then unit normal and area (solver.py:212-220) into the 4 geometry slots.
+__global__ void metrics_faces_kernel(double* nx_slot, long long fsz, long long sy, long long sz,
+                                     long long origin, NodeView nv, int ndim, int d, int e0,
+                                     int e1, int e2, int g, int gk) {
+  const long long n = (long long)e0 * e1 * e2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % e0);
+    const long long r = t / e0;
+    const int j = (int)(r % e1), k = (int)(r / e1);
+    const int ni = i + g, nj = j + g, nk = k + gk;   // node of the face's (0,0,0) corner
+    V3 s;
+    if (ndim == 3) {
+      V3 c[4];
+      for (int q = 0; q < 4; ++q)
+        c[q] = nv.at(ni + kFaceCorners[d][q][0], nj + kFaceCorners[d][q][1],
+                     nk + kFaceCorners[d][q][2]);
+      s = v_scale(0.5, v_cross(v_sub(c[2], c[0]), v_sub(c[3], c[1])));
+    } else if (d == 0) {   // fv_i = (dy, -dx, 0) along the j edge
+      const V3 a = nv.at(ni, nj, 0), b = nv.at(ni, nj + 1, 0);
+      s = {__dsub_rn(b.y, a.y), -__dsub_rn(b.x, a.x), 0.0};
+    } else {               // fv_j = (-dy, dx, 0) along the i edge
+      const V3 a = nv.at(ni, nj, 0), b = nv.at(ni + 1, nj, 0);
+      s = {-__dsub_rn(b.y, a.y), __dsub_rn(b.x, a.x), 0.0};
+    }
+    const double A =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(s.x, s.x), __dmul_rn(s.y, s.y)), __dmul_rn(s.z, s.z)));
+    const long long o = origin + i + sy * j + sz * k;
+    nx_slot[o] = A > 0.0 ? __ddiv_rn(s.x, A) : 0.0;
+    nx_slot[fsz + o] = A > 0.0 ? __ddiv_rn(s.y, A) : 0.0;
+    nx_slot[2 * fsz + o] = A > 0.0 ? __ddiv_rn(s.z, A) : 0.0;
+    nx_slot[3 * fsz + o] = A;
+  }
+}
+
+// mesh.py:287-331: (sum3(g1 t1) + sum3(g2 t2)) / 3 over the two triangles of a quad
+__device__ double tri_flux(V3 c0, V3 c1, V3 c2, V3 c3) {
+  const double third = 3.0;
+  const V3 t1 = v_scale(0.5, v_cross(v_sub(c1, c0), v_sub(c2, c0)));
+  const V3 t2 = v_scale(0.5, v_cross(v_sub(c2, c0), v_sub(c3, c0)));
+  const V3 g1 = {__ddiv_rn(__dadd_rn(__dadd_rn(c0.x, c1.x), c2.x), third),
+                 __ddiv_rn(__dadd_rn(__dadd_rn(c0.y, c1.y), c2.y), third),
+                 __ddiv_rn(__dadd_rn(__dadd_rn(c0.z, c1.z), c2.z), third)};
+  const V3 g2 = {__ddiv_rn(__dadd_rn(__dadd_rn(c0.x, c2.x), c3.x), third),
+                 __ddiv_rn(__dadd_rn(__dadd_rn(c0.y, c2.y), c3.y), third),
+                 __ddiv_rn(__dadd_rn(__dadd_rn(c0.z, c2.z), c3.z), third)};
+  return __ddiv_rn(__dadd_rn(v_sum3_mul(g1, t1), v_sum3_mul(g2, t2)), third);
+}
+
+// Interior cell volumes into the V slot; the first inverted cell (C order over the
+// interior, np.argwhere) goes to *bad as (i*nj + j)*nk + k.
+__global__ void metrics_volume_kernel(double* vol, long long sy, long long sz, NodeView nv, int ndim,
+                                      int e0, int e1, int e2, int g, int gk,
+                                      unsigned long long* bad) {
+  const long long n = (long long)e0 * e1 * e2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % e0);
+    const long long r = t / e0;
+    const int j = (int)(r % e1), k = (int)(r / e1);
+    const int a = i + g, b = j + g, c = k + gk;
+    double v;
+    if (ndim == 3) {
+      v = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        V3 lo[4], hi[4];
+        for (int q = 0; q < 4; ++q) {
+          const int* o = kFaceCorners[d][q];
+          lo[q] = nv.at(a + o[0], b + o[1], c + o[2]);
+          hi[q] = nv.at(a + o[0] + (d == 0), b + o[1] + (d == 1), c + o[2] + (d == 2));
+        }
+        const double part = __dsub_rn(tri_flux(hi[0], hi[1], hi[2], hi[3]),
+                                      tri_flux(lo[0], lo[1], lo[2], lo[3]));
+        v = d == 0 ? part : __dadd_rn(v, part);
+      }
+    } else {   // shoelace, mesh.py:250-284
+      const V3 pa = nv.at(a, b, 0), pb = nv.at(a + 1, b, 0), pc = nv.at(a + 1, b + 1, 0),
+               pd = nv.at(a, b + 1, 0);
+      const double t1 = __dsub_rn(__dmul_rn(pa.x, pb.y), __dmul_rn(pb.x, pa.y));
+      const double t2 = __dsub_rn(__dmul_rn(pb.x, pc.y), __dmul_rn(pc.x, pb.y));
+      const double t3 = __dsub_rn(__dmul_rn(pc.x, pd.y), __dmul_rn(pd.x, pc.y));
+      const double t4 = __dsub_rn(__dmul_rn(pd.x, pa.y), __dmul_rn(pa.x, pd.y));
+      v = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dadd_rn(t1, t2), t3), t4));
+    }
+    vol[i + sy * j + sz * k] = v;
+    if (v <= 0.0) atomicMin(bad, ((unsigned long long)i * e1 + j) * (unsigned long long)e2 + k);
+  }
+}
+
 int grid_for(long long n) { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
 
 // One padded field as the reference holds it: interior from the current W
@@ -1024,9 +1151,10 @@ int bf_last_error(const bf_ctx* ctx, char* buf, size_t n) {
   return BF_OK;
 }
 
-int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
-                 const double* const* face_vectors, const double* volume,
-                 const double* const* source) {
+// Arena allocation and device-block record shared by bf_add_block and
+// bf_add_block_nodes (layout: bf_internal.h).
+int add_block_arena(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth, bool has_src,
+                    HostBlock& hb) {
   if (!ctx) return BF_EINVAL;
   if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_add_block after bf_finalize");
   if (ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "duplicate block %d", block_id);
@@ -1035,7 +1163,6 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || (ndim == 2 && dims[2] != 1))
     return fail(ctx, BF_EINVAL, "bad dims (%d,%d,%d)", dims[0], dims[1], dims[2]);
   CK(cudaSetDevice(ctx->device));
-  HostBlock hb;
   hb.id = block_id;
   for (int a = 0; a < 3; ++a) hb.n[a] = dims[a];
   hb.g = ghost_depth;
@@ -1047,7 +1174,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   hb.sz = hb.sy * hb.P[1];
   hb.fsz = ((hb.sz * hb.P[2] + 63) / 64) * 64;
   hb.origin = hb.lead + hb.g + hb.sy * hb.g + hb.sz * hb.gk;
-  hb.has_src = source != nullptr;
+  hb.has_src = has_src;
   const bool want_psi = ctx->sch.limiter_freeze_at > 0;
   // arena slots (bf_internal.h): W 2x6 | Q 5 | dt/V | V | face geometry 3x4 |
   // [S*V 5] | [limiters ndim x 2 x 5]
@@ -1073,7 +1200,18 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   d.oz = hb.gk;
   hb.nslots = nfield;
   ctx->have_psi = want_psi;
+  return BF_OK;
+}
 
+int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
+                 const double* const* face_vectors, const double* volume,
+                 const double* const* source) {
+  HostBlock hb;
+  int rc0 = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
+  if (rc0) return rc0;
+  const int ndim = ctx->ndim;
+  const int gg[3] = {hb.g, hb.g, hb.gk};
+  DevBlock& d = hb.dev;
   // face unit normals and areas (solver.py:212-220): the reference's face-vector
   // arrays go to the device as they are; a kernel normalises and scatters them.
   cudaStream_t st = ctx->stream;
@@ -1118,6 +1256,72 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
       if (rc) return rc;
     }
   CK(cudaStreamSynchronize(st));
+  d.order = (int)ctx->blocks.size();
+  ctx->index_of[block_id] = (int)ctx->blocks.size();
+  ctx->blocks.push_back(std::move(hb));
+  return BF_OK;
+}
+
+int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
+                       const double* const* nodes, const double* const* source) {
+  HostBlock hb;
+  int rc = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
+  if (rc) return rc;
+  const int ndim = ctx->ndim;
+  DevBlock& d = hb.dev;
+  cudaStream_t st = ctx->stream;
+  // padded node arrays (P0+1) x (P1+1) [x (P2+1)], Fortran order
+  const long long N0 = hb.P[0] + 1, N1 = hb.P[1] + 1, N2 = ndim == 3 ? hb.P[2] + 1 : 1;
+  const long long nn = N0 * N1 * N2;
+  double* dn = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&dn), sizeof(double) * ndim * nn, st));
+  for (int c = 0; c < ndim; ++c)
+    CK(cudaMemcpyAsync(dn + c * nn, nodes[c], sizeof(double) * nn, cudaMemcpyHostToDevice, st));
+  ctx->bytes_h2d += (long long)sizeof(double) * ndim * nn;
+  NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, N0, N0 * N1};
+  for (int dd = 0; dd < ndim; ++dd) {
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+    const long long nout = (long long)ext[0] * ext[1] * ext[2];
+    metrics_faces_kernel<<<grid_for(nout), 256, 0, st>>>(d.f(ffn(dd, 0)) - hb.origin, hb.fsz,
+                                                          hb.sy, hb.sz, hb.origin, nv, ndim, dd,
+                                                          ext[0], ext[1], ext[2], hb.g, hb.gk);
+    CK(cudaGetLastError());
+  }
+  unsigned long long* bad = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  const long long ncell = (long long)hb.n[0] * hb.n[1] * hb.n[2];
+  metrics_volume_kernel<<<grid_for(ncell), 256, 0, st>>>(d.f(FVOL), hb.sy, hb.sz, nv, ndim,
+                                                         hb.n[0], hb.n[1], hb.n[2], hb.g, hb.gk,
+                                                         bad);
+  CK(cudaGetLastError());
+  unsigned long long hbad = ~0ull;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(bad, st));
+  CK(cudaFreeAsync(dn, st));
+  if (hb.has_src) {
+    const long long n = ncell;
+    double* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * n, st));
+    for (int e = 0; e < 5; ++e) {
+      CK(cudaMemcpyAsync(tmp, source[e], sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      scatter_box_kernel<<<grid_for(n), 256, 0, st>>>(d.f(FSRC + e), hb.sy, hb.sz, 0, 0, 0, tmp,
+                                                      hb.n[0], hb.n[1], hb.n[2]);
+      CK(cudaGetLastError());
+      ctx->bytes_h2d += (long long)sizeof(double) * n;
+    }
+    CK(cudaFreeAsync(tmp, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (hbad != ~0ull) {
+    for (void* p : hb.owned) cudaFree(p);
+    const unsigned long long k = hbad % (unsigned long long)hb.n[2];
+    const unsigned long long r = hbad / (unsigned long long)hb.n[2];
+    const unsigned long long j = r % (unsigned long long)hb.n[1], i = r / (unsigned long long)hb.n[1];
+    return fail(ctx, BF_EMETRIC, "block %d: inverted cell at interior index (%llu, %llu, %llu)",
+                block_id, i, j, k);
+  }
   d.order = (int)ctx->blocks.size();
   ctx->index_of[block_id] = (int)ctx->blocks.size();
   ctx->blocks.push_back(std::move(hb));
@@ -1368,6 +1572,28 @@ int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
         for (long long i = 0; i < hb.n[0]; ++i)
           out[i + hb.n[0] * (j + (long long)hb.n[1] * k)] =
               a[hb.origin + hb.off((int)i, (int)j, (int)k)];
+    return BF_OK;
+  }
+  if (what == BF_FIELD_VOL) {
+    rc = get(hb.dev.f(FVOL), a);
+    if (rc) return rc;
+    for (long long k = 0; k < hb.n[2]; ++k)
+      for (long long j = 0; j < hb.n[1]; ++j)
+        for (long long i = 0; i < hb.n[0]; ++i)
+          out[i + hb.n[0] * (j + (long long)hb.n[1] * k)] =
+              a[hb.origin + hb.off((int)i, (int)j, (int)k)];
+    return BF_OK;
+  }
+  if (what >= BF_FIELD_FACE && what < BF_FIELD_FACE + 4 * ctx->ndim) {
+    const int d = (what - BF_FIELD_FACE) / 4, cc = (what - BF_FIELD_FACE) % 4;
+    rc = get(hb.dev.f(ffn(d, cc)), a);
+    if (rc) return rc;
+    long long ext[3] = {hb.n[0], hb.n[1], hb.n[2]};
+    ext[d] += 1;
+    for (long long k = 0; k < ext[2]; ++k)
+      for (long long j = 0; j < ext[1]; ++j)
+        for (long long i = 0; i < ext[0]; ++i)
+          out[i + ext[0] * (j + ext[1] * k)] = a[hb.origin + hb.off((int)i, (int)j, (int)k)];
     return BF_OK;
   }
   if (what >= BF_FIELD_PSI && what < BF_FIELD_PSI + 10 * ctx->ndim) {

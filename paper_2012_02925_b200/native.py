@@ -16,7 +16,7 @@ from .errors import NativeLibraryError
 LIB_PATH = Path(__file__).resolve().parent / "libbfgpu.so"
 HEADER = Path(__file__).resolve().parent.parent / "include" / "bfgpu.h"
 
-BF_OK, BF_EINVAL, BF_ECUDA, BF_ENONPHYSICAL, BF_ENCCL = 0, 1, 2, 3, 4
+BF_OK, BF_EINVAL, BF_ECUDA, BF_ENONPHYSICAL, BF_ENCCL, BF_EMETRIC = 0, 1, 2, 3, 4, 5
 FLUX = {"roe": 0, "van_leer": 1}
 LIMITER = {"none": 0, "van_leer": 1, "van_albada": 2, "minmod": 3}
 BC = {"supersonic_inflow": 0, "supersonic_outflow": 1, "slip_wall": 2, "noslip_wall": 3,
@@ -24,6 +24,7 @@ BC = {"supersonic_inflow": 0, "supersonic_outflow": 1, "slip_wall": 2, "noslip_w
 FACES = ("i_min", "i_max", "j_min", "j_max", "k_min", "k_max")
 FIELD = {"rho": 0, "u": 1, "v": 2, "w": 3, "p": 4, "T": 5, "dtv": 11}
 FIELD_Q0, FIELD_PSI = 6, 12
+FIELD_VOL, FIELD_FACE = 50, 51
 ERR_FACE_LEFT, ERR_FACE_RIGHT, ERR_ROE_A2, ERR_UPDATE = 1, 2, 3, 4
 PRECISION = {"exact": 0, "fast": 1}
 
@@ -57,6 +58,7 @@ PROTOTYPES = {
     "bf_destroy": (None, [_P]),
     "bf_last_error": (_I, [_P, C.c_char_p, C.c_size_t]),
     "bf_add_block": (_I, [_P, _I, _PI, _I, _PPD, _PD, _PPD]),
+    "bf_add_block_nodes": (_I, [_P, _I, _PI, _I, _PPD, _PPD]),
     "bf_add_bc_patch": (_I, [_P, _I, _I, _I, _PI, _PD]),
     "bf_add_link": (_I, [_P, _I, _I, _PI, _PI, _I, _I, _PI, _I, _I]),
     "bf_finalize": (_I, [_P]),

@@ -26,8 +26,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import native
-from .errors import (ConfigError, DivergenceError, NativeLibraryError, NonPhysicalStateError,
-                     bridged)
+from .errors import (ConfigError, DivergenceError, MetricError, NativeLibraryError,
+                     NonPhysicalStateError, bridged)
 from .model import FIELD_NAMES, PRIM_NAMES, RK_COEFFS, validate_scheme
 
 _SUPPORTED_BC = tuple(native.BC)
@@ -72,10 +72,13 @@ class _BlockSetup:
         self.cid = cid
         self.block = plan.child_block(cid)
         self.specs = sorted(plan.boundaries[cid], key=lambda s: s.canonical_key())
-        self.metrics = (metrics_fn or geometry.compute_metrics)(self.block)
+        self._metrics_fn = metrics_fn or geometry.compute_metrics
+        self._metrics = None
+        # host metrics are only needed for a custom metrics_fn and for MMS
+        # (cell centres); otherwise the device computes them from the nodes
+        self.device_metrics = metrics_fn is None and config.mms_id is None
         self.gas, self.config, self.fs = gas, config, freestream
         self.inner = self.block.interior()
-        self.vol = self.metrics.volume[self.inner]
         self.solution = mms.manufactured_solution(config.mms_id) if config.mms_id else None
         self.source = None
         if config.mms_id is not None:
@@ -83,6 +86,17 @@ class _BlockSetup:
             xs, ys, zs = (c[i][self.inner] for i in range(3))
             self.source = [np.asfortranarray(np.asarray(s) * self.vol)
                            for s in mms.mms_source(xs, ys, zs, config.mms_id, gas)]
+
+    @property
+    def metrics(self):
+        """Host metrics (mesh.py compute_metrics), computed on first use."""
+        if self._metrics is None:
+            self._metrics = self._metrics_fn(self.block)
+        return self._metrics
+
+    @property
+    def vol(self):
+        return self.metrics.volume[self.inner]
 
     def initial_state(self, init):
         """(fields6, q5) padded Fortran arrays (solver.py:258-277)."""
@@ -162,6 +176,14 @@ class GpuContext:
             s = setups[cid] if setups is not None else \
                 _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
             self.setups[cid] = s
+            if s.device_metrics and s.source is None:
+                nodes = [np.asfortranarray(s.block.nodes[c], dtype=float)
+                         for c in range(self.ndim)]
+                self._keep = nodes
+                self._check(self.L.bf_add_block_nodes(self.ctx, cid, native.ints(s.block.dims),
+                                                      s.block.ghost_depth, native.dptrs(nodes),
+                                                      None))
+                continue
             fv = []
             for d in range(self.ndim):
                 for comp in range(3):
@@ -213,6 +235,15 @@ class GpuContext:
         msg = native.last_error(self.ctx)
         if rc == native.BF_EINVAL:
             raise bridged(ConfigError)(msg)
+        if rc == native.BF_EMETRIC:
+            # reformat the index tuple the way the reference prints np.argwhere's row
+            import re
+            m = re.match(r"block (-?\d+): inverted cell at interior index \((\d+), (\d+), (\d+)\)",
+                         msg)
+            if m:
+                bad = np.array([int(m.group(k)) for k in (2, 3, 4)])
+                msg = f"block {int(m.group(1))}: inverted cell at interior index {tuple(bad)}"
+            raise bridged(MetricError)(msg)
         raise NativeLibraryError(f"libbfgpu error {rc}: {msg}")
 
     def error_message(self):
@@ -276,8 +307,13 @@ class GpuContext:
             code = native.FIELD[what]
         else:
             code = int(what)
-        if code == native.FIELD["dtv"]:
+        if code in (native.FIELD["dtv"], native.FIELD_VOL):
             out = np.empty(blk.dims, order="F")
+        elif native.FIELD_FACE <= code < native.FIELD_FACE + 12:
+            d = (code - native.FIELD_FACE) // 4
+            shape = list(blk.dims)
+            shape[d] += 1
+            out = np.empty(shape, order="F")
         elif code >= native.FIELD_PSI:
             r = code - native.FIELD_PSI
             d = r // 10
@@ -355,15 +391,21 @@ class GpuBlockView:
         s = gpu.setups[cid]
         self._gpu, self._cid = gpu, cid
         self.block = s.block
-        self.metrics = s.metrics
         self.gas, self.config, self.freestream = gpu.gas, gpu.config, gpu.fs
         self.specs = s.specs
         self.physical_specs = [x for x in s.specs if x.kind == "physical"]
         self.dirs = (0, 1) if s.block.ndim == 2 else (0, 1, 2)
         self._int = s.inner
-        self._vol = s.vol
         self.frozen = False
         self.invalidate()
+
+    @property
+    def metrics(self):
+        return self._gpu.setups[self._cid].metrics
+
+    @property
+    def _vol(self):
+        return self._gpu.setups[self._cid].vol
 
     def invalidate(self):
         self.fields = _LazyFields(self)
