@@ -122,14 +122,16 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
                  const double* const* source);
 
 /* Same, from the block's padded node coordinates (Block.nodes, mesh.py:44-119):
-   nodes[c], c < ndim, Fortran arrays of shape (P0+1, P1+1[, P2+1]) with
-   P = dims + 2*ghost.  Face geometry and volumes are computed on the device
+   nodes[c], c < ndim, dense arrays of shape (P0+1, P1+1[, P2+1]) with
+   P = dims + 2*ghost, element strides node_strides[0..ndim-1] along i, j, k
+   (the reference's C-ordered Block.nodes[c] is passed as it is).  Face geometry and volumes are computed on the device
    with compute_metrics' operation order (mesh.py:250-331), bitwise equal to
    the host metrics; an inverted interior cell returns BF_EMETRIC with the
    reference's MetricError text.  Moves ndim/9 of bf_add_block's geometry
    bytes (one node triple per cell instead of nine face-vector components). */
 int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
-                       const double* const* nodes, const double* const* source);
+                       const double* const* nodes, const long long node_strides[3],
+                       const double* const* source);
 
 /* One physical patch (solver.py:281-403, 526-580).  box[6] = (i0,i1,j0,j1,k0,k1)
    in the block's interior cell indices (BoundarySpec.box).  dirichlet: for
@@ -148,7 +150,9 @@ int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int
 int bf_finalize(bf_ctx* ctx);
 
 /* Initial state (init_uniform / init_manufactured / sync_conserved,
-   solver.py:258-277): 6 padded primitive fields + 5 padded conserved fields. */
+   solver.py:258-277): 6 padded primitive fields + 5 padded conserved fields;
+   q5 = NULL derives the conserved fields on the device (encode_primitive,
+   reference operation order: bitwise equal to the host conversion).      */
 int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
                      const double* const* q5);
 

@@ -173,10 +173,10 @@ __device__ __forceinline__ double v_sum3_mul(V3 g, V3 t) {   // (g0 t0 + g1 t1) 
 struct NodeView {
   const double* x;
   const double* y;
-  const double* z;   // null in 2D
-  long long s1, s2;  // node strides along j, k
+  const double* z;      // null in 2D
+  long long s0, s1, s2;  // element strides along i, j, k
   __device__ V3 at(long long a, long long b, long long c) const {
-    const long long o = a + s1 * b + s2 * c;
+    const long long o = s0 * a + s1 * b + s2 * c;
     return {x[o], y[o], z ? z[o] : 0.0};
   }
 };
@@ -273,6 +273,23 @@ __global__ void metrics_volume_kernel(double* vol, long long sy, long long sz, N
     }
     vol[i + sy * j + sz * k] = v;
     if (v <= 0.0) atomicMin(bad, ((unsigned long long)i * e1 + j) * (unsigned long long)e2 + k);
+  }
+}
+
+// encode_primitive (physics.py:136-140) over a whole padded arena slot range,
+// reference operation order: rho u, rho v, rho w, p/(g-1) + rho*(0.5*((uu+vv)+ww)).
+__global__ void encode_kernel(double* W, double* Q, long long fsz, long long n, double gm1) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double r = W[t], u = W[fsz + t], v = W[2 * fsz + t], w = W[3 * fsz + t],
+                 p = W[4 * fsz + t];
+    const double ke =
+        __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), __dmul_rn(w, w)));
+    Q[t] = r;
+    Q[fsz + t] = __dmul_rn(r, u);
+    Q[2 * fsz + t] = __dmul_rn(r, v);
+    Q[3 * fsz + t] = __dmul_rn(r, w);
+    Q[4 * fsz + t] = __dadd_rn(__ddiv_rn(p, gm1), __dmul_rn(r, ke));
   }
 }
 
@@ -1263,7 +1280,8 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
 }
 
 int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
-                       const double* const* nodes, const double* const* source) {
+                       const double* const* nodes, const long long node_strides[3],
+                       const double* const* source) {
   HostBlock hb;
   int rc = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
   if (rc) return rc;
@@ -1278,7 +1296,17 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   for (int c = 0; c < ndim; ++c)
     CK(cudaMemcpyAsync(dn + c * nn, nodes[c], sizeof(double) * nn, cudaMemcpyHostToDevice, st));
   ctx->bytes_h2d += (long long)sizeof(double) * ndim * nn;
-  NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, N0, N0 * N1};
+  {   // the strides must describe a dense array (C or Fortran order)
+    const long long st[3] = {node_strides[0], node_strides[1], ndim == 3 ? node_strides[2] : 0};
+    const long long ext[3] = {N0, N1, N2};
+    long long span = 1;
+    for (int a = 0; a < ndim; ++a) span += (ext[a] - 1) * st[a];
+    if (span != nn)
+      return fail(ctx, BF_EINVAL, "node arrays must be dense (strides %lld %lld %lld)", st[0],
+                  st[1], st[2]);
+  }
+  NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, node_strides[0], node_strides[1],
+              ndim == 3 ? node_strides[2] : 0};
   for (int dd = 0; dd < ndim; ++dd) {
     int ext[3];
     for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
@@ -1441,9 +1469,16 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
     CK(cudaMemcpyAsync(hb.dev.f(fw(1, f)) - hb.origin, hb.dev.f(fw(0, f)) - hb.origin,
                        sizeof(double) * hb.fsz, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  for (int e = 0; e < 5; ++e) {
-    int rc = put(hb.dev.f(FQ + e), q5[e]);
-    if (rc) return rc;
+  if (q5) {
+    for (int e = 0; e < 5; ++e) {
+      int rc = put(hb.dev.f(FQ + e), q5[e]);
+      if (rc) return rc;
+    }
+  } else {   // sync_conserved on the device (solver.py:273-277)
+    encode_kernel<<<grid_for(hb.fsz), 256, 0, ctx->stream>>>(
+        hb.dev.f(fw(0, 0)) - hb.origin, hb.dev.f(FQ) - hb.origin, hb.fsz, hb.fsz,
+        ctx->gas.gamma - 1.0);
+    CK(cudaGetLastError());
   }
   CK(cudaFreeAsync(tmp, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

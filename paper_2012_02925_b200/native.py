@@ -58,7 +58,7 @@ PROTOTYPES = {
     "bf_destroy": (None, [_P]),
     "bf_last_error": (_I, [_P, C.c_char_p, C.c_size_t]),
     "bf_add_block": (_I, [_P, _I, _PI, _I, _PPD, _PD, _PPD]),
-    "bf_add_block_nodes": (_I, [_P, _I, _PI, _I, _PPD, _PPD]),
+    "bf_add_block_nodes": (_I, [_P, _I, _PI, _I, _PPD, _PLL, _PPD]),
     "bf_add_bc_patch": (_I, [_P, _I, _I, _I, _PI, _PD]),
     "bf_add_link": (_I, [_P, _I, _I, _PI, _PI, _I, _I, _PI, _I, _I]),
     "bf_finalize": (_I, [_P]),

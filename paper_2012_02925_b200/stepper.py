@@ -177,12 +177,19 @@ class GpuContext:
                 _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
             self.setups[cid] = s
             if s.device_metrics and s.source is None:
-                nodes = [np.asfortranarray(s.block.nodes[c], dtype=float)
-                         for c in range(self.ndim)]
-                self._keep = nodes
-                self._check(self.L.bf_add_block_nodes(self.ctx, cid, native.ints(s.block.dims),
-                                                      s.block.ghost_depth, native.dptrs(nodes),
-                                                      None))
+                nodes = []
+                for c in range(self.ndim):
+                    x = np.asarray(s.block.nodes[c], dtype=float)
+                    if not (x.flags.c_contiguous or x.flags.f_contiguous):
+                        x = np.ascontiguousarray(x)
+                    nodes.append(x)
+                st = [x // 8 for x in nodes[0].strides] + [0] * (3 - self.ndim)
+                if any(n.strides != nodes[0].strides for n in nodes):
+                    nodes = [np.ascontiguousarray(n) for n in nodes]
+                    st = [x // 8 for x in nodes[0].strides] + [0] * (3 - self.ndim)
+                self._check(self.L.bf_add_block_nodes(
+                    self.ctx, cid, native.ints(s.block.dims), s.block.ghost_depth,
+                    native.dptrs(nodes), (C.c_longlong * 3)(*st), None))
                 continue
             fv = []
             for d in range(self.ndim):
@@ -279,18 +286,19 @@ class GpuContext:
                 f = perturbed_state(blk, self.fs, self.gas, rng)
                 if c.id not in mine:
                     continue
-                f6 = [f[n] for n in FIELD_NAMES]
-                q5 = encode_primitive(*(f[n] for n in PRIM_NAMES), self.gas.gamma)
-                self.upload(c.id, f6, q5)
+                self.upload(c.id, [f[n] for n in FIELD_NAMES])   # Q derived on the device
             return
         for cid in self.child_ids:
-            f6, q5 = self.setups[cid].initial_state(init)
-            self.upload(cid, f6, q5)
+            f6, _ = self.setups[cid].initial_state(init)
+            self.upload(cid, f6)
 
-    def upload(self, cid, fields6, q5):
+    def upload(self, cid, fields6, q5=None):
+        """Padded initial fields of a child; q5=None: conserved variables are
+        derived on the device (encode_primitive, bitwise)."""
         f6 = [np.asfortranarray(x, dtype=float) for x in fields6]
-        q = [np.asfortranarray(x, dtype=float) for x in q5]
-        self._check(self.L.bf_upload_fields(self.ctx, cid, native.dptrs(f6), native.dptrs(q)))
+        q = None if q5 is None else [np.asfortranarray(x, dtype=float) for x in q5]
+        self._check(self.L.bf_upload_fields(self.ctx, cid, native.dptrs(f6),
+                                            native.dptrs(q) if q is not None else None))
 
     def update_ghosts(self):
         self._check(self.L.bf_update_ghosts(self.ctx))
@@ -301,27 +309,34 @@ class GpuContext:
         self._check(self.L.bf_step(self.ctx, int(step_index), out, C.byref(n)))
         return np.array(out[:], dtype=float), int(n.value)
 
-    def download(self, cid, what):
+    def download(self, cid, what, out=None):
+        """One array of a child (BF_FIELD_* selector or field name); `out`, when
+        given, is a preallocated Fortran float64 array of the right shape
+        (e.g. in pinned host memory)."""
         blk = self.setups[cid].block
         if isinstance(what, str):
             code = native.FIELD[what]
         else:
             code = int(what)
         if code in (native.FIELD["dtv"], native.FIELD_VOL):
-            out = np.empty(blk.dims, order="F")
+            shape = tuple(blk.dims)
         elif native.FIELD_FACE <= code < native.FIELD_FACE + 12:
             d = (code - native.FIELD_FACE) // 4
             shape = list(blk.dims)
             shape[d] += 1
-            out = np.empty(shape, order="F")
+            shape = tuple(shape)
         elif code >= native.FIELD_PSI:
             r = code - native.FIELD_PSI
             d = r // 10
             shape = list(blk.dims)
             shape[d] += 2
-            out = np.empty(shape, order="F")
+            shape = tuple(shape)
         else:
-            out = np.empty(blk.shape, order="F")
+            shape = blk.shape
+        if out is None:
+            out = np.empty(shape, order="F")
+        elif out.shape != tuple(shape) or out.dtype != np.float64 or not out.flags.f_contiguous:
+            raise ValueError(f"download: out must be a Fortran float64 array of shape {shape}")
         self._check(self.L.bf_download(self.ctx, cid, code, native.dptr(out)))
         return out
 
