@@ -157,6 +157,26 @@ struct GhostArgs {
   Consts c;
 };
 
+// Ghost values pushed by the stage kernel (bf_vl.cuh): when a cell's new
+// state is written, the cells it is the source of in the NEXT stage's ghost
+// layers are written too — connected copies into the partner block's
+// ghosts (halo.py:47-115 with the orientation folded into `coef`), message
+// packing for remote partners, and the interior-dependent physical BCs
+// (solver.py:281-403).  Inflow and MMS ghosts are constant (filled once).
+enum PushKind : int { PK_COPY = 0, PK_PACK = 1, PK_OUTFLOW = 2, PK_SLIP = 3, PK_NOSLIP = 4,
+                      PK_FARFIELD = 5 };
+constexpr int PUSH_MAX_RULES = 12;   // per block (more: ghost kernel instead)
+struct PushRule {
+  int kind;
+  int axis, side;        // the face the rule belongs to
+  int nfields;           // COPY / PACK: 6 (3D) or 5 (2D: rho u v p T)
+  int lo[3], hi[3];      // source cells covered (own interior coords, [lo, hi))
+  long long base;        // COPY / PACK: destination offset of source cell lo
+  long long coef[3];     // destination offset per source coordinate
+  long long dst_fsz;     // COPY: destination slot size; PACK: buffer field stride
+  double* dst;           // COPY: destination block (interior origin); PACK: send buffer
+};
+
 struct StageArgs {
   const DevBlock* blocks;
   const Tile* tiles;
@@ -168,6 +188,10 @@ struct StageArgs {
   double* partial;      // [ntiles][5] sum(R^2) partials (stage 0)
   unsigned long long* err;   // [0] = min error key, [1..] unused
   const unsigned char* tmaps;   // [nblocks][NTMAP] CUtensorMap (128 B each) in global memory
+  const PushRule* push_rules;   // ghost push (bf_vl.cuh), used when push != 0
+  const int* push_range;        // [nblocks][6 faces][begin, end) into push_rules
+  int push;
+  int pad_;
   Consts c;
 };
 

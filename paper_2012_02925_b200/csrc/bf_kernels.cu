@@ -380,11 +380,17 @@ static cudaError_t launch_stage_l(int lim, const StageArgs& a, cudaStream_t s) {
   }
 }
 
+#if !BF_EXACT
+// FAST Van Leer with limiters computed in-kernel runs the cell-split kernel
+// (bf_vl.cuh), which also pushes the next stage's ghosts when a.push is set.
+bool vl_active(int flux, int flags) {
+  return flux == FLUX_VAN_LEER && !(flags & (F_PSI_LOAD | F_PSI_STORE)) && !vl_disabled();
+}
+#endif
+
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s) {
 #if !BF_EXACT
-  // FAST Van Leer with limiters computed in-kernel: cell-split kernel (bf_vl.cuh)
-  if (flux == FLUX_VAN_LEER && !(a.flags & (F_PSI_LOAD | F_PSI_STORE)) && !vl_disabled())
-    return launch_vl(ndim, lim, a, s);
+  if (vl_active(flux, a.flags)) return launch_vl(ndim, lim, a, s);
 #endif
   if (ndim == 3)
     return flux == FLUX_ROE ? launch_stage_l<3, FLUX_ROE>(lim, a, s)

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -33,6 +34,7 @@ int stage_tile_rows(int ndim, int lim);
 }  // namespace bf_exact
 namespace bf_fast {
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
+bool vl_active(int flux, int flags);
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
@@ -385,6 +387,12 @@ struct bf_ctx {
   int n_fill = 0;
   long long items_fill = 0;
   GhostTask* d_tasks_unpack = nullptr;
+  std::vector<PushRule> h_push;
+  PushRule* d_push = nullptr;      // ghost push rules (stage kernel writes next ghosts)
+  int* d_push_range = nullptr;     // [nblocks][6][2]
+  bool push_ok = false;            // push rules built (all blocks >= 2 ghost depths thick)
+  bool pushed = false;             // ghosts of W[cur] were written by the last stage
+  bool other_filled = false;       // constant ghosts (inflow, MMS) present in W[cur ^ 1]
   int2* d_map_fill = nullptr;      // ghost launch block -> (task, first item)
   int2* d_map_unpack = nullptr;
   int nmap_fill = 0, nmap_unpack = 0;
@@ -782,6 +790,144 @@ int build_tables(bf_ctx* ctx) {
   return BF_OK;
 }
 
+// Ghost push rules (PushRule): for every source cell band of a block face,
+// where the stage kernel writes the next stage's ghost values (bf_vl.cuh).
+// Disabled (ghost kernel instead) when a block is thinner than 2 ghost depths.
+// The in-kernel ghost push is measured slower on C4 than the separate ghost
+// launch (stage 1.76 ms vs 1.30 + 0.11 ms: the x-face band cells run it on
+// 2-4 divergent lanes on the critical path of every plane), so it is opt-in:
+// BF_PUSH=1.
+bool push_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BF_PUSH");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int build_push(bf_ctx* ctx) {
+  const int ndim = ctx->ndim;
+  const int nb = (int)ctx->blocks.size();
+  ctx->push_ok = true;
+  for (const HostBlock& hb : ctx->blocks)
+    for (int a = 0; a < ndim; ++a)
+      if (hb.n[a] < 2 * hb.g) ctx->push_ok = false;
+  if (!ctx->push_ok) return BF_OK;
+  std::vector<std::vector<PushRule>> per((size_t)nb * 6);
+  for (const HostPatch& hp : ctx->patches) {
+    int kind;
+    switch (hp.type) {
+      case BC_OUTFLOW: kind = PK_OUTFLOW; break;
+      case BC_SLIP: kind = PK_SLIP; break;
+      case BC_NOSLIP: kind = PK_NOSLIP; break;
+      case BC_FARFIELD: kind = PK_FARFIELD; break;
+      default: continue;   // inflow / MMS Dirichlet ghosts are constant
+    }
+    const int bi = ctx->index_of[hp.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    PushRule r{};
+    r.kind = kind;
+    r.axis = hp.face / 2;
+    r.side = hp.face % 2;
+    for (int a = 0; a < 3; ++a) {
+      r.lo[a] = hp.box[2 * a];
+      r.hi[a] = hp.box[2 * a + 1];
+    }
+    const int ax = r.axis, n = hb.n[ax];
+    const int layers = (kind == PK_SLIP || kind == PK_NOSLIP) ? hb.g : 1;   // source layers
+    r.lo[ax] = r.side == 0 ? 0 : n - layers;
+    r.hi[ax] = r.side == 0 ? layers : n;
+    per[(size_t)bi * 6 + hp.face].push_back(r);
+  }
+  const int nf = ndim == 3 ? 6 : 5;
+  for (auto& L : ctx->links) {
+    const int bi = ctx->index_of[L.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    const int ghost[3] = {hb.g, hb.g, ndim == 3 ? hb.g : 0};
+    int send[6], recv[6];
+    halo_boxes(L.face, L.box, hb.n, ghost, send, recv);
+    const bool local = (L.peer_rank == ctx->rank) && ctx->index_of.count(L.peer_block);
+    PushRule r{};
+    r.nfields = nf;
+    if (!local) {   // own send box -> message buffer, i-fastest over the box
+      r.kind = PK_PACK;
+      r.axis = L.face / 2;
+      r.side = L.face % 2;
+      int sext[3];
+      for (int a = 0; a < 3; ++a) {
+        r.lo[a] = send[2 * a];
+        r.hi[a] = send[2 * a + 1];
+        sext[a] = r.hi[a] - r.lo[a];
+      }
+      r.base = 0;
+      r.coef[0] = 1;
+      r.coef[1] = sext[0];
+      r.coef[2] = (long long)sext[0] * sext[1];
+      r.dst_fsz = L.cells;
+      r.dst = L.send;
+      per[(size_t)bi * 6 + L.face].push_back(r);
+      continue;
+    }
+    // this endpoint receives from the peer block: the rule lives on the peer's face
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = recv[2 * a + 1] - recv[2 * a];
+    int perm[3];
+    bool flip[3];
+    unpack_axes(L.face, L.amap, L.peer_face, perm, flip);
+    const int pi = ctx->index_of[L.peer_block];
+    const HostBlock& pb = ctx->blocks[pi];
+    const int pghost[3] = {pb.g, pb.g, ndim == 3 ? pb.g : 0};
+    int psend[6], precv[6];
+    halo_boxes(L.peer_face, L.peer_box, pb.n, pghost, psend, precv);
+    const long long own_st[3] = {1, hb.sy, hb.sz};
+    r.kind = PK_COPY;
+    r.axis = L.peer_face / 2;
+    r.side = L.peer_face % 2;
+    for (int b = 0; b < 3; ++b) {
+      r.lo[b] = psend[2 * b];
+      r.hi[b] = psend[2 * b + 1];
+    }
+    r.base = hb.off(recv[0], recv[2], recv[4]);
+    for (int a = 0; a < 3; ++a) {
+      if (flip[a]) {
+        r.base += (long long)(ext[a] - 1) * own_st[a];
+        r.coef[perm[a]] = -own_st[a];
+      } else {
+        r.coef[perm[a]] = own_st[a];
+      }
+    }
+    r.dst_fsz = hb.fsz;
+    r.dst = hb.dev.base;
+    per[(size_t)pi * 6 + L.peer_face].push_back(r);
+  }
+  for (int bi = 0; bi < nb; ++bi) {
+    size_t cnt = 0;
+    for (int f = 0; f < 6; ++f) cnt += per[(size_t)bi * 6 + f].size();
+    if (cnt > (size_t)PUSH_MAX_RULES) {
+      ctx->push_ok = false;
+      return BF_OK;
+    }
+  }
+  std::vector<int> range((size_t)nb * 12, 0);
+  ctx->h_push.clear();
+  for (size_t q = 0; q < per.size(); ++q) {
+    range[2 * q] = (int)ctx->h_push.size();
+    for (auto& r : per[q]) ctx->h_push.push_back(r);
+    range[2 * q + 1] = (int)ctx->h_push.size();
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(ctx->h_push.size(), 1) * sizeof(PushRule)));
+  if (!ctx->h_push.empty())
+    CK(cudaMemcpy(p, ctx->h_push.data(), ctx->h_push.size() * sizeof(PushRule),
+                  cudaMemcpyHostToDevice));
+  ctx->d_push = static_cast<PushRule*>(p);
+  CK(cudaMalloc(&p, range.size() * sizeof(int)));
+  CK(cudaMemcpy(p, range.data(), range.size() * sizeof(int), cudaMemcpyHostToDevice));
+  ctx->d_push_range = static_cast<int*>(p);
+  return BF_OK;
+}
+
 // One 4-D tensor map per (block, box shape) over the block arena:
 // dims (pitch, P1, P2, field slot), strides (sy, sz, fsz) doubles.  Box shapes
 // follow the stage kernel's tile (bf_stage.cuh): the 5-variable haloed plane,
@@ -917,8 +1063,24 @@ int nccl_exchange(bf_ctx* ctx) {
 }
 
 // ghosts of W[cur] for a standalone / NCCL ctx
+// Physical + local ghosts of W[cur] (and packed messages) unless the last
+// stage kernel already pushed them; on the first fill after an upload the
+// other buffer gets its constant ghosts (inflow, MMS) too, since pushes never
+// write those.
+int fill_ghosts(bf_ctx* ctx) {
+  if (ctx->pushed) return BF_OK;
+  if (!ctx->other_filled) {
+    ctx->cur ^= 1;
+    int rc = launch_fill(ctx);
+    ctx->cur ^= 1;
+    if (rc) return rc;
+    ctx->other_filled = true;
+  }
+  return launch_fill(ctx);
+}
+
 int ghosts_solo(bf_ctx* ctx) {
-  int rc = launch_fill(ctx);
+  int rc = fill_ghosts(ctx);
   if (rc) return rc;
   if (ctx->n_unpack) {
     if (!ctx->comm)
@@ -965,6 +1127,11 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.err = ctx->d_err;
   a.tmaps = ctx->d_tmaps;
   a.c = ctx->c;
+  const bool vl = ctx->sch.precision != BF_PRECISION_EXACT &&
+                  bf_fast::vl_active(ctx->sch.flux, flags);
+  a.push = (vl && ctx->push_ok && push_enabled()) ? 1 : 0;
+  a.push_rules = ctx->d_push;
+  a.push_range = ctx->d_push_range;
   {
     ProfScope ps(ctx, 0);
     CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
@@ -977,6 +1144,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
            ctx->stream));
   }
   if (flags & (F_PSI_STORE | F_PSI_LOAD)) ctx->psi_valid = true;
+  ctx->pushed = a.push != 0;
   ctx->cur ^= 1;
   ctx->t_derived = 1;
   return BF_OK;
@@ -1145,6 +1313,8 @@ void bf_destroy(bf_ctx* ctx) {
   cudaFree(ctx->d_tasks_fill);
   cudaFree(ctx->d_tasks_unpack);
   cudaFree(ctx->d_map_fill);
+  cudaFree(ctx->d_push);
+  cudaFree(ctx->d_push_range);
   cudaFree(ctx->d_map_unpack);
   cudaFree(ctx->d_partial);
   cudaFree(ctx->d_blocksum);
@@ -1418,6 +1588,8 @@ int bf_finalize(bf_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   int rc = build_tables(ctx);
   if (rc) return rc;
+  rc = build_push(ctx);
+  if (rc) return rc;
   rc = build_tiles(ctx);
   if (rc) return rc;
   rc = build_tensor_maps(ctx);
@@ -1486,6 +1658,8 @@ int bf_upload_fields(bf_ctx* ctx, int block_id, const double* const* fields6,
   ctx->ghost_buf = 0;
   ctx->t_derived = 0;
   ctx->psi_valid = false;
+  ctx->pushed = false;
+  ctx->other_filled = false;
   return BF_OK;
 }
 
@@ -1735,7 +1909,7 @@ int group_ghosts(bf_group* g) {
       for (int q = 0; q < n; ++q)
         if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
     }
-    int rc = launch_fill(ctx);
+    int rc = fill_ghosts(ctx);
     if (rc) return rc;
     for (auto& L : ctx->links) {
       if (!L.send) continue;

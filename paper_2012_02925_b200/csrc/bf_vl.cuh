@@ -129,6 +129,106 @@ BF_DEV double lam_term(double u, double v, double w, double snd, double nx, doub
   return (fabs(fma(u, nx, fma(v, ny, w * nz))) + snd) * A;
 }
 
+// Ghost push (PushRule, bf_internal.h): cell (i, j, k) got its new state
+// (r, u, v, w, p) in W[cur ^ 1]; write every ghost value of W[cur ^ 1] that the
+// next ghost update would derive from this cell.  Rare (cells within `g`
+// layers of a face) and kept out of line; the block's rules sit in shared
+// memory and the block scalars come by value, so a call has no global-load
+// dependency chain before its stores.
+struct PushSmem {
+  int range[6][2];
+  PushRule rules[PUSH_MAX_RULES];
+};
+
+__device__ __noinline__ void push_ghosts(const PushSmem* ps, double* base, long long sy,
+                                         long long sz, long long fsz, int n0, int n1, int n2,
+                                         int g, int ndim, int out, const Consts& c, int i, int j,
+                                         int k, double r, double u, double v, double w,
+                                         double p) {
+  const double T = BF_DIV(p, r * c.R);
+  const int cell[3] = {i, j, k};
+  const int nn[3] = {n0, n1, n2};
+  const long long st[3] = {1, sy, sz};
+  const long long o = i + sy * (long long)j + sz * (long long)k;
+  double* const W = base + (long long)fw(out, 0) * fsz;
+  for (int f = 0; f < 2 * ndim; ++f) {
+    const int ax = f >> 1, side = f & 1;
+    const int n = nn[ax], co = cell[ax];
+    if (side == 0 ? co >= g : co < n - g) continue;
+    for (int q = ps->range[f][0]; q < ps->range[f][1]; ++q) {
+      const PushRule& R = ps->rules[q];
+      if (i < R.lo[0] || i >= R.hi[0] || j < R.lo[1] || j >= R.hi[1] || k < R.lo[2] ||
+          k >= R.hi[2])
+        continue;
+      if (R.kind == PK_COPY || R.kind == PK_PACK) {
+        const long long d = R.base + (long long)(i - R.lo[0]) * R.coef[0] +
+                            (long long)(j - R.lo[1]) * R.coef[1] +
+                            (long long)(k - R.lo[2]) * R.coef[2];
+        const long long fs = R.dst_fsz;
+        if (R.kind == PK_COPY) {   // partner block's ghosts (halo.py:70-106)
+          double* D = R.dst + (long long)fw(out, 0) * fs;
+          D[d] = r;
+          D[fs + d] = u;
+          D[2 * fs + d] = v;
+          if (R.nfields == 6) D[3 * fs + d] = w;
+          D[4 * fs + d] = p;
+          D[5 * fs + d] = T;
+        } else {                   // message buffer (halo.py:47-67), fields packed in order
+          double* B = R.dst;
+          int e = 0;
+          B[(e++) * fs + d] = r;
+          B[(e++) * fs + d] = u;
+          B[(e++) * fs + d] = v;
+          if (R.nfields == 6) B[(e++) * fs + d] = w;
+          B[(e++) * fs + d] = p;
+          B[(e++) * fs + d] = T;
+        }
+        continue;
+      }
+      // physical patch (solver.py:281-403): ghost layer L sits at -1-L / n+L
+      const int layer = side == 0 ? co : n - 1 - co;
+      auto gofs = [&](int L) { return o + (long long)((side == 0 ? -1 - L : n + L) - co) * st[ax]; };
+      auto put = [&](long long og, double r_, double u_, double v_, double w_, double p_,
+                     double T_) {
+        W[og] = r_;
+        W[fsz + og] = u_;
+        W[2 * fsz + og] = v_;
+        W[3 * fsz + og] = w_;
+        W[4 * fsz + og] = p_;
+        W[5 * fsz + og] = T_;
+      };
+      if (R.kind == PK_OUTFLOW) {
+        for (int L = 0; L < g; ++L) put(gofs(L), r, u, v, w, p, T);
+        continue;
+      }
+      // outward unit normal of the boundary face at this tangential position
+      const long long fo = o + (long long)((side == 0 ? 0 : n) - co) * st[ax];
+      const double sg = side == 0 ? -1.0 : 1.0;
+      const double* fn = base + (long long)ffn(ax, 0) * fsz + fo;
+      const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
+      if (R.kind == PK_FARFIELD) {
+        const St qb = farfield_state(St{r, u, v, w, p}, nx, ny, nz, c);
+        const double tb = qb.p / (qb.r * c.R);
+        for (int L = 0; L < g; ++L) put(gofs(L), qb.r, qb.u, qb.v, qb.w, qb.p, tb);
+        continue;
+      }
+      double ug, vg, wg;
+      if (R.kind == PK_SLIP) {
+        const double vn = u * nx + v * ny + w * nz;
+        ug = u - 2.0 * vn * nx;
+        vg = v - 2.0 * vn * ny;
+        wg = w - 2.0 * vn * nz;
+      } else {
+        ug = -u;
+        vg = -v;
+        wg = -w;
+      }
+      const double tg = (R.kind == PK_NOSLIP && c.has_tw) ? 2.0 * c.tw - T : T;
+      put(gofs(layer), p / (c.R * tg), ug, vg, wg, p, tg);
+    }
+  }
+}
+
 template <int NDIM, int LIM>
 struct VCfg {
   static constexpr int TJ = Cfg<NDIM, LIM>::TJ;   // same tiles as the reference-order kernel
@@ -150,7 +250,8 @@ struct VCfg {
   static constexpr int OFY = r16(OFX + 4 * NFX);
   static constexpr int OZG = r16(OFY + 4 * NFY);         // [2][4][TJ][TI] z faces (3D)
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
-  static constexpr int OBAR = r16(OQ + 6 * NT);
+  static constexpr int OPS = r16(OQ + 6 * NT);                     // PushSmem
+  static constexpr int OBAR = r16(OPS + (int)((sizeof(PushSmem) + 7) / 8));
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr unsigned WBYTES = 5u * PLANE * 8u;
@@ -160,7 +261,7 @@ struct VCfg {
 };
 
 template <int NDIM, int LIM, bool K1, bool S0>
-__global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const __grid_constant__ StageArgs a) {
   using K = VCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
   constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
@@ -174,6 +275,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   double* const sZG = smem + K::OZG;
   double* const sQ = smem + K::OQ;
   unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem + K::OBAR);
+  PushSmem* const sPS = reinterpret_cast<PushSmem*>(smem + K::OPS);
   // bars[0..2]: plane ring, bars[3]: geometry group, bars[4]: Q0 / dt group
 
   const Tile t = a.tiles[blockIdx.x];
@@ -285,6 +387,15 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   if (tid == 0) {
     for (int q = 0; q < 5; ++q) mbar_init(bars + q, 1);
     fence_mbar_init();
+  }
+  if (a.push) {   // this block's ghost-push rules -> shared memory
+    const int* rg = a.push_range + t.block * 12;
+    const int r0 = rg[0], r1 = rg[11];
+    if (tid < 12) (&sPS->range[0][0])[tid] = rg[tid] - r0;
+    constexpr int RW = (int)(sizeof(PushRule) / 8);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.push_rules + r0);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(sPS->rules);
+    for (int q = tid; q < (r1 - r0) * RW; q += NT) dst[q] = src[q];
   }
   __syncthreads();
   if (tid == 0) {
@@ -645,6 +756,14 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
       if (last) {
 #pragma unroll
         for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
+      }
+      if (a.push) {
+        const int g = b.g;
+        const bool near = i < g || i >= ni - g || j < g || j >= nj - g ||
+                          (NDIM == 3 && (k < g || k >= nk - g));
+        if (near)
+          push_ghosts(sPS, b.base, sy, sz, fsz, ni, nj, nk, g, NDIM, a.cur ^ 1, c, i, j, k, qn[0],
+                      uu, vv, ww, pp);
       }
     }
   }
