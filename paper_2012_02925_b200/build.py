@@ -43,16 +43,17 @@ def up_to_date():
     return all(p.stat().st_mtime <= t for p in _sources())
 
 
-def build(force=False, verbose=False, tile_rows=None, lib=None):
+def build(force=False, verbose=False, tile_rows=None, lib=None, defines=(), tag=None):
     """tile_rows: 3D stage-kernel tile rows (16: 512-thread CTAs, 1 per SM;
-    8: 256-thread CTAs, 2 per SM); lib: output path (default libbfgpu.so)."""
+    8: 256-thread CTAs, 2 per SM); lib: output path (default libbfgpu.so);
+    defines / tag: extra -D flags for an experiment variant and its object tag."""
     global LIB
     out_lib = Path(lib) if lib else LIB
-    if not force and lib is None and tile_rows is None and up_to_date():
+    if not force and lib is None and tile_rows is None and not defines and up_to_date():
         return LIB
     OUT.mkdir(exist_ok=True)
-    tag = f"_tj{tile_rows}" if tile_rows else ""
-    defs = [f"-DBF_TJ3={tile_rows}"] if tile_rows else []
+    tag = f"_{tag}" if tag else (f"_tj{tile_rows}" if tile_rows else "")
+    defs = ([f"-DBF_TJ3={tile_rows}"] if tile_rows else []) + list(defines)
     jobs = [
         (CSRC / "bf_kernels.cu", OUT / f"bf_kernels_exact{tag}.o",
          ["-DBF_EXACT=1", "-fmad=false", *defs]),
@@ -76,10 +77,19 @@ def build(force=False, verbose=False, tile_rows=None, lib=None):
 
 if __name__ == "__main__":
     rows = None
+    variant = None
+    defs = []
     for a in sys.argv[1:]:
         if a.startswith("--tile-rows="):
             rows = int(a.split("=", 1)[1])
-    if rows:
+        elif a.startswith("--variant="):
+            variant = a.split("=", 1)[1]
+        elif a.startswith("-D"):
+            defs.append(a)
+    if variant:
+        build(force=True, verbose=True, tile_rows=rows, lib=PKG / f"libbfgpu_{variant}.so",
+              defines=defs, tag=variant)
+    elif rows:
         build(force=True, verbose=True, tile_rows=rows, lib=PKG / f"libbfgpu_tj{rows}.so")
     else:
         build(force="--force" in sys.argv, verbose=True)

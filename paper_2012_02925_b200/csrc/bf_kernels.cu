@@ -383,6 +383,8 @@ static cudaError_t launch_stage_l(int lim, const StageArgs& a, cudaStream_t s) {
 #if !BF_EXACT
 // FAST Van Leer with limiters computed in-kernel runs the cell-split kernel
 // (bf_vl.cuh), which also pushes the next stage's ghosts when a.push is set.
+bool vl_push_compiled() { return BF_VL_PUSH != 0; }
+
 bool vl_active(int flux, int flags) {
   return flux == FLUX_VAN_LEER && !(flags & (F_PSI_LOAD | F_PSI_STORE)) && !vl_disabled();
 }

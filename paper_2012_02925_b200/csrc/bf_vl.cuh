@@ -30,11 +30,26 @@
 // scaling per half, FMA, Newton reciprocals): held to the 1e-12 bar.
 #pragma once
 
+// In-kernel ghost push (PushRule): compiled in with -DBF_VL_PUSH=1 only; on
+// C4 it is slower than the separate ghost launch.
+#ifndef BF_VL_PUSH
+#define BF_VL_PUSH 0
+#endif
+
 BF_DEV void tma_prefetch4(const void* tmap, int x, int y, int z, int s) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
                    reinterpret_cast<unsigned long long>(tmap)),
                "r"(x), "r"(y), "r"(z), "r"(s)
                : "memory");
+}
+
+// 1/b: MUFU seed (~2^-22) and one Newton step (~2^-44 relative).  Used only for
+// the Van Albada limiter quotient, whose error enters the face states as
+// (error) x (eps/4) x D, i.e. ~1e-14 of the cell-to-cell difference.
+BF_DEV double frcp1(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  return fma(r, fma(-b, r, 1.0), r);
 }
 
 // a / b with a single-Newton reciprocal and one quotient correction (~1 ulp)
@@ -69,7 +84,7 @@ BF_DEV void vl_recon(double wm, double w0, double wp, const Consts& c, double& q
   const double dm = w0 - wm, dp = wp - w0;
   if constexpr (K1 && LIM == LIM_VAN_ALBADA) {
     // (eps/4)(1-k) Psi = Psi/2 = (ab + 1e-12/2) / (a^2 + b^2 + 1e-12), a = D+, b = D-
-    const double t = fmax(fdiv1(fma(dp, dm, 0.5e-12), fma(dp, dp, fma(dm, dm, 1e-12))), 0.0);
+    const double t = fmax(fma(dp, dm, 0.5e-12) * frcp1(fma(dp, dp, fma(dm, dm, 1e-12))), 0.0);
     qL = fma(t, dm, w0);
     qR = fma(-t, dp, w0);
     return;
@@ -124,6 +139,12 @@ BF_DEV void vl_half(const double q[5], double nx, double ny, double nz, double A
 }
 
 // local-time-step term (solver.py:709-716) of one face
+// sound speed sqrt(g p / rho) = g p / sqrt(g p rho): one reciprocal square root
+BF_DEV double sound_speed(double rho, double p, const Consts& c) {
+  const double gp = c.gamma * p;
+  return gp * frsqrt(gp * rho);
+}
+
 BF_DEV double lam_term(double u, double v, double w, double snd, double nx, double ny, double nz,
                        double A) {
   return (fabs(fma(u, nx, fma(v, ny, w * nz))) + snd) * A;
@@ -474,7 +495,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         }
       }
       if (stage0) {
-        const double snd = fsqrt(c.gamma * wc[4] * frcp(wc[0]));
+        const double snd = sound_speed(wc[0], wc[4], c);
         lamz = lam_term(wc[1], wc[2], wc[3], snd, g0[0], g0[1], g0[2], g0[3]) +
                lam_term(wc[1], wc[2], wc[3], snd, g1[0], g1[1], g1[2], g1[3]);
       }
@@ -499,7 +520,10 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     mbar_wait(bar_of(k), par_of(k));
 
     // ---- phase A1: tile-edge half fluxes ----------------------------------------------
-    if (tid < K::NH) {
+#ifndef BF_ABLATE_HALO
+#define BF_ABLATE_HALO 0
+#endif
+    if (!BF_ABLATE_HALO && tid < K::NH) {
       const int h = tid;
       int cx, cy, st, d, fo;
       double sg;
@@ -597,7 +621,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         sHM[v * NHY + ty * TI + tx] = hm[v];
       }
       if (stage0 && cell_on) {
-        const double snd = fsqrt(c.gamma * w[4 * PLANE] * frcp(w[0]));
+        const double snd = sound_speed(w[0], w[4 * PLANE], c);
         lam = lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[0], gl[NFY], gl[2 * NFY],
                        gl[3 * NFY]) +
               lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[TI], gl[NFY + TI],
@@ -641,9 +665,10 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
           hpz[v] = hp1[v];
         }
         if (stage0) {
-          const double snd = fsqrt(c.gamma * wc[4] * frcp(wc[0]));
-          lamz = lam_term(wc[1], wc[2], wc[3], snd, glo[0], glo[NT], glo[2 * NT], glo[3 * NT]) +
-                 lam_term(wc[1], wc[2], wc[3], snd, ghi[0], ghi[NT], ghi[2 * NT], ghi[3 * NT]);
+          const double snd1 = sound_speed(wc[0], wc[4], c);
+          lamz = lam_term(wc[1], wc[2], wc[3], snd1, glo[0], glo[NT], glo[2 * NT], glo[3 * NT]) +
+                 lam_term(wc[1], wc[2], wc[3], snd1, ghi[0], ghi[NT], ghi[2 * NT], ghi[3 * NT]);
+
         }
       }
     }
@@ -700,7 +725,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
 #pragma unroll
       for (int v = 0; v < 5; ++v) R[v] += fhi[v] - flo[v];
       if (stage0 && cell_on) {
-        const double snd = fsqrt(c.gamma * w[4 * PLANE] * frcp(w[0]));
+        const double snd = sound_speed(w[0], w[4 * PLANE], c);
         lam += lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[0], gl[NFX], gl[2 * NFX],
                         gl[3 * NFX]) +
                lam_term(w[PLANE], w[2 * PLANE], w[3 * PLANE], snd, gl[1], gl[NFX + 1],
@@ -757,6 +782,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
 #pragma unroll
         for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
       }
+#if BF_VL_PUSH
       if (a.push) {
         const int g = b.g;
         const bool near = i < g || i >= ni - g || j < g || j >= nj - g ||
@@ -765,6 +791,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
           push_ghosts(sPS, b.base, sy, sz, fsz, ni, nj, nk, g, NDIM, a.cur ^ 1, c, i, j, k, qn[0],
                       uu, vv, ww, pp);
       }
+#endif
     }
   }
 
