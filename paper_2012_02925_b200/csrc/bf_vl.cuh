@@ -514,6 +514,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
       issue_b(k);
       if constexpr (NDIM == 3) {
         if (kk > 0) issue_plane(k + 2);   // into the slot of plane k-1
+        // plane k+3 into L2 now, so next iteration's TMA of it is an L2 hit
+        if (kk + 1 < kc)
+          tma_prefetch4(tm, b.ox + i0 - HALO, b.oy + j0 - HALO, b.oz + k + 3, fw(a.cur, 0));
       }
     }
     mbar_wait(bars + 3, (unsigned)(kk & 1));
