@@ -424,6 +424,7 @@ def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist,
     dt = marks["download"] - t0
     names = list(marks)
     phases = {n: marks[n] - marks[p] for p, n in zip(names, names[1:])}
+    phases["ctx_detail"] = gpu.timing
     if dist:
         t = torch.tensor([dt], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

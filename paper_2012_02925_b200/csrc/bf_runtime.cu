@@ -1269,6 +1269,15 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
     return nullptr;
   }
   ctx->stream = ctx->own_stream;
+  {   // staging buffers (uploads, downloads) come from the stream-ordered pool;
+      // keep its memory mapped between calls instead of releasing it at every
+      // synchronisation (re-mapping 100+ MB per call dominated the transfers)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      cuuint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   // constants, in the reference's scalar evaluation order (python floats)
   Consts& c = ctx->c;
   const double g = gas->gamma;
@@ -1308,6 +1317,10 @@ void bf_destroy(bf_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
   for (auto& hb : ctx->blocks) {
     for (double* p : hb.owned) cudaFree(p);
     for (int f = 0; f < 6; ++f)

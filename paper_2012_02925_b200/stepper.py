@@ -167,8 +167,10 @@ class GpuContext:
             precision=native.PRECISION[precision])
         gas_s = native.Gas(gamma=float(gas.gamma), R=float(gas.R))
         fs_s = native.Freestream(*(float(getattr(freestream, n)) for n in FIELD_NAMES))
+        t_create = time.perf_counter()
         self.ctx = self.L.bf_create(self.ndim, C.byref(gas_s), C.byref(sch), C.byref(fs_s),
                                     device, rank, nranks)
+        self.timing = {"create_s": time.perf_counter() - t_create, "blocks_s": []}
         if not self.ctx:
             raise NativeLibraryError(f"bf_create failed (device {device}, rank {rank}/{nranks})")
         self.setups = {}
@@ -187,9 +189,11 @@ class GpuContext:
                 if any(n.strides != nodes[0].strides for n in nodes):
                     nodes = [np.ascontiguousarray(n) for n in nodes]
                     st = [x // 8 for x in nodes[0].strides] + [0] * (3 - self.ndim)
+                t_blk = time.perf_counter()
                 self._check(self.L.bf_add_block_nodes(
                     self.ctx, cid, native.ints(s.block.dims), s.block.ghost_depth,
                     native.dptrs(nodes), (C.c_longlong * 3)(*st), None))
+                self.timing["blocks_s"].append(time.perf_counter() - t_blk)
                 continue
             fv = []
             for d in range(self.ndim):
