@@ -180,6 +180,7 @@ struct PushRule {
 struct StageArgs {
   const DevBlock* blocks;
   const Tile* tiles;
+  const int* tile_list; // CTA b runs tile tile_list[b] (null: tile b); partials by tile id
   int ntiles;
   int cur;              // read W[cur], write W[cur ^ 1]
   int stage;

@@ -18,6 +18,7 @@
 #include <map>
 #include <memory>
 #include <cstdlib>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -373,6 +374,17 @@ struct bf_ctx {
   int device = 0, rank = 0, nranks = 1;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // halo exchange overlapped with interior tiles (bf_step): messages + unpack on
+  // comm_stream while the stage kernel runs the tiles that read no remote ghost
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_filled = nullptr, ev_unpacked = nullptr;
+  int* d_tiles_in = nullptr;       // tile ids reading no remote-received ghost cell
+  int* d_tiles_bd = nullptr;       // the others (launched after the unpack)
+  int n_tiles_in = 0, n_tiles_bd = 0;
+  bool split_tiles = false;        // interior / boundary tile lists built
+  bool split_forced = false;       // BF_SPLIT_TILES=1
+  bool exchange_pending = false;   // ev_unpacked must be waited on before boundary tiles
+  bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
   std::vector<HostBlock> blocks;
   std::map<int, int> index_of;     // block id -> position
   std::vector<HostPatch> patches;
@@ -1011,6 +1023,49 @@ int build_tiles(bf_ctx* ctx) {
   }
   tb.push_back((int)tiles.size());
   ctx->ntiles = (int)tiles.size();
+  {
+    // interior / boundary split: a tile is boundary when it touches a block face
+    // carrying a remote (message) link — its halo reads ghost cells filled by the
+    // unpack.  BF_SPLIT_TILES=1 forces the two-launch path on every block face
+    // (exercised on one GPU by the tests).
+    const char* e = std::getenv("BF_SPLIT_TILES");
+    const bool force = e && e[0] == '1';
+    std::vector<std::array<bool, 6>> remote(ctx->blocks.size());
+    for (auto& r : remote) r.fill(force);
+    bool any = force;
+    for (auto& L : ctx->links)
+      if (L.send) {
+        remote[ctx->index_of[L.block]][L.face] = true;
+        any = true;
+      }
+    std::vector<int> tin, tbd;
+    const int TJ = bf_exact::stage_tile_rows(ctx->ndim, ctx->sch.limiter);
+    for (int q = 0; q < (int)tiles.size(); ++q) {
+      const Tile& t = tiles[q];
+      const HostBlock& hb = ctx->blocks[t.block];
+      const auto& rf = remote[t.block];
+      const bool bd = (rf[0] && t.i0 == 0) || (rf[1] && t.i0 + TI >= hb.n[0]) ||
+                      (rf[2] && t.j0 == 0) || (rf[3] && t.j0 + TJ >= hb.n[1]) ||
+                      (ctx->ndim == 3 && ((rf[4] && t.k0 == 0) || (rf[5] && t.k0 + t.kc >= hb.n[2])));
+      (bd ? tbd : tin).push_back(q);
+    }
+    ctx->split_tiles = any;
+    ctx->split_forced = force;
+    ctx->n_tiles_in = (int)tin.size();
+    ctx->n_tiles_bd = (int)tbd.size();
+    if (any) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, std::max<size_t>(tin.size(), 1) * sizeof(int)));
+      if (!tin.empty()) CK(cudaMemcpy(q, tin.data(), tin.size() * sizeof(int), cudaMemcpyHostToDevice));
+      ctx->d_tiles_in = static_cast<int*>(q);
+      CK(cudaMalloc(&q, std::max<size_t>(tbd.size(), 1) * sizeof(int)));
+      if (!tbd.empty()) CK(cudaMemcpy(q, tbd.data(), tbd.size() * sizeof(int), cudaMemcpyHostToDevice));
+      ctx->d_tiles_bd = static_cast<int*>(q);
+      CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_filled, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_unpacked, cudaEventDisableTiming));
+    }
+  }
   void* p = nullptr;
   CK(cudaMalloc(&p, std::max<size_t>(tiles.size(), 1) * sizeof(Tile)));
   CK(cudaMemcpy(p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
@@ -1094,6 +1149,22 @@ int fill_ghosts(bf_ctx* ctx) {
 int ghosts_solo(bf_ctx* ctx) {
   int rc = fill_ghosts(ctx);
   if (rc) return rc;
+  if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap) {
+    // messages and unpack on the comm stream; the interior tiles of the next stage
+    // launch run meanwhile (launch_stage_kernel waits on ev_unpacked)
+    CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_filled, 0));
+    cudaStream_t saved = ctx->stream;
+    ctx->stream = ctx->comm_stream;
+    rc = nccl_exchange(ctx);
+    if (!rc) rc = launch_unpack(ctx);
+    ctx->stream = saved;
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev_unpacked, ctx->comm_stream));
+    ctx->exchange_pending = true;
+    ctx->ghost_buf = ctx->cur;
+    return BF_OK;
+  }
   if (ctx->n_unpack) {
     if (!ctx->comm)
       return fail(ctx, BF_EINVAL,
@@ -1146,7 +1217,26 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.push_range = ctx->d_push_range;
   {
     ProfScope ps(ctx, 0);
-    CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
+    // two launches only when they buy an overlap (NCCL messages in flight) or
+    // when forced; the split costs tile-order L2 locality and a second tail
+    const bool split = ctx->split_tiles &&
+                       (ctx->split_forced || (ctx->comm && ctx->n_unpack && !ctx->no_overlap));
+    if (!split) {
+      CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
+    } else {
+      // interior tiles first; the boundary tiles after the exchange has landed
+      StageArgs b = a;
+      b.tile_list = ctx->d_tiles_in;
+      b.ntiles = ctx->n_tiles_in;
+      CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->stream));
+      if (ctx->exchange_pending) {
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_unpacked, 0));
+        ctx->exchange_pending = false;
+      }
+      b.tile_list = ctx->d_tiles_bd;
+      b.ntiles = ctx->n_tiles_bd;
+      CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->stream));
+    }
   }
   if (flags & F_STAGE0) {
     ProfScope ps(ctx, 3);
@@ -1262,6 +1352,7 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   ctx->rank = rank;
   ctx->nranks = nranks;
   if (const char* e = std::getenv("BF_KC")) ctx->kc = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("BF_NO_OVERLAP")) ctx->no_overlap = e[0] == '1';
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
                                                                         cudaStreamNonBlocking) !=
                                                   cudaSuccess) {
@@ -1354,6 +1445,11 @@ void bf_destroy(bf_ctx* ctx) {
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_filled) cudaEventDestroy(ctx->ev_filled);
+  if (ctx->ev_unpacked) cudaEventDestroy(ctx->ev_unpacked);
+  cudaFree(ctx->d_tiles_in);
+  cudaFree(ctx->d_tiles_bd);
   delete ctx;
 }
 

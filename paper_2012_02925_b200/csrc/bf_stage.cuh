@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
   constexpr int NFLAT = NT - NHALF;            // threads on the flat limiter loop
   // bars[0..2]: plane ring slots, bars[3]: per-plane geometry/Q0 group
 
-  const Tile t = a.tiles[blockIdx.x];
+  const int tile_id = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
+  const Tile t = a.tiles[tile_id];
   const DevBlock b = a.blocks[t.block];     // by value: no aliasing reloads
   const Consts& c = a.c;
   const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
     if (tid < 5) {
       double x = 0.0;
       for (int w = 0; w < NT / 32; ++w) x += red[w * 5 + tid];
-      a.partial[(long long)blockIdx.x * 5 + tid] = x;
+      a.partial[(long long)tile_id * 5 + tid] = x;
     }
   }
 }

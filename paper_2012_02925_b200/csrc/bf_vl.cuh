@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   PushSmem* const sPS = reinterpret_cast<PushSmem*>(smem + K::OPS);
   // bars[0..2]: plane ring, bars[3]: geometry group, bars[4]: Q0 / dt group
 
-  const Tile t = a.tiles[blockIdx.x];
+  const int tile_id = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
+  const Tile t = a.tiles[tile_id];
   const DevBlock b = a.blocks[t.block];
   const Consts& c = a.c;
   const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
     if (tid < 5) {
       double x = 0.0;
       for (int q = 0; q < NT / 32; ++q) x += red[q * 5 + tid];
-      a.partial[(long long)blockIdx.x * 5 + tid] = x;
+      a.partial[(long long)tile_id * 5 + tid] = x;
     }
   }
 }
