@@ -1061,7 +1061,11 @@ int build_tiles(bf_ctx* ctx) {
       CK(cudaMalloc(&q, std::max<size_t>(tbd.size(), 1) * sizeof(int)));
       if (!tbd.empty()) CK(cudaMemcpy(q, tbd.data(), tbd.size() * sizeof(int), cudaMemcpyHostToDevice));
       ctx->d_tiles_bd = static_cast<int*>(q);
-      CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+      // high priority: when a stage-kernel CTA retires, the block scheduler hands the
+      // SM to the NCCL / unpack kernels first
+      int lo_prio = 0, hi_prio = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      CK(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
       CK(cudaEventCreateWithFlags(&ctx->ev_filled, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ctx->ev_unpacked, cudaEventDisableTiming));
     }

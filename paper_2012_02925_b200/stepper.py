@@ -286,10 +286,19 @@ class GpuContext:
             rng = np.random.default_rng(seed)
             mine = set(self.child_ids)
             for c in sorted(self.plan.children, key=lambda c: c.id):
-                blk = self.setups[c.id].block if c.id in mine else self.plan.child_block(c.id)
-                f = perturbed_state(blk, self.fs, self.gas, rng)
                 if c.id not in mine:
+                    # consume the same draws (rho, then p, C order) without the arrays
+                    n = int(np.prod(c.dims)) if hasattr(c, "dims") else \
+                        self.plan.child_block(c.id).cell_count()
+                    for _ in range(2):
+                        left = n
+                        while left > 0:
+                            m = min(left, 1 << 24)
+                            rng.standard_normal(m)
+                            left -= m
                     continue
+                blk = self.setups[c.id].block
+                f = perturbed_state(blk, self.fs, self.gas, rng)
                 self.upload(c.id, [f[n] for n in FIELD_NAMES])   # Q derived on the device
             return
         for cid in self.child_ids:
