@@ -79,9 +79,13 @@ extern "C" {
 typedef struct bf_ctx bf_ctx;
 typedef struct bf_group bf_group;
 
-typedef struct bf_gas {            /* physics.py:47-62 (inviscid part) */
+typedef struct bf_gas {            /* physics.py:47-90 */
   double gamma;
   double R;
+  double mu;                       /* constant viscosity (sutherland unset)      */
+  double prandtl;
+  int has_sutherland;              /* 1: mu(T) = Sutherland's law               */
+  double sutherland[3];            /* (mu_ref, T_ref, S)                        */
 } bf_gas;
 
 typedef struct bf_freestream {     /* solver.py:74-98 */
@@ -100,6 +104,7 @@ typedef struct bf_scheme {         /* solver.py:38-66 */
   int has_wall_temperature;
   double wall_temperature;
   int precision;                   /* BF_PRECISION_*                 */
+  int viscous;                     /* laminar NS (solver.py:38-71)   */
 } bf_scheme;
 
 /* --- context lifetime (replaces BlockSolver construction, solver.py:189-231,
@@ -140,11 +145,31 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
 int bf_add_bc_patch(bf_ctx* ctx, int block_id, int bc_type, int face, const int box[6],
                     const double* dirichlet);
 
+/* Same as bf_add_bc_patch plus, for laminar NS (ghost round 2,
+   solver.py:285-305), the MMS ghost values of the EXTENDED patch: tangential
+   ranges widened by the ghost depth, layout [layer][6 fields][t] i-fastest
+   over the extended tangential cells (NULL for other bc types).           */
+int bf_add_bc_patch_ext(bf_ctx* ctx, int block_id, int bc_type, int face, const int box[6],
+                        const double* dirichlet, const double* dirichlet_ext);
+
 /* One connected endpoint (topology.py:90-188; halo.py:47-115).  axis_map[6] =
    (b0,s0,b1,s1,b2,s2).  peer_rank == own rank and peer_block registered in this
    ctx -> same-device copy; otherwise a message to/from peer_rank tagged `tag`. */
 int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int axis_map[6],
                 int peer_block, int peer_face, const int peer_box[6], int peer_rank, int tag);
+
+/* Laminar NS: the face gradient matrices of a block (solver.py:582-642, the
+   inverse-transposed computational->physical Jacobian), computed on the host
+   with the reference's numpy operations.  grad_invT[9*d + 3*r + e] for
+   d < ndim: Fortran array over the faces of direction d (N_d+1 along d,
+   interior tangential), row r, column e; NULL entries are zero.           */
+int bf_add_viscous_geometry(bf_ctx* ctx, int block_id, const double* const* grad_invT);
+
+/* Ghost round 2 (viscous) unpack order: order[q] = position of the q-th
+   bf_add_link call in the reference's exchange sequence (serial driver:
+   rank-major schedule order, solver.py:869-899; distributed engine: local
+   entries, then remote, exchange.py:495-521).  Default: call order.      */
+int bf_set_round2_order(bf_ctx* ctx, int nlinks, const int* order);
 
 /* Freeze the topology: device tables, tiles, buffers.  Must precede uploads. */
 int bf_finalize(bf_ctx* ctx);

@@ -134,6 +134,28 @@ def van_leer(left, right, nx, ny, nz, gamma):
     return tuple(a + b for a, b in zip(plus, minus))
 
 
+def viscous_flux_arrays(grad_vel, grad_t, u, v, w, mu, k, nx, ny, nz):
+    """Stokes viscous normal flux (physics.py:312-344): lambda = -2/3 mu,
+    tau from the velocity gradient, energy = tau . V + k grad T."""
+    (ux, uy, uz), (vx, vy, vz), (wx, wy, wz) = grad_vel
+    div = ux + vy + wz
+    lam = -2.0 / 3.0 * mu
+    txx = 2.0 * mu * ux + lam * div
+    tyy = 2.0 * mu * vy + lam * div
+    tzz = 2.0 * mu * wz + lam * div
+    txy = mu * (uy + vx)
+    txz = mu * (uz + wx)
+    tyz = mu * (vz + wy)
+    fx = nx * txx + ny * txy + nz * txz
+    fy = nx * txy + ny * tyy + nz * tyz
+    fz = nx * txz + ny * tyz + nz * tzz
+    qx = u * txx + v * txy + w * txz + k * grad_t[0]
+    qy = u * txy + v * tyy + w * tyz + k * grad_t[1]
+    qz = u * txz + v * tyz + w * tzz + k * grad_t[2]
+    fe = nx * qx + ny * qy + nz * qz
+    return np.zeros_like(fx), fx, fy, fz, fe
+
+
 def farfield(rho, u, v, w, p, fs, nx, ny, nz, gamma):
     """Riemann-invariant farfield state; (nx,ny,nz) outward (solver.py:138-171)."""
     g = gamma
@@ -225,11 +247,30 @@ def _exchanged(ndim):
 
 
 def pack_face(fields, spec, dims, ghost, round_no=1):
-    """Send-box values, i-fastest, one flat array per exchanged field."""
+    """Send-box values, i-fastest, one flat array per exchanged field.
+
+    Like halo.py:47-67: the velocity components are copied into an
+    interleaved buffer, while rho, p and T are ``ravel(order="F")`` of the
+    box — a VIEW of the field when the box is Fortran-contiguous (e.g. a
+    full-width j- or k-face box), so in round 2 (pack-all-then-unpack-all)
+    those fields are read at unpack time, after earlier unpacks.  The device
+    reproduces this (bf_runtime.cu round-2 tasks, `view` fields)."""
     send, _ = _halo_boxes(spec, dims, ghost, round_no)
     cut = tuple(slice(lo, hi) for lo, hi in send)
     ndim = 2 if ghost[2] == 0 else 3
-    return {n: fields[n][cut].ravel(order="F") for n in _exchanged(ndim)}
+    out = {}
+    for n in _exchanged(ndim):
+        flat = fields[n][cut].ravel(order="F")
+        out[n] = flat.copy() if n in ("u", "v", "w") else flat
+    return out
+
+
+def pack_is_view(shape, box):
+    """Whether halo.pack_face's ravel(order="F") of `box` in a padded Fortran
+    array of `shape` is a view (then rho, p, T are read at unpack time)."""
+    probe = np.zeros(shape, order="F")
+    cut = tuple(slice(lo, hi) for lo, hi in box)
+    return bool(np.shares_memory(probe[cut].ravel(order="F"), probe))
 
 
 def unpack_face(buffers, fields, spec, dims, ghost, partner_side, round_no=1):
@@ -292,6 +333,8 @@ class OracleBlock:
         self.mms_solution = mms_solution
         self.source = None
         self._dirichlet = {}
+        if config.viscous:
+            self.grad_invT = {d: self.gradient_matrix(d) for d in self.dirs}
         if config.mms_id is not None:
             c = metrics.centers
             xs, ys, zs = (c[i][self.inner] for i in range(3))
@@ -505,8 +548,111 @@ class OracleBlock:
         F = [comp * ar for comp in F]
         self._boundary_fluxes(d, F)
         if self.config.viscous:
-            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+            Fv = self.viscous_flux(d)
+            F = [a - b for a, b in zip(F, Fv)]
         return F
+
+    # laminar viscous terms (solver.py:582-692, physics.py:312-344) --------------------
+    def gradient_matrix(self, d):
+        """(3, 3, faces) inverse-transposed Jacobian of computational -> physical
+        coordinates at the faces of direction d (solver.py:582-642): column e of
+        the Jacobian is the cell-centre difference across the face (e = d) or
+        the mid-edge node difference along e; out[row, e] = inv(J)^T."""
+        g, n, ndim = self.g, self.n, self.block.ndim
+        cen = self.metrics.centers
+        cols = {}
+        line = [slice(g[a], g[a] + n[a]) for a in range(3)]
+        hi_c, lo_c = list(line), list(line)
+        hi_c[d] = slice(g[d], g[d] + n[d] + 1)
+        lo_c[d] = slice(g[d] - 1, g[d] + n[d])
+        cols[d] = cen[(slice(None), *hi_c)] - cen[(slice(None), *lo_c)]
+        if ndim == 3:
+            xyz = tuple(self.block.nodes)
+        else:
+            x2, y2 = self.block.nodes[0][..., None], self.block.nodes[1][..., None]
+            xyz = (x2, y2, np.zeros_like(x2))
+        for e in self.dirs:
+            if e == d:
+                continue
+            base = [slice(g[a], g[a] + n[a]) for a in range(3)]
+            base[d] = slice(g[d], g[d] + n[d] + 1)
+            others = [a for a in self.dirs if a not in (d, e)]
+
+            def shifted(sl, axis):
+                out = list(sl)
+                out[axis] = slice(sl[axis].start + 1, sl[axis].stop + 1)
+                return out
+
+            up = shifted(base, e)
+            diff = []
+            for comp in xyz:
+                if others:
+                    a = others[0]
+                    hi = 0.5 * (comp[tuple(up)] + comp[tuple(shifted(up, a))])
+                    lo = 0.5 * (comp[tuple(base)] + comp[tuple(shifted(base, a))])
+                else:
+                    hi, lo = comp[tuple(up)], comp[tuple(base)]
+                diff.append(hi - lo)
+            cols[e] = np.stack(diff)
+        shape = cols[d].shape[1:]
+        J = np.zeros((*shape, ndim, ndim))
+        for c, e in enumerate(self.dirs):
+            for r in range(ndim):
+                J[..., r, c] = cols[e][r]
+        jinvT = np.linalg.inv(J).swapaxes(-1, -2)
+        out = np.zeros((3, 3, *shape))
+        for r in range(ndim):
+            for c, e in enumerate(self.dirs):
+                out[r, e] = jinvT[..., r, c]
+        return out
+
+    def viscous_flux(self, d):
+        """Viscous normal flux x area on the faces of direction d (solver.py:644-692):
+        computational-space differences of u, v, w, T (normal: across the face;
+        tangential: quarter of the 4-point difference), mapped by the face
+        matrix, Stokes stress with the face-averaged T, mu and k."""
+        g, n = self.g[d], self.n[d]
+        names = ("u", "v", "w", "T")
+        dxi = {}
+        for nm in names:
+            w = self.fields[nm]
+            per = {d: w[self.run(d, g, g + n + 1)] - w[self.run(d, g - 1, g + n)]}
+            for e in self.dirs:
+                if e == d:
+                    continue
+
+                def shift(start, stop, off):
+                    cut = list(self.run(d, start, stop))
+                    cut[e] = slice(cut[e].start + off, cut[e].stop + off)
+                    return tuple(cut)
+
+                plus = w[shift(g - 1, g + n, +1)] + w[shift(g, g + n + 1, +1)]
+                minus = w[shift(g - 1, g + n, -1)] + w[shift(g, g + n + 1, -1)]
+                per[e] = 0.25 * (plus - minus)
+            dxi[nm] = per
+        M = self.grad_invT[d]
+
+        def physical(nm):
+            rows = []
+            for r in range(3):
+                acc = None
+                for e in self.dirs:
+                    t = M[r, e] * dxi[nm][e]
+                    acc = t if acc is None else acc + t
+                rows.append(acc)
+            return rows
+
+        gu, gv, gw, gT = (physical(nm) for nm in names)
+        mean = {nm: 0.5 * (self.fields[nm][self.run(d, g - 1, g + n)]
+                           + self.fields[nm][self.run(d, g, g + n + 1)]) for nm in names}
+        mu = self.gas.viscosity(mean["T"])
+        k = self.gas.conductivity(mean["T"])
+        cut = self.face_cut(d)
+        nh = self.normal[d][cut]
+        ar = self.area[d][cut[1:]]
+        Fv = viscous_flux_arrays([gu, gv, gw], gT, mean["u"], mean["v"], mean["w"], mu, k,
+                                 nh[0], nh[1], nh[2])
+        return [comp * ar for comp in Fv]
 
     def _boundary_fluxes(self, d, F):
         f, g = self.fields, self.g
@@ -565,7 +711,13 @@ class OracleBlock:
                 nx, ny, nz = (along(nh[i], d, lo, lo + self.n[d]) for i in range(3))
                 lam += (np.abs((u * nx + v * ny) + w * nz) + a) * along(ar, d, lo, lo + self.n[d])
         if self.config.viscous:
-            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+            # viscous spectral radius (solver.py:717-730)
+            mu = self.gas.viscosity(f["T"][self.inner])
+            coeff = 2.0 * max(4.0 / 3.0, self.gas.gamma / self.gas.prandtl)
+            for d in self.dirs:
+                ar = self.area[d][self.face_cut(d)[1:]]
+                abar = 0.5 * (along(ar, d, 0, self.n[d]) + along(ar, d, 1, self.n[d] + 1))
+                lam += coeff * (mu / rho) * abar * abar / self.vol
         return (cfl * self.vol) / lam
 
     def snapshot(self):
@@ -608,8 +760,10 @@ class OracleStepper:
         self.exchange_fn(1)
         for b in self.blocks.values():
             b.fill_physical_ghosts(extended=False)
-        if self.config.viscous:
-            raise NotImplementedError("viscous path is not restated (SURVEY §8f row 1)")
+        if self.config.viscous:   # edge / corner completion (solver.py:781-784)
+            self.exchange_fn(2)
+            for b in self.blocks.values():
+                b.fill_physical_ghosts(extended=True)
 
     def step(self, step_index):
         fz = self.config.limiter_freeze_at
@@ -647,14 +801,20 @@ def make_serial_exchange(plan, schedule, blocks):
     order = [e for r in sorted(schedule.per_rank) for e in schedule.per_rank[r]]
 
     def exchange(round_no):
-        if round_no != 1:
-            raise NotImplementedError("round 2 is viscous-only")
+        # round 1: copy per entry; round 2: every buffer packed before any unpack
+        # (snapshot of the post-round-1 state, solver.py:869-899)
+        packed = []
         for e in order:
             dst, src = blocks[e.child], blocks[e.peer_child]
             ps = _peer_spec(plan, e)
-            bufs = pack_face(src.fields, ps, src.block.dims, src.block.ghost, 1)
+            bufs = pack_face(src.fields, ps, src.block.dims, src.block.ghost, round_no)
             side = FACE_NAMES.index(ps.face) % 2
-            unpack_face(bufs, dst.fields, e.spec, dst.block.dims, dst.block.ghost, side, 1)
+            if round_no == 1:
+                unpack_face(bufs, dst.fields, e.spec, dst.block.dims, dst.block.ghost, side, 1)
+            else:
+                packed.append((e, dst, bufs, side))
+        for e, dst, bufs, side in packed:
+            unpack_face(bufs, dst.fields, e.spec, dst.block.dims, dst.block.ghost, side, 2)
     return exchange
 
 

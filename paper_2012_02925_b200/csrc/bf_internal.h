@@ -75,6 +75,11 @@ struct Consts {
   double inv_gamma, inv_vlc;               // 1/gamma, 1/vl_c (fast mode only)
   double tw;                               // wall temperature
   int has_tw;
+  double mu, prandtl, cp;                  // viscosity law (physics.py:47-90)
+  double suth_mu, suth_t, suth_s;          // Sutherland (mu_ref, T_ref, S)
+  double visc_coeff;                       // 2 max(4/3, gamma/Pr) (solver.py:722)
+  int has_suth;
+  int viscous;
   int eps0;                                // epsilon == 0
   int kappa_m1;                            // kappa == -1 (fast mode drops the zero terms)
   int muscl_k1;                            // epsilon == 1 and kappa == -1 (cell-split kernel)
@@ -87,6 +92,10 @@ constexpr int FDTV = 17;         // dt / V
 constexpr int FVOL = 18;         // V
 constexpr int FFN = 19;          // face geometry FFN + 4*d + c   (nx, ny, nz, A)
 constexpr int FSRC = 31;         // S*V [5] when present; limiter arrays follow
+// laminar NS (DevBlock::vis0 >= 0): face gradient matrices then viscous face fluxes
+//   vis0 + 9*d + 3*r + e : grad_invT[d][r][e] at face f of direction d (stored at cell f)
+//   vis0 + 27 + 4*d + m  : viscous flux x area, momentum x/y/z (m = 0..2), energy (m = 3)
+constexpr int NVIS = 27 + 12;
 __host__ __device__ constexpr int fw(int b, int f) { return FW + 6 * b + f; }
 __host__ __device__ constexpr int ffn(int d, int c) { return FFN + 4 * d + c; }
 
@@ -97,8 +106,8 @@ struct DevBlock {
   int order;        // position of this block in the rank's id order
   int id;
   int psi0;         // first limiter slot (psi[d][pm][v] = psi0 + 10d + 5pm + v), -1: none
+  int vis0;         // first viscous slot (NVIS slots), -1: inviscid
   int ox, oy, oz;   // TMA coordinates of interior cell (0,0,0) in the arena tensor
-  int pad2_;
   long long sy, sz;
   long long fsz;    // doubles per slot
   double* base;     // arena base, pre-offset to the interior origin
@@ -137,6 +146,12 @@ struct GhostTask {
   long long buf_cells;  // field stride inside a message buffer
   double* dst_buf;      // GK_COPY into a buffer (pack)
   const double* src_buf;// GK_COPY from a buffer (unpack)
+  // round-2 unpack of a local link: fields whose pack was a view of the
+  // sender (halo.py:58, ravel of a contiguous box) are read from the sender
+  // at unpack time — bit f of live_mask (buffer field order), map below
+  int live_mask;
+  int live_block;
+  long long live_origin, live_stride[3];
   const double* dirichlet;   // GK_BC mms: [layer][6][tn0*tn1]
 };
 
@@ -152,7 +167,7 @@ struct GhostArgs {
   int ntasks;
   int cur;              // W buffer being filled
   int t_derived;        // interior T is p/(rho R) (after the first update)
-  int pad_;
+  int extended;         // GK_BC: ghost round 2 (tangential range widened, solver.py:285-305)
   long long total_items;
   Consts c;
 };
@@ -177,6 +192,23 @@ struct PushRule {
   double* dst;           // COPY: destination block (interior origin); PACK: send buffer
 };
 
+// Viscous face-flux launch: one task per (block, direction), faces f = 0..N_d
+// over the interior tangential range (e[d] = N_d + 1).
+struct ViscTask {
+  int block, d;
+  int e[3];
+  int pad_;
+  long long items;
+};
+struct ViscArgs {
+  const DevBlock* blocks;
+  const ViscTask* tasks;
+  const int2* map;      // CUDA block -> (task, first item), 128 items per block
+  int cur;
+  int t_derived;
+  Consts c;
+};
+
 struct StageArgs {
   const DevBlock* blocks;
   const Tile* tiles;
@@ -192,7 +224,7 @@ struct StageArgs {
   const PushRule* push_rules;   // ghost push (bf_vl.cuh), used when push != 0
   const int* push_range;        // [nblocks][6 faces][begin, end) into push_rules
   int push;
-  int pad_;
+  int t_derived;        // interior T is p/(rho R) (viscous dt reads T)
   Consts c;
 };
 

@@ -155,9 +155,24 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
 // ---------------------------------------------------------------------------
 // ghost fill / pack / unpack (one launch per stage, all blocks)
 // ---------------------------------------------------------------------------
-BF_DEV double interior_T(const double* W, long long fsz, long long o, int t_derived,
-                         const Consts& c) {
-  return t_derived ? W[4 * fsz + o] / (W[o] * c.R) : W[5 * fsz + o];
+
+// Whether the cell at offset `o` (from the interior origin) is an interior cell.
+BF_DEV bool is_interior(const DevBlock& b, long long o) {
+  const int g3 = b.ndim == 3 ? b.g : 0;
+  const long long s = o + b.g + b.sy * b.g + b.sz * g3;   // shift coords to >= 0
+  const long long k = s / b.sz, r = s - k * b.sz;
+  const long long j = r / b.sy, i = r - j * b.sy;
+  return i >= b.g && i < b.g + b.n[0] && j >= b.g && j < b.g + b.n[1] && k >= g3 &&
+         k < g3 + b.n[2];
+}
+
+// The stored T of a cell as the reference holds it: interior cells carry
+// p/(rho R) once updated (solver.py:753, not stored by the stage kernels),
+// ghost cells whatever their ghost fill wrote.
+BF_DEV double cell_T(const DevBlock& b, const double* W, long long o, int t_derived,
+                     const Consts& c) {
+  return (t_derived && is_interior(b, o)) ? W[4 * b.fsz + o] / (W[o] * c.R)
+                                          : W[5 * b.fsz + o];
 }
 
 __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
@@ -197,9 +212,19 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       val[f++] = W[2 * sb.fsz + soff];
       if (t.nfields == 6) val[f++] = W[3 * sb.fsz + soff];
       val[f++] = W[4 * sb.fsz + soff];
-      val[f++] = interior_T(W, sb.fsz, soff, a.t_derived, c);
+      val[f++] = cell_T(sb, W, soff, a.t_derived, c);
     } else {
       for (int f = 0; f < t.nfields; ++f) val[f] = t.src_buf[f * t.buf_cells + soff];
+    }
+    if (t.live_mask) {   // round-2 fields packed by reference: read them now (halo.py:58)
+      const DevBlock& lb = a.blocks[t.live_block];
+      const double* W = lb.base + (long long)fw(a.cur, 0) * lb.fsz;
+      const long long loff = t.live_origin + o0 * t.live_stride[0] + o1 * t.live_stride[1] +
+                             o2 * t.live_stride[2];
+      const int nf = t.nfields;
+      if (t.live_mask & 1) val[0] = W[loff];
+      if (t.live_mask & (1 << (nf - 2))) val[nf - 2] = W[4 * lb.fsz + loff];
+      if (t.live_mask & (1 << (nf - 1))) val[nf - 1] = cell_T(lb, W, loff, a.t_derived, c);
     }
     if (t.block >= 0) {
       const DevBlock& db = a.blocks[t.block];
@@ -248,7 +273,7 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
     const long long oi = base + st[d] * ipos(0);
     const double v0 = W[oi], v1 = W[fsz + oi], v2 = W[2 * fsz + oi], v3 = W[3 * fsz + oi],
                  v4 = W[4 * fsz + oi];
-    const double v5 = interior_T(W, fsz, oi, a.t_derived, c);
+    const double v5 = cell_T(b, W, oi, a.t_derived, c);
     for (int L = 0; L < t.depth; ++L) {
       const long long o = base + st[d] * gpos(L);
       W[o] = v0;
@@ -279,7 +304,7 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       }
       const double pg = W[4 * fsz + oi];
       W[4 * fsz + og] = pg;
-      const double ti = interior_T(W, fsz, oi, a.t_derived, c);
+      const double ti = cell_T(b, W, oi, a.t_derived, c);
       const double tg = (bc == BC_NOSLIP && c.has_tw) ? 2.0 * c.tw - ti : ti;
       W[5 * fsz + og] = tg;
       W[og] = pg / (c.R * tg);
@@ -310,6 +335,93 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       for (int f = 0; f < 6; ++f) W[f * fsz + o] = src[f * nt];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// laminar viscous face fluxes (solver.py:644-692, physics.py:312-344)
+// ---------------------------------------------------------------------------
+// mu(T): constant or Sutherland (physics.py:79-85), reference operation order
+BF_DEV double viscosity(double T, const Consts& c) {
+  if (!c.has_suth) return c.mu;
+  return c.suth_mu * pow(T / c.suth_t, 1.5) * (c.suth_t + c.suth_s) / (T + c.suth_s);
+}
+
+// One thread per face (f along d, interior tangential) of one block direction:
+// Fv x A into the block's viscous-flux slots (vis0 + 27 + 4 d + m), the stage
+// kernel subtracts them after the inviscid flux and its boundary overwrite.
+__global__ void __launch_bounds__(128) viscous_kernel(const ViscArgs a) {
+  const int2 bm = a.map[blockIdx.x];
+  const ViscTask t = a.tasks[bm.x];
+  const long long m = (long long)bm.y + threadIdx.x;
+  if (m >= t.items) return;
+  const DevBlock& b = a.blocks[t.block];
+  const Consts& c = a.c;
+  const int d = t.d;
+  const int i = (int)(m % t.e[0]);
+  const long long r = m / t.e[0];
+  const int j = (int)(r % t.e[1]), k = (int)(r / t.e[1]);
+  const long long st[3] = {1, b.sy, b.sz};
+  const long long fsz = b.fsz;
+  const long long hi = i + b.sy * (long long)j + b.sz * (long long)k;   // cell f (face f)
+  const long long lo = hi - st[d];                                      // cell f-1
+  const double* W = b.base + (long long)fw(a.cur, 0) * fsz;
+  const int ndim = b.ndim;
+  // field n of cell o: u, v, w (slots 1..3) or T (stored / derived)
+  auto val = [&](int n, long long o) {
+    return n < 3 ? W[(n + 1) * fsz + o] : cell_T(b, W, o, a.t_derived, c);
+  };
+  double dxi[4][3], avg[4];
+#pragma unroll
+  for (int n = 0; n < 4; ++n) {
+    const double wl = val(n, lo), wh = val(n, hi);
+    dxi[n][0] = dxi[n][1] = dxi[n][2] = 0.0;
+    dxi[n][d] = wh - wl;
+    for (int e = 0; e < ndim; ++e) {
+      if (e == d) continue;
+      const double plus = val(n, lo + st[e]) + val(n, hi + st[e]);
+      const double minus = val(n, lo - st[e]) + val(n, hi - st[e]);
+      dxi[n][e] = 0.25 * (plus - minus);
+    }
+    avg[n] = 0.5 * (wl + wh);
+  }
+  // physical gradients: row r = sum over e (in order) of invT[d][r][e] * dxi[e]
+  const double* M = b.base + (long long)(b.vis0 + 9 * d) * fsz + hi;
+  double gr[4][3];
+#pragma unroll
+  for (int n = 0; n < 4; ++n)
+#pragma unroll
+    for (int row = 0; row < 3; ++row) {
+      double acc = M[(3 * row + 0) * fsz] * dxi[n][0];
+      acc = acc + M[(3 * row + 1) * fsz] * dxi[n][1];
+      if (ndim == 3) acc = acc + M[(3 * row + 2) * fsz] * dxi[n][2];
+      gr[n][row] = acc;
+    }
+  const double mu = viscosity(avg[3], c);
+  const double kc = mu * c.cp / c.prandtl;
+  const double* fn = b.base + (long long)ffn(d, 0) * fsz + hi;
+  const double nx = fn[0], ny = fn[fsz], nz = fn[2 * fsz], A = fn[3 * fsz];
+  // physics.py:312-344
+  const double div = gr[0][0] + gr[1][1] + gr[2][2];
+  const double lam = -2.0 / 3.0 * mu;
+  const double txx = 2.0 * mu * gr[0][0] + lam * div;
+  const double tyy = 2.0 * mu * gr[1][1] + lam * div;
+  const double tzz = 2.0 * mu * gr[2][2] + lam * div;
+  const double txy = mu * (gr[0][1] + gr[1][0]);
+  const double txz = mu * (gr[0][2] + gr[2][0]);
+  const double tyz = mu * (gr[1][2] + gr[2][1]);
+  const double fx = nx * txx + ny * txy + nz * txz;
+  const double fy = nx * txy + ny * tyy + nz * tyz;
+  const double fz = nx * txz + ny * tyz + nz * tzz;
+  const double u = avg[0], v = avg[1], w = avg[2];
+  const double qx = u * txx + v * txy + w * txz + kc * gr[3][0];
+  const double qy = u * txy + v * tyy + w * tyz + kc * gr[3][1];
+  const double qz = u * txz + v * tyz + w * tzz + kc * gr[3][2];
+  const double fe = nx * qx + ny * qy + nz * qz;
+  double* out = b.base + (long long)(b.vis0 + 27 + 4 * d) * fsz + hi;
+  out[0] = fx * A;
+  out[fsz] = fy * A;
+  out[2 * fsz] = fz * A;
+  out[3 * fsz] = fe * A;
 }
 
 // Fixed-order per-block reduction of the per-tile partial sums.
@@ -392,7 +504,7 @@ bool vl_active(int flux, int flags) {
 
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s) {
 #if !BF_EXACT
-  if (vl_active(flux, a.flags)) return launch_vl(ndim, lim, a, s);
+  if (vl_active(flux, a.flags) && !a.c.viscous) return launch_vl(ndim, lim, a, s);
 #endif
   if (ndim == 3)
     return flux == FLUX_ROE ? launch_stage_l<3, FLUX_ROE>(lim, a, s)
@@ -411,6 +523,12 @@ int stage_tile_rows(int ndim, int lim) {
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s) {
   if (a.total_items == 0 || a.nlaunch == 0) return cudaSuccess;
   ghost_kernel<<<(unsigned)a.nlaunch, GHOST_BLOCK, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
+  if (nlaunch == 0) return cudaSuccess;
+  viscous_kernel<<<(unsigned)nlaunch, 128, 0, s>>>(a);
   return cudaGetLastError();
 }
 

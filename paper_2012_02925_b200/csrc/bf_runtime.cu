@@ -19,6 +19,7 @@
 #include <memory>
 #include <cstdlib>
 #include <array>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -28,6 +29,7 @@
 namespace bf {
 namespace bf_exact {
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s);
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
@@ -35,6 +37,7 @@ int stage_tile_rows(int ndim, int lim);
 }  // namespace bf_exact
 namespace bf_fast {
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s);
 bool vl_active(int flux, int flags);
 bool vl_push_compiled();
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
@@ -135,13 +138,15 @@ __global__ void face_normals_kernel(double* nx_slot, long long fsz, long long sy
   const long long n = (long long)e0 * e1 * e2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t % e0);
+    // e0..e2 span the padded tangential range: input index = padded index,
+    // output cell = padded index - ghost (negative = tangential ghost column)
+    const int ii = (int)(t % e0);
     const long long r = t / e0;
-    const int j = (int)(r % e1), k = (int)(r / e1);
-    const long long ii = (d == 0) ? i : i + g0;
-    const long long jj = (d == 1) ? j : j + g1;
-    const long long kk = (d == 2) ? k : k + g2;
+    const int jj = (int)(r % e1), kk = (int)(r / e1);
     const long long s = ii + (long long)in0 * (jj + (long long)in1 * kk);
+    const int i = (d == 0) ? ii : ii - g0;
+    const int j = (d == 1) ? jj : jj - g1;
+    const int k = (d == 2) ? kk : kk - g2;
     const double x = sv[s], y = sv[ncomp_stride + s], z = sv[2 * ncomp_stride + s];
     const double A =
         __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
@@ -192,15 +197,18 @@ __constant__ int kFaceCorners[3][4][3] = {
 
 // Faces f = 0..N_d of direction d over the interior tangential range: face vector,
 // then unit normal and area (solver.py:212-220) into the 4 geometry slots.
+// Tangential coverage is the padded range (ghost columns included): the
+// boundary-face normals there serve the extended (round-2) wall / farfield
+// ghosts of laminar NS runs (solver.py:310-319 reads padded _nhat).
 __global__ void metrics_faces_kernel(double* nx_slot, long long fsz, long long sy, long long sz,
                                      long long origin, NodeView nv, int ndim, int d, int e0,
-                                     int e1, int e2, int g, int gk) {
+                                     int e1, int e2, int g, int gk, int l0, int l1, int l2) {
   const long long n = (long long)e0 * e1 * e2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t % e0);
+    const int i = (int)(t % e0) + l0;
     const long long r = t / e0;
-    const int j = (int)(r % e1), k = (int)(r / e1);
+    const int j = (int)(r % e1) + l1, k = (int)(r / e1) + l2;
     const int ni = i + g, nj = j + g, nk = k + gk;   // node of the face's (0,0,0) corner
     V3 s;
     if (ndim == 3) {
@@ -324,6 +332,7 @@ struct HostPatch {
   int block, type, face;
   int box[6];
   std::vector<double> dirichlet;
+  std::vector<double> dirichlet_ext;   // round-2 (extended) MMS ghost values
 };
 
 struct HostLink {
@@ -335,6 +344,10 @@ struct HostLink {
   int peer_rank, tag;
   // remote only, filled at finalize
   long long cells = 0;
+  int order2 = -1;           // position in the round-2 unpack sequence
+  long long cells2 = 0;      // round-2 (extended) box cells
+  double* send2 = nullptr;   // round-2 message buffers (remote) / snapshot buffer (local)
+  double* recv2 = nullptr;
   int nfields = 0;
   double* send = nullptr;
   double* recv = nullptr;
@@ -412,6 +425,21 @@ struct bf_ctx {
   int n_unpack = 0;
   long long items_unpack = 0;
   std::vector<GhostTask> h_tasks_fill, h_tasks_unpack;
+  // laminar NS ghost round 2 (solver.py:777-784): pack (one launch) -> messages ->
+  // unpacks one launch per link in reference order -> extended BCs one launch per
+  // per-block patch position
+  struct GhostLaunch {
+    GhostTask* d = nullptr;
+    int2* map = nullptr;
+    int ntasks = 0, nmap = 0;
+    long long items = 0;
+  };
+  GhostLaunch r2_pack;
+  std::vector<GhostLaunch> r2_unpack, r2_bc;
+  std::set<int> visc_geometry;      // blocks given their face gradient matrices
+  ViscTask* d_visc = nullptr;        // viscous face-flux launch
+  int2* d_visc_map = nullptr;
+  int n_visc_map = 0;
   std::vector<double*> dirichlet_d;
   double* d_partial = nullptr;
   double* d_blocksum = nullptr;
@@ -482,7 +510,7 @@ int face_side(int face) { return face % 2; }
 
 // topology.py:224-257 in INTERIOR coordinates: [lo, hi) per axis.
 void halo_boxes(int face, const int box[6], const int n[3], const int ghost[3], int send[6],
-                int recv[6]) {
+                int recv[6], int round_no = 1) {
   const int ax = face_axis(face);
   const int g = ghost[ax];
   for (int a = 0; a < 3; ++a) {
@@ -498,11 +526,26 @@ void halo_boxes(int face, const int box[6], const int n[3], const int ghost[3], 
         recv[2 * a] = n[a];
         recv[2 * a + 1] = n[a] + g;
       }
-    } else {
-      send[2 * a] = recv[2 * a] = box[2 * a];
-      send[2 * a + 1] = recv[2 * a + 1] = box[2 * a + 1];
+    } else {   // round 2 widens the tangential ranges by the ghost depth (topology.py:235-257)
+      const int ext = round_no == 2 ? ghost[a] : 0;
+      send[2 * a] = recv[2 * a] = box[2 * a] - ext;
+      send[2 * a + 1] = recv[2 * a + 1] = box[2 * a + 1] + ext;
     }
   }
+}
+
+// Whether numpy's ravel(order="F") of this box of a padded Fortran array is a
+// view (the box is F-contiguous, size-1 axes ignored): halo.py:58 then packs
+// rho, p and T by reference, so a round-2 unpack reads them at unpack time.
+bool box_is_view(const int box[6], const int P[3]) {
+  long long expect = 1, stride = 1;
+  for (int a = 0; a < 3; ++a) {
+    const int e = box[2 * a + 1] - box[2 * a];
+    if (e > 1 && stride != expect) return false;
+    if (e > 1) expect *= e;
+    stride *= P[a];
+  }
+  return true;
 }
 
 // Affine map of one endpoint's unpack (halo.py:70-106): for own recv-box
@@ -952,6 +995,259 @@ int build_push(bf_ctx* ctx) {
   return BF_OK;
 }
 
+std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx);
+
+// A ghost task list as its own launch: begin offsets and the block map.
+int make_launch(bf_ctx* ctx, std::vector<GhostTask>& ts, bf_ctx::GhostLaunch& L) {
+  long long acc = 0;
+  for (auto& t : ts) {
+    t.begin = acc;
+    acc += t.items;
+  }
+  L.items = acc;
+  L.ntasks = (int)ts.size();
+  if (ts.empty()) return BF_OK;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, ts.size() * sizeof(GhostTask)));
+  CK(cudaMemcpy(p, ts.data(), ts.size() * sizeof(GhostTask), cudaMemcpyHostToDevice));
+  L.d = static_cast<GhostTask*>(p);
+  std::vector<int2> m;
+  for (size_t ti = 0; ti < ts.size(); ++ti)
+    for (long long it = 0; it < ts[ti].items; it += GHOST_BLOCK)
+      m.push_back(make_int2((int)ti, (int)it));
+  L.nmap = (int)m.size();
+  CK(cudaMalloc(&p, std::max<size_t>(m.size(), 1) * sizeof(int2)));
+  if (!m.empty()) CK(cudaMemcpy(p, m.data(), m.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  L.map = static_cast<int2*>(p);
+  return BF_OK;
+}
+
+// Laminar NS ghost round 2 (solver.py:777-784; exchange.py:495-521; halo.py):
+// every round-2 send box is packed before any unpack (snapshot), unpacks run
+// in the reference's exchange order (their widened boxes overlap at edges and
+// corners: the last writer wins), then the extended physical BCs in each
+// block's canonical patch order (later patches overwrite shared corners).
+int build_round2(bf_ctx* ctx) {
+  const int ndim = ctx->ndim;
+  const int nf = ndim == 3 ? 6 : 5;
+  std::vector<GhostTask> pack;
+  std::vector<std::pair<int, GhostTask>> unp;   // (order, task)
+  for (size_t q = 0; q < ctx->links.size(); ++q) {
+    HostLink& L = ctx->links[q];
+    const int bi = ctx->index_of[L.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    const int ghost[3] = {hb.g, hb.g, ndim == 3 ? hb.g : 0};
+    int send[6], recv[6];
+    halo_boxes(L.face, L.box, hb.n, ghost, send, recv, 2);
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = recv[2 * a + 1] - recv[2 * a];
+    int perm[3];
+    bool flip[3];
+    unpack_axes(L.face, L.amap, L.peer_face, perm, flip);
+    int P[3];   // partner send-box extents, partner axes
+    for (int a = 0; a < 3; ++a) P[perm[a]] = ext[a];
+    const bool local = (L.peer_rank == ctx->rank) && ctx->index_of.count(L.peer_block);
+    L.cells2 = (long long)ext[0] * ext[1] * ext[2];
+    int err = 0;
+    L.send2 = dalloc(ctx, (size_t)nf * std::max<long long>(L.cells2, 1), &err);
+    if (err) return err;
+    if (!local) {
+      L.recv2 = dalloc(ctx, (size_t)nf * std::max<long long>(L.cells2, 1), &err);
+      if (err) return err;
+    }
+    // pack: the SENDER's round-2 send box, i-fastest in the sender's axes
+    GhostTask pk{};
+    pk.kind = GK_COPY;
+    pk.nfields = nf;
+    pk.block = -1;
+    pk.dst_buf = L.send2;
+    pk.buf_cells = L.cells2;
+    pk.live_block = -1;
+    int sbox[6];
+    const HostBlock* sb = &hb;
+    int sbi = bi;
+    if (local) {
+      sbi = ctx->index_of[L.peer_block];
+      sb = &ctx->blocks[sbi];
+      const int pg[3] = {sb->g, sb->g, ndim == 3 ? sb->g : 0};
+      int precv[6];
+      halo_boxes(L.peer_face, L.peer_box, sb->n, pg, sbox, precv, 2);
+    } else {
+      std::memcpy(sbox, send, sizeof sbox);
+    }
+    int sext[3];
+    for (int a = 0; a < 3; ++a) sext[a] = sbox[2 * a + 1] - sbox[2 * a];
+    if (local)
+      for (int a = 0; a < 3; ++a)
+        if (sext[a] != P[a]) return fail(ctx, BF_EINVAL, "link tag %d: round-2 boxes differ", L.tag);
+    for (int a = 0; a < 3; ++a) pk.n[a] = sext[a];
+    pk.items = (long long)sext[0] * sext[1] * sext[2];
+    pk.dst_origin = 0;
+    pk.dst_stride[0] = 1;
+    pk.dst_stride[1] = sext[0];
+    pk.dst_stride[2] = (long long)sext[0] * sext[1];
+    pk.src_block = sbi;
+    pk.src_origin = sb->off(sbox[0], sbox[2], sbox[4]);
+    pk.src_stride[0] = 1;
+    pk.src_stride[1] = sb->sy;
+    pk.src_stride[2] = sb->sz;
+    if (pk.items > 0) pack.push_back(pk);
+    // unpack: buffer (partner axes, flips) -> own widened recv box
+    GhostTask t{};
+    t.kind = GK_COPY;
+    t.nfields = nf;
+    for (int a = 0; a < 3; ++a) t.n[a] = ext[a];
+    t.items = L.cells2;
+    t.block = bi;
+    t.src_block = -1;
+    t.dst_origin = hb.off(recv[0], recv[2], recv[4]);
+    const long long own_st[3] = {1, hb.sy, hb.sz};
+    for (int a = 0; a < 3; ++a) t.dst_stride[a] = own_st[a];
+    t.src_buf = local ? L.send2 : L.recv2;
+    t.buf_cells = L.cells2;
+    const long long Pst[3] = {1, P[0], (long long)P[0] * P[1]};
+    t.src_origin = 0;
+    for (int a = 0; a < 3; ++a) {
+      const long long st = Pst[perm[a]];
+      if (flip[a]) {
+        t.src_origin += (long long)(ext[a] - 1) * st;
+        t.src_stride[a] = -st;
+      } else {
+        t.src_stride[a] = st;
+      }
+    }
+    t.live_block = -1;
+    t.live_mask = 0;
+    if (local && box_is_view(sbox, sb->P)) {   // rho, p, T by reference (halo.py:58)
+      // sbox is in interior coords; the view test needs padded coords (shift is harmless)
+      t.live_mask = (1 << 0) | (1 << (nf - 2)) | (1 << (nf - 1));
+      t.live_block = sbi;
+      const long long pst[3] = {1, sb->sy, sb->sz};
+      t.live_origin = sb->off(sbox[0], sbox[2], sbox[4]);
+      for (int a = 0; a < 3; ++a) {
+        const long long st = pst[perm[a]];
+        if (flip[a]) {
+          t.live_origin += (long long)(ext[a] - 1) * st;
+          t.live_stride[a] = -st;
+        } else {
+          t.live_stride[a] = st;
+        }
+      }
+    }
+    const int ord = L.order2 >= 0 ? L.order2 : (int)q;
+    // distributed engine: local entries first, then the remote ones (exchange.py:506-521)
+    if (t.items > 0) unp.push_back({(local ? 0 : 1 << 20) + ord, t});
+  }
+  int rc = make_launch(ctx, pack, ctx->r2_pack);
+  if (rc) return rc;
+  std::stable_sort(unp.begin(), unp.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  ctx->r2_unpack.clear();
+  for (auto& e : unp) {
+    std::vector<GhostTask> one{e.second};
+    bf_ctx::GhostLaunch L;
+    rc = make_launch(ctx, one, L);
+    if (rc) return rc;
+    ctx->r2_unpack.push_back(L);
+  }
+  // extended BCs: launch j = the j-th physical patch (insertion = canonical order) of
+  // every block
+  std::map<int, int> seen;
+  std::vector<std::vector<GhostTask>> levels;
+  for (const HostPatch& hp : ctx->patches) {
+    const int bi = ctx->index_of[hp.block];
+    const HostBlock& hb = ctx->blocks[bi];
+    const int j = seen[bi]++;
+    if ((int)levels.size() <= j) levels.resize(j + 1);
+    GhostTask t{};
+    t.kind = GK_BC;
+    t.bc_type = hp.type;
+    t.block = bi;
+    t.src_block = -1;
+    t.axis = hp.face / 2;
+    t.side = hp.face % 2;
+    int ta = -1, tb = -1;
+    for (int a = 0; a < 3; ++a)
+      if (a != t.axis) (ta < 0 ? ta : tb) = a;
+    t.ta = ta;
+    t.tb = tb;
+    const int gg[3] = {hb.g, hb.g, ndim == 3 ? hb.g : 0};
+    t.tlo[0] = hp.box[2 * ta] - gg[ta];
+    t.tn[0] = hp.box[2 * ta + 1] - hp.box[2 * ta] + 2 * gg[ta];
+    t.tlo[1] = hp.box[2 * tb] - gg[tb];
+    t.tn[1] = hp.box[2 * tb + 1] - hp.box[2 * tb] + 2 * gg[tb];
+    t.depth = hb.g;
+    t.items = (long long)t.tn[0] * t.tn[1];
+    if (hp.type == BC_MMS) {
+      const size_t need = (size_t)t.depth * 6 * t.items;
+      if (hp.dirichlet_ext.size() != need)
+        return fail(ctx, BF_EINVAL, "mms_dirichlet patch on block %d: %zu extended values, need %zu",
+                    hp.block, hp.dirichlet_ext.size(), need);
+      void* d = nullptr;
+      CK(cudaMalloc(&d, need * sizeof(double)));
+      CK(cudaMemcpy(d, hp.dirichlet_ext.data(), need * sizeof(double), cudaMemcpyHostToDevice));
+      ctx->dirichlet_d.push_back(static_cast<double*>(d));
+      t.dirichlet = static_cast<double*>(d);
+    }
+    if (t.items > 0) levels[j].push_back(t);
+  }
+  ctx->r2_bc.clear();
+  for (auto& lv : levels) {
+    bf_ctx::GhostLaunch L;
+    rc = make_launch(ctx, lv, L);
+    if (rc) return rc;
+    ctx->r2_bc.push_back(L);
+  }
+  return BF_OK;
+}
+
+// One of the round-2 launches on ctx->stream.
+int run_ghost_launch(bf_ctx* ctx, const bf_ctx::GhostLaunch& L, int extended) {
+  if (L.ntasks == 0 || L.nmap == 0) return BF_OK;
+  GhostArgs g{};
+  g.blocks = ctx->d_blocks;
+  g.tasks = L.d;
+  g.block_map = L.map;
+  g.nlaunch = L.nmap;
+  g.ntasks = L.ntasks;
+  g.total_items = L.items;
+  g.cur = ctx->cur;
+  g.t_derived = ctx->t_derived;
+  g.extended = extended;
+  g.c = ctx->c;
+  CK(ghost_fn(ctx)(g, ctx->stream));
+  return BF_OK;
+}
+
+// Round 2 of a ghost update: packs, remote messages, ordered unpacks, extended BCs.
+int ghosts_round2(bf_ctx* ctx) {
+  int rc = run_ghost_launch(ctx, ctx->r2_pack, 0);
+  if (rc) return rc;
+  bool remote = false;
+  for (auto& L : ctx->links)
+    if (L.recv2) remote = true;
+  if (remote) {
+    if (!ctx->comm)
+      return fail(ctx, BF_EINVAL, "rank %d has remote links but no communicator", ctx->rank);
+    NK(nccl().GroupStart());
+    for (HostLink* L : remote_links_sorted(ctx)) {
+      const size_t cnt = (size_t)L->nfields * L->cells2;
+      NK(nccl().Send(L->send2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+      NK(nccl().Recv(L->recv2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    }
+    NK(nccl().GroupEnd());
+  }
+  for (auto& L : ctx->r2_unpack) {
+    rc = run_ghost_launch(ctx, L, 0);
+    if (rc) return rc;
+  }
+  for (auto& L : ctx->r2_bc) {
+    rc = run_ghost_launch(ctx, L, 1);
+    if (rc) return rc;
+  }
+  return BF_OK;
+}
+
 // One 4-D tensor map per (block, box shape) over the block arena:
 // dims (pitch, P1, P2, field slot), strides (sy, sz, fsz) doubles.  Box shapes
 // follow the stage kernel's tile (bf_stage.cuh): the 5-variable haloed plane,
@@ -1153,7 +1449,7 @@ int fill_ghosts(bf_ctx* ctx) {
 int ghosts_solo(bf_ctx* ctx) {
   int rc = fill_ghosts(ctx);
   if (rc) return rc;
-  if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap) {
+  if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap && !ctx->sch.viscous) {
     // messages and unpack on the comm stream; the interior tiles of the next stage
     // launch run meanwhile (launch_stage_kernel waits on ev_unpacked)
     CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
@@ -1177,6 +1473,10 @@ int ghosts_solo(bf_ctx* ctx) {
     rc = nccl_exchange(ctx);
     if (rc) return rc;
     rc = launch_unpack(ctx);
+    if (rc) return rc;
+  }
+  if (ctx->sch.viscous) {   // edge / corner completion (solver.py:781-784)
+    rc = ghosts_round2(ctx);
     if (rc) return rc;
   }
   ctx->ghost_buf = ctx->cur;
@@ -1214,8 +1514,22 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.err = ctx->d_err;
   a.tmaps = ctx->d_tmaps;
   a.c = ctx->c;
-  const bool vl = ctx->sch.precision != BF_PRECISION_EXACT &&
+  const bool vl = ctx->sch.precision != BF_PRECISION_EXACT && !ctx->sch.viscous &&
                   bf_fast::vl_active(ctx->sch.flux, flags);
+  a.t_derived = ctx->t_derived;
+  if (ctx->sch.viscous) {   // Fv x A of every face from the current state (ghosts round 2)
+    ProfScope ps(ctx, 2);
+    ViscArgs va{};
+    va.blocks = ctx->d_blocks;
+    va.tasks = ctx->d_visc;
+    va.map = ctx->d_visc_map;
+    va.cur = ctx->cur;
+    va.t_derived = ctx->t_derived;
+    va.c = ctx->c;
+    auto fn = ctx->sch.precision == BF_PRECISION_EXACT ? bf_exact::launch_viscous
+                                                       : bf_fast::launch_viscous;
+    CK(fn(va, ctx->n_visc_map, ctx->stream));
+  }
   a.push = (vl && ctx->push_ok && push_enabled()) ? 1 : 0;
   a.push_rules = ctx->d_push;
   a.push_range = ctx->d_push_range;
@@ -1401,6 +1715,15 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   c.inv_gamma = 1.0 / g;
   c.inv_vlc = 1.0 / c.vl_c;
   c.kappa_m1 = scheme->kappa == -1.0;
+  c.viscous = scheme->viscous != 0;
+  c.mu = gas->mu;
+  c.prandtl = gas->prandtl > 0.0 ? gas->prandtl : 0.72;
+  c.cp = g * gas->R / (g - 1.0);                     // physics.py:75-77
+  c.has_suth = gas->has_sutherland != 0;
+  c.suth_mu = gas->sutherland[0];
+  c.suth_t = gas->sutherland[1];
+  c.suth_s = gas->sutherland[2];
+  c.visc_coeff = 2.0 * std::max(4.0 / 3.0, g / c.prandtl);   // solver.py:722
   c.tw = scheme->wall_temperature;
   c.has_tw = scheme->has_wall_temperature;
   c.eps0 = scheme->epsilon == 0.0;
@@ -1491,7 +1814,9 @@ int add_block_arena(bf_ctx* ctx, int block_id, const int dims[3], int ghost_dept
   // arena slots (bf_internal.h): W 2x6 | Q 5 | dt/V | V | face geometry 3x4 |
   // [S*V 5] | [limiters ndim x 2 x 5]
   const int psi0 = want_psi ? FSRC + (hb.has_src ? 5 : 0) : -1;
-  const int nfield = FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0);
+  const bool visc = ctx->sch.viscous != 0;
+  const int vis0 = visc ? FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0) : -1;
+  const int nfield = FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0) + (visc ? NVIS : 0);
   int err = 0;
   hb.arena = dalloc(ctx, (size_t)nfield * hb.fsz, &err);
   if (err) return err;
@@ -1507,6 +1832,7 @@ int add_block_arena(bf_ctx* ctx, int block_id, const int dims[3], int ghost_dept
   d.fsz = hb.fsz;
   d.base = hb.arena + hb.origin;
   d.psi0 = psi0;
+  d.vis0 = vis0;
   d.ox = (int)(hb.lead + hb.g);
   d.oy = hb.g;
   d.oz = hb.gk;
@@ -1531,7 +1857,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
     long long in_shape[3], ext[3];
     for (int a = 0; a < 3; ++a) {
       in_shape[a] = (a == dd) ? hb.n[a] + 1 : hb.P[a];
-      ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+      ext[a] = in_shape[a];
     }
     const long long nin = in_shape[0] * in_shape[1] * in_shape[2];
     double* tmp = nullptr;
@@ -1603,12 +1929,16 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, node_strides[0], node_strides[1],
               ndim == 3 ? node_strides[2] : 0};
   for (int dd = 0; dd < ndim; ++dd) {
-    int ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+    int ext[3], lo[3];
+    const int gg[3] = {hb.g, hb.g, hb.gk};
+    for (int a = 0; a < 3; ++a) {
+      ext[a] = (a == dd) ? hb.n[a] + 1 : hb.P[a];
+      lo[a] = (a == dd) ? 0 : -gg[a];
+    }
     const long long nout = (long long)ext[0] * ext[1] * ext[2];
-    metrics_faces_kernel<<<grid_for(nout), 256, 0, st>>>(d.f(ffn(dd, 0)) - hb.origin, hb.fsz,
-                                                          hb.sy, hb.sz, hb.origin, nv, ndim, dd,
-                                                          ext[0], ext[1], ext[2], hb.g, hb.gk);
+    metrics_faces_kernel<<<grid_for(nout), 256, 0, st>>>(
+        d.f(ffn(dd, 0)) - hb.origin, hb.fsz, hb.sy, hb.sz, hb.origin, nv, ndim, dd, ext[0], ext[1],
+        ext[2], hb.g, hb.gk, lo[0], lo[1], lo[2]);
     CK(cudaGetLastError());
   }
   unsigned long long* bad = nullptr;
@@ -1680,6 +2010,62 @@ int bf_add_bc_patch(bf_ctx* ctx, int block_id, int bc_type, int face, const int 
   return BF_OK;
 }
 
+int bf_add_bc_patch_ext(bf_ctx* ctx, int block_id, int bc_type, int face, const int box[6],
+                        const double* dirichlet, const double* dirichlet_ext) {
+  int rc = bf_add_bc_patch(ctx, block_id, bc_type, face, box, dirichlet);
+  if (rc) return rc;
+  if (bc_type == BC_MMS && dirichlet_ext) {
+    const HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
+    const int gg[3] = {hb.g, hb.g, ctx->ndim == 3 ? hb.g : 0};
+    const int ax = face / 2;
+    long long nt = 1;
+    for (int a = 0; a < 3; ++a)
+      if (a != ax) nt *= box[2 * a + 1] - box[2 * a] + 2 * gg[a];
+    ctx->patches.back().dirichlet_ext.assign(dirichlet_ext, dirichlet_ext + (size_t)hb.g * 6 * nt);
+  }
+  return BF_OK;
+}
+
+int bf_add_viscous_geometry(bf_ctx* ctx, int block_id, const double* const* grad_invT) {
+  if (!ctx) return BF_EINVAL;
+  if (!ctx->sch.viscous) return fail(ctx, BF_EINVAL, "bf_add_viscous_geometry on an inviscid ctx");
+  if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);
+  CK(cudaSetDevice(ctx->device));
+  HostBlock& hb = ctx->blocks[ctx->index_of[block_id]];
+  DevBlock& d = hb.dev;
+  cudaStream_t st = ctx->stream;
+  for (int dd = 0; dd < ctx->ndim; ++dd) {
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = (a == dd) ? hb.n[a] + 1 : hb.n[a];
+    const long long n = (long long)ext[0] * ext[1] * ext[2];
+    double* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * n, st));
+    for (int m = 0; m < 9; ++m) {
+      const double* src = grad_invT[9 * dd + m];
+      if (!src) continue;   // zero (arena is zero-initialised)
+      CK(cudaMemcpyAsync(tmp, src, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      scatter_box_kernel<<<grid_for(n), 256, 0, st>>>(d.f(d.vis0 + 9 * dd + m), hb.sy, hb.sz, 0, 0,
+                                                      0, tmp, ext[0], ext[1], ext[2]);
+      CK(cudaGetLastError());
+      ctx->bytes_h2d += (long long)sizeof(double) * n;
+    }
+    CK(cudaFreeAsync(tmp, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  ctx->visc_geometry.insert(block_id);
+  return BF_OK;
+}
+
+int bf_set_round2_order(bf_ctx* ctx, int nlinks, const int* order) {
+  if (!ctx) return BF_EINVAL;
+  if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_set_round2_order after bf_finalize");
+  if (nlinks != (int)ctx->links.size())
+    return fail(ctx, BF_EINVAL, "round-2 order for %d links, ctx has %zu", nlinks,
+                ctx->links.size());
+  for (int q = 0; q < nlinks; ++q) ctx->links[q].order2 = order[q];
+  return BF_OK;
+}
+
 int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int axis_map[6],
                 int peer_block, int peer_face, const int peer_box[6], int peer_rank, int tag) {
   if (!ctx) return BF_EINVAL;
@@ -1711,10 +2097,40 @@ int bf_finalize(bf_ctx* ctx) {
   if (!ctx) return BF_EINVAL;
   if (ctx->finalized) return BF_OK;
   CK(cudaSetDevice(ctx->device));
+  if (ctx->sch.viscous)
+    for (auto& hb : ctx->blocks)
+      if (!ctx->visc_geometry.count(hb.id))
+        return fail(ctx, BF_EINVAL, "viscous run: block %d has no bf_add_viscous_geometry", hb.id);
   int rc = build_tables(ctx);
   if (rc) return rc;
   rc = build_push(ctx);
   if (rc) return rc;
+  if (ctx->sch.viscous) {
+    rc = build_round2(ctx);
+    if (rc) return rc;
+    std::vector<ViscTask> vt;
+    std::vector<int2> vm;
+    for (size_t bi = 0; bi < ctx->blocks.size(); ++bi)
+      for (int d = 0; d < ctx->ndim; ++d) {
+        const HostBlock& hb = ctx->blocks[bi];
+        ViscTask t{};
+        t.block = (int)bi;
+        t.d = d;
+        for (int a = 0; a < 3; ++a) t.e[a] = (a == d) ? hb.n[a] + 1 : hb.n[a];
+        t.items = (long long)t.e[0] * t.e[1] * t.e[2];
+        for (long long it = 0; it < t.items; it += 128)
+          vm.push_back(make_int2((int)vt.size(), (int)it));
+        vt.push_back(t);
+      }
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(vt.size(), 1) * sizeof(ViscTask)));
+    CK(cudaMemcpy(p, vt.data(), vt.size() * sizeof(ViscTask), cudaMemcpyHostToDevice));
+    ctx->d_visc = static_cast<ViscTask*>(p);
+    CK(cudaMalloc(&p, std::max<size_t>(vm.size(), 1) * sizeof(int2)));
+    CK(cudaMemcpy(p, vm.data(), vm.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    ctx->d_visc_map = static_cast<int2*>(p);
+    ctx->n_visc_map = (int)vm.size();
+  }
   rc = build_tiles(ctx);
   if (rc) return rc;
   rc = build_tensor_maps(ctx);
@@ -2063,6 +2479,47 @@ int group_ghosts(bf_group* g) {
     }
     CK(cudaEventRecord(g->ev_unpacked[r], ctx->stream));
     ctx->ghost_buf = ctx->cur;
+  }
+  if (g->ctxs[0]->sch.viscous) {
+    // round 2 (viscous): packs everywhere, messages as peer copies, then ordered
+    // unpacks and the extended BCs on each member
+    for (int r = 0; r < n; ++r) {
+      bf_ctx* ctx = g->ctxs[r];
+      CK(cudaSetDevice(ctx->device));
+      for (int q = 0; q < n; ++q)
+        if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
+      int rc = run_ghost_launch(ctx, ctx->r2_pack, 0);
+      if (rc) return rc;
+      for (auto& L : ctx->links) {
+        if (!L.recv2) continue;
+        bf_ctx* peer = g->ctxs[L.peer_rank];
+        HostLink* match = nullptr;
+        for (auto& M : peer->links)
+          if (M.recv2 && M.tag == L.tag && M.peer_rank == ctx->rank && M.block == L.peer_block) {
+            match = &M;
+            break;
+          }
+        if (!match) return fail(ctx, BF_EINVAL, "link tag %d has no round-2 partner", L.tag);
+        CK(cudaMemcpyAsync(match->recv2, L.send2, sizeof(double) * L.nfields * L.cells2,
+                           cudaMemcpyDefault, ctx->stream));
+      }
+      CK(cudaEventRecord(g->ev_packed[r], ctx->stream));
+    }
+    for (int r = 0; r < n; ++r) {
+      bf_ctx* ctx = g->ctxs[r];
+      CK(cudaSetDevice(ctx->device));
+      for (int q = 0; q < n; ++q)
+        if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_packed[q], 0));
+      for (auto& L : ctx->r2_unpack) {
+        int rc = run_ghost_launch(ctx, L, 0);
+        if (rc) return rc;
+      }
+      for (auto& L : ctx->r2_bc) {
+        int rc = run_ghost_launch(ctx, L, 1);
+        if (rc) return rc;
+      }
+      CK(cudaEventRecord(g->ev_unpacked[r], ctx->stream));
+    }
   }
   g->first = false;
   return BF_OK;

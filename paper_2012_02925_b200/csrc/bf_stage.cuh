@@ -246,6 +246,11 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
     }
     const int ez = face_flux<FLUX, LIM>(st[0], st[1], st[2], st[3], 1, ppl, pml, ppr, pmr, 1, g[0],
                                         g[1], g[2], g[3], bk, sg, c, F);
+    if (c.viscous && col_on) {   // F - Fv (solver.py:522-524)
+      const double* fv = b.base + (long long)(b.vis0 + 27 + 8) * fsz + colofs + sz * (long long)fk;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) F[m + 1] = F[m + 1] - fv[m * fsz];
+    }
     if (ez && col_on) {
       const unsigned long long lin =
           ((unsigned long long)i * nj + j) * (unsigned long long)(nk + 1) + fk;
@@ -457,6 +462,24 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
           }
         }
         const double vol = sQ[5 * NT + tid];
+        if (c.viscous) {   // viscous spectral radius (solver.py:717-730)
+          const long long co = colofs + kofs;
+          const double* Wc = b.base + (long long)fw(a.cur, 0) * fsz;
+          const double T = a.t_derived ? p / (rho * c.R) : Wc[5 * fsz + co];
+          double mu = c.mu;
+          if (c.has_suth)
+            mu = c.suth_mu * pow(T / c.suth_t, 1.5) * (c.suth_t + c.suth_s) / (T + c.suth_s);
+          auto vterm = [&](double alo, double ahi) {
+            const double abar = 0.5 * (alo + ahi);
+            lam = lam + c.visc_coeff * (mu / rho) * abar * abar / vol;
+          };
+          vterm(sFX[3 * NFX + qx], sFX[3 * NFX + qx + 1]);
+          vterm(sFY[3 * NFY + qy], sFY[3 * NFY + qy + TI]);
+          if constexpr (NDIM == 3) {
+            const double* fz0 = b.base + (long long)ffn(2, 3) * fsz + colofs + kofs;
+            vterm(fz0[0], fz0[sz]);
+          }
+        }
 #if BF_EXACT
         dtv = c.cfl * vol / lam / vol;
 #else
@@ -488,6 +511,11 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
                                          sPX + po + 1, sPX + (PC == 2 ? 5 * NPX : 0) + po + 1,
                                          NPX, sFX[q], sFX[NFX + q], sFX[2 * NFX + q],
                                          on ? sFX[3 * NFX + q] : 0.0, bk, sg, c, F);
+      if (c.viscous && on) {
+        const double* fv = b.base + (long long)(b.vis0 + 27) * fsz + gi + sy * (long long)gj + kofs;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) F[m + 1] = F[m + 1] - fv[m * fsz];
+      }
       if (e && on) {
         const unsigned long long lin =
             ((unsigned long long)gi * nj + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +
@@ -517,6 +545,11 @@ __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
                                          sPY + po + TI, sPY + (PC == 2 ? 5 * NPY : 0) + po + TI,
                                          NPY, sFY[q], sFY[NFY + q], sFY[2 * NFY + q],
                                          on ? sFY[3 * NFY + q] : 0.0, bk, sg, c, F);
+      if (c.viscous && on) {
+        const double* fv = b.base + (long long)(b.vis0 + 27 + 4) * fsz + gi + sy * (long long)gj + kofs;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) F[m + 1] = F[m + 1] - fv[m * fsz];
+      }
       if (e && on) {
         const unsigned long long lin =
             ((unsigned long long)gi * (nj + 1) + gj) * (unsigned long long)(NDIM == 3 ? nk : 1) +

@@ -255,6 +255,64 @@ def _metrics_3d(block):
                         ghost=block.ghost)
 
 
+def face_gradient_matrix(block, metrics, d):
+    """Laminar NS face matrices of direction d (solver.py:582-642), shape
+    (3, 3, N_d+1, interior tangential): out[r, e] = (J^-1)^T where column e
+    of J is the centre-to-centre difference across the face (e = d) or the
+    mid-edge node difference along the face (e != d).  Same numpy operations
+    as the reference (incl. np.linalg.inv), so the device's viscous fluxes are
+    computed from bit-identical matrices."""
+    g, n, ndim = block.ghost, block.dims, block.ndim
+    dirs = tuple(range(ndim))
+    cen = metrics.centers
+    inner = [slice(g[a], g[a] + n[a]) for a in range(3)]
+
+    def along_d(lo, hi, arr, lead=True):
+        cut = list(inner)
+        cut[d] = slice(lo, hi)
+        return arr[(slice(None), *cut)] if lead else arr[tuple(cut)]
+
+    col = {d: along_d(g[d], g[d] + n[d] + 1, cen) - along_d(g[d] - 1, g[d] + n[d], cen)}
+    if ndim == 3:
+        xyz = tuple(block.nodes)
+    else:
+        xyz = (block.nodes[0][..., None], block.nodes[1][..., None])
+        xyz = xyz + (np.zeros_like(xyz[0]),)
+
+    def bump(cut, axis):
+        out = list(cut)
+        out[axis] = slice(cut[axis].start + 1, cut[axis].stop + 1)
+        return out
+
+    for e in dirs:
+        if e == d:
+            continue
+        base = [slice(g[a], g[a] + n[a]) for a in range(3)]
+        base[d] = slice(g[d], g[d] + n[d] + 1)
+        rest = [a for a in dirs if a not in (d, e)]
+        up = bump(base, e)
+        comps = []
+        for x in xyz:
+            if rest:
+                hi = 0.5 * (x[tuple(up)] + x[tuple(bump(up, rest[0]))])
+                lo = 0.5 * (x[tuple(base)] + x[tuple(bump(base, rest[0]))])
+            else:
+                hi, lo = x[tuple(up)], x[tuple(base)]
+            comps.append(hi - lo)
+        col[e] = np.stack(comps)
+    shape = col[d].shape[1:]
+    J = np.zeros((*shape, ndim, ndim))
+    for c, e in enumerate(dirs):
+        for r in range(ndim):
+            J[..., r, c] = col[e][r]
+    inv_t = np.linalg.inv(J).swapaxes(-1, -2)
+    out = np.zeros((3, 3, *shape))
+    for r in range(ndim):
+        for c, e in enumerate(dirs):
+            out[r, e] = inv_t[..., r, c]
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Case grids (mesh.py:433-601) and the multi-parent 2D channel of SURVEY §8d C2
 # ---------------------------------------------------------------------------

@@ -12,6 +12,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import numpy as np
+
 from .errors import ConfigError
 
 FLUXES = ("roe", "van_leer")                                  # solver.py:31
@@ -24,8 +26,7 @@ FIELD_NAMES = ("rho", "u", "v", "w", "p", "T")
 
 @dataclass(frozen=True)
 class GasModel:
-    """Perfect gas (physics.py:47-90).  Viscosity terms are carried for API
-    parity; the inviscid path never reads them."""
+    """Perfect gas with an optional viscosity law (physics.py:47-90)."""
     gamma: float = 1.4
     R: float = 287.0
     mu: float = 0.0
@@ -47,6 +48,18 @@ class GasModel:
     @property
     def cv(self) -> float:
         return self.R / (self.gamma - 1.0)
+
+    def viscosity(self, T):
+        """mu(T): constant, or Sutherland's law (physics.py:79-85)."""
+        if self.sutherland is None:
+            return self.mu if np.isscalar(T) else np.full_like(np.asarray(T, float), self.mu)
+        mu_ref, t_ref, s = self.sutherland
+        T = np.asarray(T, float)
+        return mu_ref * (T / t_ref) ** 1.5 * (t_ref + s) / (T + s)
+
+    def conductivity(self, T):
+        """k = mu cp / Pr (physics.py:87-89)."""
+        return self.viscosity(T) * self.cp / self.prandtl
 
 
 @dataclass(frozen=True)

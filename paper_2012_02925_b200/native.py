@@ -30,7 +30,9 @@ PRECISION = {"exact": 0, "fast": 1}
 
 
 class Gas(C.Structure):
-    _fields_ = [("gamma", C.c_double), ("R", C.c_double)]
+    _fields_ = [("gamma", C.c_double), ("R", C.c_double), ("mu", C.c_double),
+                ("prandtl", C.c_double), ("has_sutherland", C.c_int),
+                ("sutherland", C.c_double * 3)]
 
 
 class Freestream(C.Structure):
@@ -42,7 +44,7 @@ class Scheme(C.Structure):
                 ("kappa", C.c_double), ("rk_stages", C.c_int), ("cfl", C.c_double),
                 ("limiter_freeze_at", C.c_int), ("entropy_fix_coeff", C.c_double),
                 ("has_wall_temperature", C.c_int), ("wall_temperature", C.c_double),
-                ("precision", C.c_int)]
+                ("precision", C.c_int), ("viscous", C.c_int)]
 
 
 _P = C.c_void_p
@@ -60,6 +62,9 @@ PROTOTYPES = {
     "bf_add_block": (_I, [_P, _I, _PI, _I, _PPD, _PD, _PPD]),
     "bf_add_block_nodes": (_I, [_P, _I, _PI, _I, _PPD, _PLL, _PPD]),
     "bf_add_bc_patch": (_I, [_P, _I, _I, _I, _PI, _PD]),
+    "bf_add_bc_patch_ext": (_I, [_P, _I, _I, _I, _PI, _PD, _PD]),
+    "bf_add_viscous_geometry": (_I, [_P, _I, _PPD]),
+    "bf_set_round2_order": (_I, [_P, _I, _PI]),
     "bf_add_link": (_I, [_P, _I, _I, _PI, _PI, _I, _I, _PI, _I, _I]),
     "bf_finalize": (_I, [_P]),
     "bf_upload_fields": (_I, [_P, _I, _PPD, _PPD]),
@@ -124,7 +129,7 @@ def dptr(arr):
 
 
 def dptrs(arrays):
-    return (_PD * len(arrays))(*[dptr(a) for a in arrays])
+    return (_PD * len(arrays))(*[dptr(a) if a is not None else None for a in arrays])
 
 
 def last_error(ctx):

@@ -114,8 +114,9 @@ class _BlockSetup:
              encode_primitive(*(f[n] for n in PRIM_NAMES), self.gas.gamma)]
         return [f[n] for n in FIELD_NAMES], q
 
-    def dirichlet_values(self, spec):
-        """Cached MMS ghost values of one patch, [layer][6][tangential] (solver.py:385-401)."""
+    def dirichlet_values(self, spec, extended=False):
+        """Cached MMS ghost values of one patch, [layer][6][tangential] (solver.py:385-401);
+        extended: tangential ranges widened by the ghost depth (round 2, solver.py:285-305)."""
         g = self.block.ghost
         d = spec.axis
         n = self.block.dims[d]
@@ -125,7 +126,8 @@ class _BlockSetup:
                 tang.append(None)
             else:
                 lo, hi = spec.box[a]
-                tang.append(slice(g[a] + lo, g[a] + hi))
+                ext = g[a] if extended else 0
+                tang.append(slice(g[a] + lo - ext, g[a] + hi + ext))
         c = self.metrics.centers
         out = []
         for depth in range(self.block.ghost_depth):
@@ -144,11 +146,10 @@ class GpuContext:
     """One libbfgpu context: the children of one rank on one device."""
 
     def __init__(self, plan, child_ids, gas, config, freestream, device=0, rank=0, nranks=1,
-                 precision="auto", metrics_fn=None, setups=None):
+                 precision="auto", metrics_fn=None, setups=None, schedule=None):
         validate_scheme(config)
         precision = resolve_precision(precision, config)
-        if getattr(config, "viscous", False):
-            raise ConfigError("the device path is inviscid; laminar NS is SURVEY §8f row 1")
+        self.viscous = bool(getattr(config, "viscous", False))
         self.L = native.lib()
         self.plan = plan
         self.gas, self.config, self.fs = gas, config, freestream
@@ -164,8 +165,13 @@ class GpuContext:
             entropy_fix_coeff=float(config.entropy_fix_coeff),
             has_wall_temperature=int(config.wall_temperature is not None),
             wall_temperature=float(config.wall_temperature or 0.0),
-            precision=native.PRECISION[precision])
-        gas_s = native.Gas(gamma=float(gas.gamma), R=float(gas.R))
+            precision=native.PRECISION[precision], viscous=int(self.viscous))
+        suth = getattr(gas, "sutherland", None)
+        gas_s = native.Gas(gamma=float(gas.gamma), R=float(gas.R),
+                           mu=float(getattr(gas, "mu", 0.0)),
+                           prandtl=float(getattr(gas, "prandtl", 0.72)),
+                           has_sutherland=int(suth is not None),
+                           sutherland=(C.c_double * 3)(*(suth if suth is not None else (0, 0, 0))))
         fs_s = native.Freestream(*(float(getattr(freestream, n)) for n in FIELD_NAMES))
         t_create = time.perf_counter()
         self.ctx = self.L.bf_create(self.ndim, C.byref(gas_s), C.byref(sch), C.byref(fs_s),
@@ -205,6 +211,22 @@ class GpuContext:
             self._check(self.L.bf_add_block(self.ctx, cid, native.ints(s.block.dims),
                                             s.block.ghost_depth, native.dptrs(fv),
                                             native.dptr(vol), src))
+        if self.viscous:   # face gradient matrices (solver.py:582-642), host numpy
+            geometry, _ = _geometry()
+            for cid in self.child_ids:
+                s = self.setups[cid]
+                mats = [None] * 27
+                keep = []
+                for d in range(self.ndim):
+                    M = geometry.face_gradient_matrix(s.block, s.metrics, d)
+                    for r in range(3):
+                        for e in range(3):
+                            if r < self.ndim and e < self.ndim:
+                                arr = np.asfortranarray(M[r, e])
+                                keep.append(arr)
+                                mats[9 * d + 3 * r + e] = arr
+                self._check(self.L.bf_add_viscous_geometry(self.ctx, cid, native.dptrs(mats)))
+        added = []   # connected endpoints in bf_add_link order
         for cid in self.child_ids:
             s = self.setups[cid]
             for spec in s.specs:
@@ -213,14 +235,17 @@ class GpuContext:
                 if spec.kind == "physical":
                     if spec.bc_type not in native.BC:
                         raise bridged(ConfigError)(f"unknown physical bc type {spec.bc_type!r}")
-                    vals = None
+                    vals = vext = None
                     if spec.bc_type == "mms_dirichlet":
                         if s.solution is None:
                             raise bridged(ConfigError)("mms_dirichlet patch needs config.mms_id")
                         vals = s.dirichlet_values(spec)
-                    self._check(self.L.bf_add_bc_patch(
+                        if self.viscous:
+                            vext = s.dirichlet_values(spec, extended=True)
+                    self._check(self.L.bf_add_bc_patch_ext(
                         self.ctx, cid, native.BC[spec.bc_type], face, box,
-                        native.dptr(vals) if vals is not None else None))
+                        native.dptr(vals) if vals is not None else None,
+                        native.dptr(vext) if vext is not None else None))
                 else:
                     peer = spec.neighbor_block
                     prank = plan.child(peer).rank if nranks > 1 else rank
@@ -230,6 +255,26 @@ class GpuContext:
                         native.FACES.index(spec.neighbor_face),
                         native.ints([x for r in spec.neighbor_box for x in r]), prank,
                         int(spec.link_id)))
+                    added.append((cid, spec))
+        if self.viscous and added:
+            # round-2 unpack order = the reference's exchange sequence: the schedule's
+            # entries rank-major (solver.py:869-899); the runtime puts remote ones last
+            if schedule is None:
+                from .planning import reorder_boundaries
+                schedule = reorder_boundaries(plan)
+            seq = [(e.child, id(e.spec)) for r in sorted(schedule.per_rank)
+                   for e in schedule.per_rank[r]]
+            pos = {key: q for q, key in enumerate(seq)}
+            keyed = [(cid, spec) for cid, spec in added]
+            order = []
+            for cid, spec in keyed:
+                q = pos.get((cid, id(spec)))
+                if q is None:   # schedule built from another plan object: match by value
+                    q = next(i for i, (e) in enumerate(
+                        [e for r in sorted(schedule.per_rank) for e in schedule.per_rank[r]])
+                        if e.child == cid and e.spec == spec)
+                order.append(q)
+            self._check(self.L.bf_set_round2_order(self.ctx, len(order), native.ints(order)))
         self._finalized = False
 
     def finalize(self):
@@ -563,7 +608,8 @@ def iterate_gpu(plan, schedule, gas, config, freestream, max_steps, residual_tar
     """solver.iterate on one GPU: every child of the plan in one context, all
     connected boundaries served by device copies (solver.py:914-936)."""
     gpu = GpuContext(plan, [c.id for c in plan.children], gas, config, freestream,
-                     device=device, precision=precision, metrics_fn=metrics_fn)
+                     device=device, precision=precision, metrics_fn=metrics_fn,
+                     schedule=schedule)
     gpu.upload_initial(init)
     stepper = GpuRankStepper(gpu, config)
     history, converged = [], False
@@ -642,7 +688,7 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
         device = int(os.environ.get("LOCAL_RANK", rank)) if devices is None else devices[rank]
         gpu = GpuContext(plan, [c.id for c in plan.rank_children(rank)], gas, config, freestream,
                          device=device, rank=rank, nranks=nr, precision=precision,
-                         metrics_fn=metrics_fn)
+                         metrics_fn=metrics_fn, schedule=schedule)
         uid = bytearray(128)
         if rank == 0:
             buf = (C.c_char * 128)()
@@ -676,7 +722,7 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
     devs = list(devices) if devices is not None else [0]
     gpus = [GpuContext(plan, [c.id for c in plan.rank_children(r)], gas, config, freestream,
                        device=devs[r % len(devs)], rank=r, nranks=nr, precision=precision,
-                       metrics_fn=metrics_fn) for r in range(nr)]
+                       metrics_fn=metrics_fn, schedule=schedule) for r in range(nr)]
     for g in gpus:
         g.upload_initial(init)
     L = native.lib()

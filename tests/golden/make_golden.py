@@ -31,6 +31,15 @@ TABLES = {
     "c_annulus_2d": (0.25, 84307.0, 300.0, 5.0),
     "multiblock_box_3d": (0.8395, 315979.763, 255.556, 3.06),
     "cartesian_box": (0.3, 1.0e5, 300.0, 0.0),
+    "channel": (2.0, 1.0e5, 250.0, 0.0),
+}
+
+# laminar Navier-Stokes cases: (gas kwargs) per case name
+GAS = {
+    "ns_channel2d_noslip_tw_np3": dict(mu=0.5),
+    "ns_channel3d_noslip_np4": dict(mu=0.3),
+    "ns_mms2d_l1": dict(mu=0.01),
+    "ns_box3d_sutherland_np8": dict(sutherland=(0.05, 273.15, 110.4)),
 }
 
 # name: (grid, level, np, scheme kwargs, init, steps, farfield?)
@@ -55,10 +64,35 @@ CASES = {
                                                   mms_id="euler_2d"), "manufactured", 3),
     "inlet_eps0_kappa": ("inlet_ramp_2d", 0, 1, dict(flux="roe", limiter="none", epsilon=0.0,
                                                      cfl=0.5), "uniform", 4),
+    "ns_channel2d_noslip_tw_np3": ("channel2d", None, 3,
+                                   dict(flux="van_leer", limiter="van_albada", cfl=0.5,
+                                        viscous=True, wall_temperature=300.0), "uniform", 6),
+    "ns_channel3d_noslip_np4": ("channel3d", None, 4,
+                                dict(flux="roe", limiter="minmod", cfl=0.5, viscous=True),
+                                "perturbed", 4),
+    "ns_mms2d_l1": ("cartesian_box", 1, 2, dict(flux="roe", limiter="none", cfl=0.5,
+                                                viscous=True, mms_id="ns_2d"), "manufactured", 4),
+    "ns_box3d_sutherland_np8": ("multiblock_box_3d", 0, 8,
+                                dict(flux="van_leer", limiter="van_albada", cfl=0.6, viscous=True),
+                                "perturbed", 3),
 }
 
 
 def build_grid(name, level):
+    if name in ("channel2d", "channel3d"):
+        # duct: supersonic in/outflow in i, no-slip j_min, slip j_max (+ no-slip k_min,
+        # slip k_max in 3D); dims not multiples of the device tile
+        if name == "channel2d":
+            blk = mesh.make_cartesian_block(0, (30, 12), (0.0, 0.0), (1.5, 0.5), 2)
+            faces = [("i_min", "supersonic_inflow"), ("i_max", "supersonic_outflow"),
+                     ("j_min", "noslip_wall"), ("j_max", "slip_wall")]
+        else:
+            blk = mesh.make_cartesian_block(0, (20, 10, 8), (0.0, 0.0, 0.0), (1.5, 0.6, 0.5), 3)
+            faces = [("i_min", "supersonic_inflow"), ("i_max", "supersonic_outflow"),
+                     ("j_min", "noslip_wall"), ("j_max", "slip_wall"),
+                     ("k_min", "noslip_wall"), ("k_max", "slip_wall")]
+        specs = [mesh._physical(0, f, blk.dims, t) for f, t in faces]
+        return mesh.MultiBlockGrid(blocks=[blk], boundaries=specs)
     if name == "cube3d_8":
         blk = mesh.make_cartesian_block(0, (8, 8, 8), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 3)
         specs = [mesh._physical(0, f, blk.dims, "mms_dirichlet")
@@ -69,6 +103,7 @@ def build_grid(name, level):
 
 def freestream(name, gas, ndim):
     key = "cartesian_box" if name == "cube3d_8" else name
+    key = "channel" if name.startswith("channel") else key
     m, p, T, a = TABLES[key]
     return solver.FreestreamState.from_mach(gas, m, p, T, a, ndim)
 
@@ -89,7 +124,7 @@ def perturb(solvers, fs, gas, seed=0):
 
 def run_case(name):
     grid_name, level, npr, kw, init, steps = CASES[name]
-    gas = physics.GasModel()
+    gas = physics.GasModel(**GAS.get(name, {}))
     grid = build_grid(grid_name, level)
     plan = decomp.aggregate(grid, npr) if npr < grid.parent_count else \
         decomp.decompose(grid, npr, grid.ndim)
@@ -115,6 +150,7 @@ def run_case(name):
                 out[f"c{cid}_psi{d}_plus"] = s.psi[d][0]
                 out[f"c{cid}_psi{d}_minus"] = s.psi[d][1]
     desc = {"grid": grid_name, "level": level, "np": npr, "scheme": kw, "init": init,
+            "gas": GAS.get(name, {}),
             "steps": steps, "children": [c.id for c in plan.children],
             "numpy": np.__version__}
     out["desc"] = np.array(json.dumps(desc))
@@ -123,6 +159,6 @@ def run_case(name):
 
 
 if __name__ == "__main__":
-    for name in CASES:
+    for name in (sys.argv[1:] or CASES):
         d = run_case(name)
         print(name, d["children"])

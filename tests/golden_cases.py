@@ -19,8 +19,9 @@ TABLES = {
     "c_annulus_2d": (0.25, 84307.0, 300.0, 5.0),
     "multiblock_box_3d": (0.8395, 315979.763, 255.556, 3.06),
     "cartesian_box": (0.3, 1.0e5, 300.0, 0.0),
+    "channel": (2.0, 1.0e5, 250.0, 0.0),
 }
-FARFIELD = ("c_annulus_2d", "multiblock_box_3d")
+FARFIELD = ("c_annulus_2d", "multiblock_box_3d")   # libm pow on the path
 
 
 def names():
@@ -33,10 +34,32 @@ def load(name):
     return desc, z
 
 
+def channel(name):
+    """Same ducts as make_golden.build_grid, through this repo's mirror."""
+    from paper_2012_02925_b200.geometry import MultiBlockGrid, make_cartesian_block, physical_patch
+    if name == "channel2d":
+        blk = make_cartesian_block(0, (30, 12), (0.0, 0.0), (1.5, 0.5), 2)
+        faces = [("i_min", "supersonic_inflow"), ("i_max", "supersonic_outflow"),
+                 ("j_min", "noslip_wall"), ("j_max", "slip_wall")]
+    else:
+        blk = make_cartesian_block(0, (20, 10, 8), (0.0, 0.0, 0.0), (1.5, 0.6, 0.5), 3)
+        faces = [("i_min", "supersonic_inflow"), ("i_max", "supersonic_outflow"),
+                 ("j_min", "noslip_wall"), ("j_max", "slip_wall"),
+                 ("k_min", "noslip_wall"), ("k_max", "slip_wall")]
+    return MultiBlockGrid(blocks=[blk], boundaries=[physical_patch(0, f, blk.dims, t)
+                                                    for f, t in faces])
+
+
 def build(desc):
-    gas = GasModel()
+    gas_kw = dict(desc.get("gas", {}))
+    if "sutherland" in gas_kw:
+        gas_kw["sutherland"] = tuple(gas_kw["sutherland"])
+    gas = GasModel(**gas_kw)
     gname, level = desc["grid"], desc["level"]
-    if gname == "cube3d_8":
+    if gname.startswith("channel"):
+        grid = channel(gname)
+        fkey = "channel"
+    elif gname == "cube3d_8":
         grid = geometry.cartesian_box_3d(8, mms=True)
         fkey = "cartesian_box"
     else:
@@ -52,8 +75,9 @@ def build(desc):
 
 
 def bitwise_case(desc):
-    """Cases whose path avoids libm pow (no farfield patches) are bitwise."""
-    return desc["grid"] not in FARFIELD
+    """Cases whose path avoids libm pow (no farfield patches, no Sutherland law)
+    are bitwise."""
+    return desc["grid"] not in FARFIELD and "sutherland" not in desc.get("gas", {})
 
 
 def fields_of(z, cid):

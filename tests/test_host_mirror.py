@@ -118,3 +118,25 @@ def test_oracle_equals_reference_iterate_random_schemes(ref):
         for cid in r1.solvers:
             for n in ("rho", "u", "v", "w", "p", "T"):
                 np.testing.assert_array_equal(r1.solvers[cid].fields[n], r2.solvers[cid].fields[n])
+
+
+@pytest.mark.parametrize("case,level", [("c_annulus_2d", 1), ("multiblock_box_3d", 1)])
+def test_face_gradient_matrices_bitwise(ref, case, level):
+    """geometry.face_gradient_matrix (viscous setup uploaded to the device) and the
+    oracle's restatement vs BlockSolver._grad_invT (solver.py:582-642)."""
+    import oracle
+    g_ref = ref.mesh.generate_case_grid(case, level)
+    g_me = geometry.generate_case_grid(case, level)
+    gas = ref.physics.GasModel(mu=1.8e-5)
+    cfg = ref.solver.SchemeConfig(viscous=True)
+    fs = ref.solver.FreestreamState.from_mach(gas, 0.5, 1e5, 300.0, 0.0, g_ref.ndim)
+    for b1, b2 in zip(g_ref.blocks, g_me.blocks):
+        specs = g_ref.block_boundaries(b1.id)
+        s = ref.solver.BlockSolver(b1, specs, gas, cfg, fs)
+        m2 = geometry.compute_metrics(b2)
+        ob = oracle.blockflow_oracle.OracleBlock(b2, g_me.block_boundaries(b2.id), m2,
+                                                 GasModel(mu=1.8e-5), cfg, fs)
+        for d in range(b1.ndim):
+            np.testing.assert_array_equal(geometry.face_gradient_matrix(b2, m2, d),
+                                          s._grad_invT[d])
+            np.testing.assert_array_equal(ob.grad_invT[d], s._grad_invT[d])
