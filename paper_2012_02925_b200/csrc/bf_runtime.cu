@@ -305,6 +305,27 @@ __global__ void encode_kernel(double* W, double* Q, long long fsz, long long n, 
   }
 }
 
+// Laminar NS keeps the reference's single-array ghost semantics: round 2 and
+// the extended BCs read edge / corner ghost cells, which in the reference still
+// hold the PREVIOUS ghost update's values, while the ping-pong buffer being
+// filled holds those of two updates ago.  Copy every ghost cell (6 fields)
+// from the other buffer before a viscous ghost update.
+__global__ void ghost_sync_kernel(double* dst, const double* src, long long fsz, long long lead,
+                                  long long sy, long long sz, int P0, int P1, int P2, int g0,
+                                  int g1, int g2, int n0, int n1, int n2) {
+  const long long n = (long long)P0 * P1 * P2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % P0);
+    const long long r = t / P0;
+    const int j = (int)(r % P1), k = (int)(r / P1);
+    const bool inner = i >= g0 && i < g0 + n0 && j >= g1 && j < g1 + n1 && k >= g2 && k < g2 + n2;
+    if (inner) continue;
+    const long long o = lead + i + sy * j + sz * k;
+    for (int f = 0; f < 6; ++f) dst[f * fsz + o] = src[f * fsz + o];
+  }
+}
+
 int grid_for(long long n) { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
 
 // One padded field as the reference holds it: interior from the current W
@@ -398,6 +419,8 @@ struct bf_ctx {
   bool split_forced = false;       // BF_SPLIT_TILES=1
   bool exchange_pending = false;   // ev_unpacked must be waited on before boundary tiles
   bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
+  long long cur_epoch = 0;         // bumped by every stage launch (buffer swap)
+  long long synced_cur = -1;       // epoch whose ghosts were synced from the other buffer
   std::vector<HostBlock> blocks;
   std::map<int, int> index_of;     // block id -> position
   std::vector<HostPatch> patches;
@@ -1219,6 +1242,18 @@ int run_ghost_launch(bf_ctx* ctx, const bf_ctx::GhostLaunch& L, int extended) {
   return BF_OK;
 }
 
+int sync_ghosts_from_other(bf_ctx* ctx) {
+  for (auto& hb : ctx->blocks) {
+    const long long np = (long long)hb.P[0] * hb.P[1] * hb.P[2];
+    ghost_sync_kernel<<<grid_for(np), 256, 0, ctx->stream>>>(
+        hb.dev.f(fw(ctx->cur, 0)) - hb.origin, hb.dev.f(fw(ctx->cur ^ 1, 0)) - hb.origin,
+        hb.fsz, hb.lead, hb.sy, hb.sz, hb.P[0], hb.P[1], hb.P[2], hb.g, hb.g,
+        ctx->ndim == 3 ? hb.g : 0, hb.n[0], hb.n[1], hb.n[2]);
+    CK(cudaGetLastError());
+  }
+  return BF_OK;
+}
+
 // Round 2 of a ghost update: packs, remote messages, ordered unpacks, extended BCs.
 int ghosts_round2(bf_ctx* ctx) {
   int rc = run_ghost_launch(ctx, ctx->r2_pack, 0);
@@ -1447,6 +1482,11 @@ int fill_ghosts(bf_ctx* ctx) {
 }
 
 int ghosts_solo(bf_ctx* ctx) {
+  if (ctx->sch.viscous && ctx->synced_cur != ctx->cur_epoch) {
+    int r0 = sync_ghosts_from_other(ctx);
+    if (r0) return r0;
+    ctx->synced_cur = ctx->cur_epoch;
+  }
   int rc = fill_ghosts(ctx);
   if (rc) return rc;
   if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap && !ctx->sch.viscous) {
@@ -1566,6 +1606,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   if (flags & (F_PSI_STORE | F_PSI_LOAD)) ctx->psi_valid = true;
   ctx->pushed = a.push != 0;
   ctx->cur ^= 1;
+  ctx->cur_epoch += 1;
   ctx->t_derived = 1;
   return BF_OK;
 }
@@ -2449,6 +2490,11 @@ int group_ghosts(bf_group* g) {
       // do not overwrite a peer's receive buffers before it consumed them
       for (int q = 0; q < n; ++q)
         if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
+    }
+    if (ctx->sch.viscous && ctx->synced_cur != ctx->cur_epoch) {
+      int r0 = sync_ghosts_from_other(ctx);
+      if (r0) return r0;
+      ctx->synced_cur = ctx->cur_epoch;
     }
     int rc = fill_ghosts(ctx);
     if (rc) return rc;
