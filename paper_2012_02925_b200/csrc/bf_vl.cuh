@@ -270,8 +270,12 @@ struct VCfg {
   static constexpr int OFX = r16(OXH + 10 * TJ);
   static constexpr int OFY = r16(OFX + 4 * NFX);
   static constexpr int OZG = r16(OFY + 4 * NFY);         // [2][4][TJ][TI] z faces (3D)
+  // 2 CTAs per SM (TJ <= 8, 3D): Q0 / dt/V are read from L2 (prefetched) instead
+  // of staged, to fit two CTAs' shared memory
+  static constexpr bool QLDG = NDIM == 3 && TJ <= 8;
+  static constexpr int MINB = QLDG ? 2 : 1;
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
-  static constexpr int OPS = r16(OQ + 6 * NT);                     // PushSmem
+  static constexpr int OPS = r16(OQ + (QLDG ? 5 * (NT / 32) : 6 * NT));   // PushSmem
   static constexpr int OBAR = r16(OPS + (int)((sizeof(PushSmem) + 7) / 8));
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
@@ -282,7 +286,7 @@ struct VCfg {
 };
 
 template <int NDIM, int LIM, bool K1, bool S0>
-__global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl_stage_kernel(const __grid_constant__ StageArgs a) {
   using K = VCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
   constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
@@ -349,10 +353,17 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
   auto issue_b = [&](int k) {        // x face geometry, Q0 (and dt/V) of plane k (phase B)
     unsigned long long* bar = bars + 4;
     const int z = (NDIM == 3) ? b.oz + k : 0;
-    mbar_expect_tx(bar, K::GXBYTES + (stage0 ? 5u : 6u) * NT * 8u);
-    tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
-    tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
-    if (!stage0) tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV, bar);
+    if constexpr (K::QLDG) {
+      mbar_expect_tx(bar, K::GXBYTES);
+      tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+      tma_prefetch4(tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ);
+      if (!stage0) tma_prefetch4(tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV);
+    } else {
+      mbar_expect_tx(bar, K::GXBYTES + (stage0 ? 5u : 6u) * NT * 8u);
+      tma_load4(sFX, tm + 1 * 128, b.ox + i0, b.oy + j0, z, ffn(0, 0), bar);
+      tma_load4(sQ, tm + 3 * 128, b.ox + i0, b.oy + j0, z, FQ, bar);
+      if (!stage0) tma_load4(sQ + 5 * NT, tm + 4 * 128, b.ox + i0, b.oy + j0, z, FDTV, bar);
+    }
   };
   auto prefetch_l2 = [&](int k) {    // geometry and Q0 of plane k into L2
     const int z = (NDIM == 3) ? b.oz + k : 0;
@@ -763,12 +774,13 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, 1) vl_stage_kernel(const 
         dtv = c.cfl * frcp(lam);
         b.base[(long long)FDTV * fsz + co] = dtv;
       } else {
-        dtv = sQ[5 * NT + tid];
+        dtv = K::QLDG ? b.base[(long long)FDTV * fsz + co] : sQ[5 * NT + tid];
       }
       const double adt = a.alpha * dtv;
       double qn[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) qn[v] = fma(-adt, R[v], sQ[v * NT + tid]);
+      for (int v = 0; v < 5; ++v)
+        qn[v] = fma(-adt, R[v], K::QLDG ? b.base[(long long)(FQ + v) * fsz + co] : sQ[v * NT + tid]);
       const double rq = frcp(qn[0]);
       const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
       const double pp = c.gm1 * fma(-0.5, fma(qn[1], uu, fma(qn[2], vv, qn[3] * ww)), qn[4]);
