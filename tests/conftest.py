@@ -32,6 +32,7 @@ def ref():
     import blockflow.physics
     import blockflow.solver
     import blockflow.topology
+    import blockflow.cli
     return blockflow
 
 
