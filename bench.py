@@ -347,7 +347,7 @@ def main():
 
 
 def gpu_kc():
-    return int(os.environ.get("BF_KC", "16"))
+    return int(os.environ.get("BF_KC", "32"))   # runtime default for the FAST Van Leer path
 
 
 def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist, setups):
