@@ -458,6 +458,7 @@ struct bf_ctx {
     long long items = 0;
   };
   GhostLaunch r2_pack;
+  std::vector<GhostLaunch> r1_bc;   // thin blocks: round-1 BCs in canonical order
   std::vector<GhostLaunch> r2_unpack, r2_bc;
   std::set<int> visc_geometry;      // blocks given their face gradient matrices
   ViscTask* d_visc = nullptr;        // viscous face-flux launch
@@ -645,6 +646,9 @@ void drain_profile(bf_ctx* ctx) {
 
 // ---- finalize helpers ---------------------------------------------------------
 
+int make_launch(bf_ctx* ctx, std::vector<GhostTask>& ts, bf_ctx::GhostLaunch& L);
+int run_ghost_launch(bf_ctx* ctx, const bf_ctx::GhostLaunch& L, int extended);
+
 int build_tables(bf_ctx* ctx) {
   const int ndim = ctx->ndim;
   // boundary-face overwrite maps (solver.py:526-580), canonical patch order
@@ -692,12 +696,25 @@ int build_tables(bf_ctx* ctx) {
     }
   }
 
-  // ghost tasks: physical patches (one item per tangential cell)
+  // ghost tasks: physical patches (one item per tangential cell).  A block thinner
+  // than the ghost depth along an axis with physical patches has BC ghosts that
+  // mirror the opposite face's ghosts, so the reference's sequential patch order
+  // matters: such contexts run the BCs after the exchange, one launch per
+  // per-block patch position (canonical order).
   std::vector<GhostTask>& fill = ctx->h_tasks_fill;
   std::vector<GhostTask>& unp = ctx->h_tasks_unpack;
   fill.clear();
   unp.clear();
-  for (int p : order) {
+  bool thin = false;
+  for (const HostPatch& hp : ctx->patches) {
+    const HostBlock& hb = ctx->blocks[ctx->index_of[hp.block]];
+    if (hb.n[hp.face / 2] < hb.g) thin = true;
+  }
+  std::vector<std::vector<GhostTask>> bc_levels;
+  std::map<int, int> bc_pos;
+  std::vector<int> canon(ctx->patches.size());
+  for (size_t p = 0; p < canon.size(); ++p) canon[p] = (int)p;
+  for (int p : (thin ? canon : order)) {
     const HostPatch& hp = ctx->patches[p];
     const int bi = ctx->index_of[hp.block];
     const HostBlock& hb = ctx->blocks[bi];
@@ -730,7 +747,20 @@ int build_tables(bf_ctx* ctx) {
       ctx->dirichlet_d.push_back(static_cast<double*>(d));
       t.dirichlet = static_cast<double*>(d);
     }
-    if (t.items > 0) fill.push_back(t);
+    if (thin) {
+      const int j = bc_pos[bi]++;
+      if ((int)bc_levels.size() <= j) bc_levels.resize(j + 1);
+      if (t.items > 0) bc_levels[j].push_back(t);
+    } else if (t.items > 0) {
+      fill.push_back(t);
+    }
+  }
+  ctx->r1_bc.clear();
+  for (auto& lv : bc_levels) {
+    bf_ctx::GhostLaunch L;
+    int rc = make_launch(ctx, lv, L);
+    if (rc) return rc;
+    ctx->r1_bc.push_back(L);
   }
 
   // connected endpoints
@@ -1482,14 +1512,15 @@ int fill_ghosts(bf_ctx* ctx) {
 }
 
 int ghosts_solo(bf_ctx* ctx) {
-  if (ctx->sch.viscous && ctx->synced_cur != ctx->cur_epoch) {
+  if ((ctx->sch.viscous || !ctx->r1_bc.empty()) && ctx->synced_cur != ctx->cur_epoch) {
     int r0 = sync_ghosts_from_other(ctx);
     if (r0) return r0;
     ctx->synced_cur = ctx->cur_epoch;
   }
   int rc = fill_ghosts(ctx);
   if (rc) return rc;
-  if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap && !ctx->sch.viscous) {
+  if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap && !ctx->sch.viscous &&
+      ctx->r1_bc.empty()) {
     // messages and unpack on the comm stream; the interior tiles of the next stage
     // launch run meanwhile (launch_stage_kernel waits on ev_unpacked)
     CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
@@ -1513,6 +1544,10 @@ int ghosts_solo(bf_ctx* ctx) {
     rc = nccl_exchange(ctx);
     if (rc) return rc;
     rc = launch_unpack(ctx);
+    if (rc) return rc;
+  }
+  for (auto& L : ctx->r1_bc) {   // thin blocks: BCs after the exchange, in order
+    rc = run_ghost_launch(ctx, L, 0);
     if (rc) return rc;
   }
   if (ctx->sch.viscous) {   // edge / corner completion (solver.py:781-784)
@@ -2495,7 +2530,7 @@ int group_ghosts(bf_group* g) {
       for (int q = 0; q < n; ++q)
         if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
     }
-    if (ctx->sch.viscous && ctx->synced_cur != ctx->cur_epoch) {
+    if ((ctx->sch.viscous || !ctx->r1_bc.empty()) && ctx->synced_cur != ctx->cur_epoch) {
       int r0 = sync_ghosts_from_other(ctx);
       if (r0) return r0;
       ctx->synced_cur = ctx->cur_epoch;
@@ -2525,6 +2560,10 @@ int group_ghosts(bf_group* g) {
       if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_packed[q], 0));
     if (ctx->n_unpack) {
       int rc = launch_unpack(ctx);
+      if (rc) return rc;
+    }
+    for (auto& L : ctx->r1_bc) {
+      int rc = run_ghost_launch(ctx, L, 0);
       if (rc) return rc;
     }
     CK(cudaEventRecord(g->ev_unpacked[r], ctx->stream));

@@ -139,3 +139,34 @@ def test_split_matches_reference_order_kernel():
             inner = a.solvers[cid].block.interior()
             scale = max(abs(getattr(fs, n)), abs(fs.u)) if n in ("u", "v", "w") else abs(getattr(fs, n))
             assert np.max(np.abs(x[inner] - y[inner])) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 3, 1), (5, 1, 4), (33, 17, 3), (3, 40, 2)])
+@pytest.mark.parametrize("precision", ["fast", "exact"])
+def test_thin_and_tiny_blocks(dims, precision):
+    """Degenerate shapes: one-cell-thick blocks (the stencil reads only ghosts
+    across them, and a wall's second ghost layer mirrors the opposite face's
+    ghost: BCs then run in the reference's patch order), partial tiles in every
+    axis, tiles thinner than the k-chunk."""
+    grid = channel_3d(dims=dims, kwall="slip_wall")
+    plan = cases.make_plan(grid, 1)
+    fs = FreestreamState.from_mach(GAS, 2.5, 50000.0, 250.0, 4.0, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.5)
+    ref, got = run_pair(plan, cfg, fs, 4, init="perturbed", precision=precision)
+    compare(ref, got, fs, bitwise=False)
+
+
+@pytest.mark.parametrize("dims", [(1, 1), (2, 5), (70, 3)])
+def test_thin_blocks_2d(dims):
+    from paper_2012_02925_b200.geometry import MultiBlockGrid, make_cartesian_block, physical_patch
+    blk = make_cartesian_block(0, dims, (0.0, 0.0), (1.0, 0.4), 2)
+    d = blk.dims
+    grid = MultiBlockGrid(blocks=[blk], boundaries=[
+        physical_patch(0, "i_min", d, "supersonic_inflow"),
+        physical_patch(0, "i_max", d, "supersonic_outflow"),
+        physical_patch(0, "j_min", d, "slip_wall"), physical_patch(0, "j_max", d, "slip_wall")])
+    plan = cases.make_plan(grid, 1)
+    fs = cases.freestream_for("inlet_ramp_2d", GAS, 2)
+    cfg = SchemeConfig(flux="van_leer", limiter="minmod", cfl=0.5)
+    ref, got = run_pair(plan, cfg, fs, 5, init="perturbed", precision="fast")
+    compare(ref, got, fs, bitwise=False)
