@@ -11,7 +11,8 @@ accounting — here the native engine's: packed, persistent, direct, deferred),
 solutions, and the same summary line.  The solve runs through
 ``run_distributed_gpu``: one process per GPU over NCCL under torchrun, else
 every rank as a context of the in-process group on the visible devices.
-Scaling studies and MMS order studies are bench.py / test territory here.
+``mms_levels`` runs the order-of-accuracy study on the device (cli.py:410-434);
+scaling studies are bench.py's (``--gpus N`` under torchrun).
 """
 
 from __future__ import annotations
@@ -268,12 +269,68 @@ def max_rel_primitive_diff(fields_a, fields_b, fs):
 
 # ---- run (cli.py:318-407) ---------------------------------------------------------
 
+def mms_solution_error(result):
+    """cli.py:447-461: RMS over blocks and cells of the primitive-variable error
+    relative to the manufactured fields (rho, u, v, p)."""
+    from . import mms
+    err2, count = 0.0, 0
+    for s in result.solvers.values():
+        sol = mms.manufactured_solution(s.config.mms_id)
+        c = s.metrics.centers
+        cut = s.block.interior()
+        x, y, z = (c[i][cut] for i in range(3))
+        for name in ("rho", "u", "v", "p"):
+            exact = sol[name](x, y, z)
+            e = (s.fields[name][cut] - exact) / np.abs(exact).max()
+            err2 += float(np.sum(e * e))
+            count += e.size
+    return float(np.sqrt(err2 / count))
+
+
+def run_mms_study(cfg, gas, stdout=sys.stdout, precision="auto", ndim=2, np_ranks=1):
+    """cli.py:410-434 on the device: converge the manufactured case on the
+    cartesian box at each size, report the L2 solution error and the observed
+    order.  ndim=3 runs the z-invariant 3D cube split over
+    `np_ranks` children.  Returns [(n, error, steps, converged)]."""
+    from .stepper import iterate_gpu
+    sizes = [int(v) for v in cfg.mms_levels.split(",")]
+    ms_id = "ns_2d" if cfg.physics == "laminar_ns" else "euler_2d"
+    fs = build_freestream(replace(cfg, case="cartesian_box"), gas, ndim)
+    scheme = replace(build_scheme(cfg), mms_id=ms_id)
+    out = []
+    for n in sizes:
+        if ndim == 2:
+            level, size = 0, 8
+            while size < n:
+                level, size = level + 2, size * 2
+            if size != n:
+                raise ConfigError(f"mms grid size {n} is not 8 * 2^k")
+            grid = geometry.generate_case_grid("cartesian_box", level)
+        else:
+            grid = geometry.cartesian_box_3d(n, mms=True)
+        plan = planning.decompose(grid, np_ranks, grid.ndim)
+        res = iterate_gpu(plan, planning.reorder_boundaries(plan), gas, scheme, fs,
+                          max_steps=cfg.max_steps, residual_target=cfg.residual_target,
+                          init="manufactured", precision=precision)
+        err = mms_solution_error(res)
+        out.append((n, err, res.steps, res.converged))
+        print(f"mms {ms_id} {n}^{ndim}: L2 error {err:.6e} ({res.steps} steps, "
+              f"converged={res.converged})", file=stdout)
+    for (na, a, _, _), (nb, b, _, _) in zip(out, out[1:]):
+        print(f"observed order {na}->{nb}: {np.log(a / b) / np.log(nb / na):.3f}", file=stdout)
+    return out
+
+
 def run(cfg, stdout=sys.stdout, precision="auto"):
     from .stepper import native_counters, run_distributed_gpu
     cfg.validate()
-    if cfg.mms_levels or cfg.scaling:
-        raise ConfigError("mms_levels / scaling studies: use bench.py and the test suite "
-                          "with the device runner")
+    if cfg.mms_levels:
+        if cfg.case != "cartesian_box":
+            raise ConfigError("mms_levels requires case = cartesian_box")
+        run_mms_study(cfg, build_gas(cfg), stdout, precision)
+        return EXIT_OK
+    if cfg.scaling:
+        raise ConfigError("scaling studies: bench.py (--gpus N under torchrun) measures them")
     check_strategy(cfg)
     os.makedirs(cfg.output_dir, exist_ok=True)
     gas = build_gas(cfg)

@@ -66,3 +66,18 @@ def test_device_run_writes_reference_artefacts(tmp_path):
     assert "ran 6 steps on np=3" in text
     # decomposed == serial bitwise (reference property, test_solver.py:489-512)
     assert "max relative primitive difference 0.000e+00" in text
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ndim,sizes,npr", [(2, "16,32,64", 1), (3, "16,32", 8)])
+def test_mms_order_of_accuracy(ndim, sizes, npr):
+    """manufactured solution converged on the device, second-order
+    solution error (2D cartesian box; z-invariant 3D cube split over 8 children)."""
+    cfg = cli.RunConfig(case="cartesian_box", flux="roe", limiter="none", cfl=0.5,
+                        max_steps=8000, residual_target=1e-7, mms_levels=sizes)
+    buf = io.StringIO()
+    out = cli.run_mms_study(cfg, cli.build_gas(cfg), buf, precision="fast", ndim=ndim,
+                            np_ranks=npr)
+    errs = [e for _, e, _, _ in out]
+    orders = [np.log(a / b) / np.log(2.0) for a, b in zip(errs, errs[1:])]
+    assert min(orders) > 1.8, buf.getvalue()
