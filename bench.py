@@ -218,6 +218,9 @@ def main():
     ap.add_argument("--precision", default="fast", choices=["fast", "exact"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4"],
+                    help="c4 (default, BASELINE configs[3]) is the bench line; c1-c3 are "
+                         "informational runs of the other BASELINE configs on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -237,7 +240,15 @@ def main():
     else:
         torch.cuda.set_device(0)
     level = args.level if args.level is not None else 15 + int(round(math.log2(world)))
-    plan, sched, gas, cfg, fs, init = build_case(level, world)
+    if args.workload == "c4":
+        plan, sched, gas, cfg, fs, init = build_case(level, world)
+    else:
+        from paper_2012_02925_b200 import cases
+        if world > 1:
+            raise SystemExit("--workload c1/c2/c3 are single-GPU informational runs")
+        plan, sched, gas, cfg, fs, init = {"c1": cases.c1_inlet, "c2": lambda: cases.c2_channel(1),
+                                           "c3": lambda: cases.c3_mms(128, 1)}[args.workload]()
+        args.skip_e2e = True
     ncells = plan.grid.total_cells()
     my_children = [c.id for c in plan.rank_children(rank)]
     my_cells = sum(plan.child(c).cell_count() for c in my_children)
@@ -322,7 +333,14 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(level, world, ncells, args.precision, gpu_kc()),
+            "config": (workload_config(level, world, ncells, args.precision, gpu_kc())
+                       if args.workload == "c4" else
+                       {"workload": {"c1": "C1 inlet ramp 2D 128x64, 1 block",
+                                     "c2": "C2 ramp channel 2D 4 x 512x256 connected blocks",
+                                     "c3": "C3 3D MMS cube 128^3 (Roe, no limiter), one block"
+                                     }[args.workload] + " (informational)",
+                        "cells": ncells, "precision": args.precision}),
+            "residual_evals_per_s": value * 1e6 * cfg.rk_stages,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
