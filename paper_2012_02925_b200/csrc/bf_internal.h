@@ -73,6 +73,7 @@ struct Consts {
   double two_over_gm1;                     // 2/(g-1)   (fast mode only)
   double vl_c;                             // 2*(g*g-1)
   double inv_gamma, inv_vlc;               // 1/gamma, 1/vl_c (fast mode only)
+  double lim_eps, lim_eps_half;            // limiter epsilon 1e-12 and 1e-12/2 (constant-bank operands)
   double tw;                               // wall temperature
   int has_tw;
   double mu, prandtl, cp;                  // viscosity law (physics.py:47-90)

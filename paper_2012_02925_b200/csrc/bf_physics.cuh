@@ -28,23 +28,38 @@ struct St {
 
 #if !BF_EXACT
 // FAST build: branch-free reciprocal / reciprocal square root.  The MUFU
-// seed (rcp/rsqrt.approx.ftz.f64, ~2^-22 relative) is refined by two Newton
-// steps to ~1 ulp; no special-case slow path (all operands here are normal,
-// positive, finite numbers; non-physical states are flagged separately).
+// seed (rcp/rsqrt.approx.ftz.f64, ~2^-22 relative) is refined by ONE
+// third-order step to ~1 ulp (residual e ~2^-22, truncation ~e^3 ~2^-66):
+//   1/x:       r + r (e + e^2),           e = 1 - x r
+//   1/sqrt(x): y + y e (1/2 + 3/8 e),     e = 1 - x y^2
+// (three and five fp64 ops, dependency depth three and four, against four and
+// seven / four and six for two Newton steps); no special-case slow path (all
+// operands here are normal, positive, finite numbers; non-physical states are
+// flagged separately).
 BF_DEV double frcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#ifdef BF_NEWTON2
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+#else
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+#endif
 }
 BF_DEV double frsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#ifdef BF_NEWTON2
   const double hx = 0.5 * x;
   y = y * fma(-hx * y, y, 1.5);
   return y * fma(-hx * y, y, 1.5);
+#else
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+#endif
 }
 BF_DEV double fsqrt(double x) {       // x * rsqrt(x), one residual correction
   const double y = frsqrt(x);

@@ -1794,6 +1794,8 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   c.vl_c = 2.0 * (g * g - 1.0);
   c.inv_gamma = 1.0 / g;
   c.inv_vlc = 1.0 / c.vl_c;
+  c.lim_eps = 1e-12;
+  c.lim_eps_half = 0.5e-12;
   c.kappa_m1 = scheme->kappa == -1.0;
   c.viscous = scheme->viscous != 0;
   c.mu = gas->mu;
