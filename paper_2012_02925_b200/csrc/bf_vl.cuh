@@ -558,6 +558,16 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
     const double* const pk = slot_of(k);
     const double* const w = pk + s0;
 
+    // boundary-face kinds of this cell's x / y faces (2 bits each: x lo, x hi,
+    // y lo, y hi), loaded ahead of the B0 barrier so phase A hides the latency
+    unsigned bfk = 0;
+    {
+      const int kz = (NDIM == 3) ? k : 0;
+      if (in_j && i == 0) bfk = b.bface[0][j + nj * kz];
+      if (in_j && i == ni - 1) bfk |= (unsigned)b.bface[1][j + nj * kz] << 2;
+      if (in_i && j == 0) bfk |= (unsigned)b.bface[2][i + ni * kz] << 4;
+      if (in_i && j == nj - 1) bfk |= (unsigned)b.bface[3][i + ni * kz] << 6;
+    }
     __syncthreads();   // B0: plane k-1 retired (its ring slot, x geometry, y halves, Q0)
     if (tid == 0) {
       fence_async_smem();
@@ -654,14 +664,14 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       }
       if (in_i && (j == 0 || j == nj - 1)) {
         if (j == 0) {   // whole face flux into the F- slot; phase B drops the F+ half
-          const int bk = b.bface[2][i + ni * (NDIM == 3 ? k : 0)];
+          const int bk = (bfk >> 4) & 3u;
           if (bk != BFACE_NONE) {
             overwrite(bk, w, w + PW, w - PW, PLANE, gl, NFY, hm);
             ylo_ovw = true;
           }
         }
         if (j == nj - 1) {   // whole face flux into the F+ slot
-          const int bk = b.bface[3][i + ni * (NDIM == 3 ? k : 0)];
+          const int bk = (bfk >> 6) & 3u;
           if (bk != BFACE_NONE) {
             overwrite(bk, w, w - PW, w + PW, PLANE, gl + TI, NFY, hp);
             yhi_ovw = true;
@@ -760,14 +770,14 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       }
       if (in_j && (i == 0 || i == ni - 1)) {
         if (i == 0) {
-          const int bk = b.bface[0][j + nj * (NDIM == 3 ? k : 0)];
+          const int bk = (bfk >> 0) & 3u;
           if (bk != BFACE_NONE) {
             overwrite(bk, w, w + 1, w - 1, PLANE, gl, NFX, flo);
             xlo_halo = false;
           }
         }
         if (i == ni - 1) {
-          const int bk = b.bface[1][j + nj * (NDIM == 3 ? k : 0)];
+          const int bk = (bfk >> 2) & 3u;
           if (bk != BFACE_NONE) {
             overwrite(bk, w, w - 1, w + 1, PLANE, gl + 1, NFX, fhi);
             xhi_halo = false;
