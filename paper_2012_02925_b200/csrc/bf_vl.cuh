@@ -315,7 +315,7 @@ struct VCfg {
   static constexpr int MINB = QLDG ? 2 : 1;
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
   static constexpr int OPS = r16(OQ + (QLDG ? 5 * (NT / 32) : 6 * NT));   // PushSmem
-  static constexpr int OBAR = r16(OPS + (int)((sizeof(PushSmem) + 7) / 8));
+  static constexpr int OBAR = r16(OPS + (BF_VL_PUSH ? (int)((sizeof(PushSmem) + 7) / 8) : 0));
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr unsigned WBYTES = 5u * PLANE * 8u;
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
     for (int q = 0; q < 5; ++q) mbar_init(bars + q, 1);
     fence_mbar_init();
   }
-  if (a.push) {   // this block's ghost-push rules -> shared memory
+  if (BF_VL_PUSH && a.push) {   // this block's ghost-push rules -> shared memory
     const int* rg = a.push_range + t.block * 12;
     const int r0 = rg[0], r1 = rg[11];
     if (tid < 12) (&sPS->range[0][0])[tid] = rg[tid] - r0;
