@@ -69,6 +69,14 @@ BF_DEV double dpos(double x) {
   return __hiloint2double(hi & m, __double2loint(x) & m);
 }
 
+// Positivity pre-filter on the high words: a double x <= 0 has hi(x) <= 0 as a
+// signed int (sign bit set, or +0); the converse only adds values below 2^-1042.
+// Integer min on the high halves keeps the common case off the fp64 pipe; the
+// exact double comparisons run only when the filter fires.
+BF_DEV bool maybe_nonpos(double a, double b, double c, double d) {
+  return min(min(__double2hiint(a), __double2hiint(b)), min(__double2hiint(c), __double2hiint(d))) <= 0;
+}
+
 template <int LIM>
 BF_DEV double vl_limiter(double a, double b) {
   if constexpr (LIM == LIM_NONE) {
@@ -490,8 +498,8 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
 #pragma unroll
     for (int v = 0; v < 5; ++v) vl_recon<LIM, K1>(wa[v], wb[v], wc[v], c, qL[v], qR[v]);
     vl_pair(qL, ghi, qR, glo, gs, c, hp, hm);
-    const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
-    if ((bL | bR)) {
+    if (maybe_nonpos(qL[0], qL[4], qR[0], qR[4])) {
+      const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
       // qL belongs to face kcell+1 (valid while kcell <= nk-1), qR to face kcell
       if (want_hp && bL && kcell <= nk - 1) face_err(2, ERR_FACE_LEFT, lin_z(i, j, kcell + 1));
       if (bR && kcell >= 0) face_err(2, ERR_FACE_RIGHT, lin_z(i, j, kcell));
@@ -633,15 +641,23 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       double q5[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
-        double qL, qR;
-        vl_recon<LIM, K1>(wh[v * PLANE - st], wh[v * PLANE], wh[v * PLANE + st], c, qL, qR);
-        q5[v] = sg > 0.0 ? qL : qR;
+        const double wm = wh[v * PLANE - st], w0 = wh[v * PLANE], wp = wh[v * PLANE + st];
+        if constexpr (K1 && LIM == LIM_VAN_ALBADA) {   // only the side this item needs
+          const double dm = w0 - wm, dp = wp - w0;
+          const double t =
+              dpos(fma(dp, dm, c.lim_eps_half)) * frcp1(fma(dp, dp, fma(dm, dm, c.lim_eps)));
+          q5[v] = fma(t, sg > 0.0 ? dm : -dp, w0);
+        } else {
+          double qL, qR;
+          vl_recon<LIM, K1>(wm, w0, wp, c, qL, qR);
+          q5[v] = sg > 0.0 ? qL : qR;
+        }
       }
       double F[5];
       vl_half(q5, g[0], g[1], g[2], g[3], sg, c, F);
 #pragma unroll
       for (int v = 0; v < 5; ++v) out[v * os] = F[v];
-      if (valid && ((q5[0] <= 0.0) | (q5[4] <= 0.0)))
+      if (valid && maybe_nonpos(q5[0], q5[4], q5[0], q5[4]) && ((q5[0] <= 0.0) | (q5[4] <= 0.0)))
         face_err(d, sg > 0.0 ? ERR_FACE_LEFT : ERR_FACE_RIGHT, lin);
     }
 
@@ -657,8 +673,8 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       const double* gl = sFY + ty * TI + tx;   // face j (low); face j+1 at gl + TI
       double hp[5], hm[5];
       vl_pair(qL, gl + TI, qR, gl, NFY, c, hp, hm);
-      const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
-      if ((bL | bR) && in_i) {
+      if (maybe_nonpos(qL[0], qL[4], qR[0], qR[4]) && in_i) {
+        const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
         if (bL && in_j) face_err(1, ERR_FACE_LEFT, lin_y(i, j + 1, k));
         if (bR && j <= nj) face_err(1, ERR_FACE_RIGHT, lin_y(i, j, k));
       }
@@ -754,8 +770,8 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       const double* gl = sFX + ty * GXW + tx;   // face i (low); face i+1 at gl + 1
       double hp[5], hm[5];
       vl_pair(qL, gl + 1, qR, gl, NFX, c, hp, hm);
-      const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
-      if ((bL | bR) && in_j) {
+      if (maybe_nonpos(qL[0], qL[4], qR[0], qR[4]) && in_j) {
+        const bool bL = (qL[0] <= 0.0) | (qL[4] <= 0.0), bR = (qR[0] <= 0.0) | (qR[4] <= 0.0);
         if (bL && in_i) face_err(0, ERR_FACE_LEFT, lin_x(i + 1, j, k));
         if (bR && i <= ni) face_err(0, ERR_FACE_RIGHT, lin_x(i, j, k));
       }
@@ -830,7 +846,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       const double rq = frcp(qn[0]);
       const double uu = qn[1] * rq, vv = qn[2] * rq, ww = qn[3] * rq;
       const double pp = c.gm1 * fma(-0.5, fma(qn[1], uu, fma(qn[2], vv, qn[3] * ww)), qn[4]);
-      if (qn[0] <= 0.0 || pp <= 0.0) {
+      if (maybe_nonpos(qn[0], pp, qn[0], pp) && (qn[0] <= 0.0 || pp <= 0.0)) {
         const unsigned long long lin =
             ((unsigned long long)i * nj + j) * (unsigned long long)nk + (NDIM == 3 ? k : 0);
         record_error(a.err, make_err_key(stage, 1, b.order, 0, 0, lin));
