@@ -157,13 +157,15 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
 // ---------------------------------------------------------------------------
 
 // Whether the cell at offset `o` (from the interior origin) is an interior cell.
+// (Padded blocks hold < 2^31 cells: 32-bit division.)
 BF_DEV bool is_interior(const DevBlock& b, long long o) {
   const int g3 = b.ndim == 3 ? b.g : 0;
-  const long long s = o + b.g + b.sy * b.g + b.sz * g3;   // shift coords to >= 0
-  const long long k = s / b.sz, r = s - k * b.sz;
-  const long long j = r / b.sy, i = r - j * b.sy;
-  return i >= b.g && i < b.g + b.n[0] && j >= b.g && j < b.g + b.n[1] && k >= g3 &&
-         k < g3 + b.n[2];
+  const unsigned s = (unsigned)(o + b.g + b.sy * b.g + b.sz * g3);   // shift coords to >= 0
+  const unsigned sz = (unsigned)b.sz, sy = (unsigned)b.sy;
+  const unsigned k = s / sz, r = s - k * sz;
+  const unsigned j = r / sy, i = r - j * sy;
+  return i >= (unsigned)b.g && i < (unsigned)(b.g + b.n[0]) && j >= (unsigned)b.g &&
+         j < (unsigned)(b.g + b.n[1]) && k >= (unsigned)g3 && k < (unsigned)(g3 + b.n[2]);
 }
 
 // The stored T of a cell as the reference holds it: interior cells carry
@@ -174,6 +176,12 @@ BF_DEV double cell_T(const DevBlock& b, const double* W, long long o, int t_deri
   return (t_derived && is_interior(b, o)) ? W[4 * b.fsz + o] / (W[o] * c.R)
                                           : W[5 * b.fsz + o];
 }
+
+// One ghost cell's six stored values (rho u v w p T); 2D tasks carry five
+// fields (no w) in buffers, in this order (halo.py:27-32).
+struct G6 {
+  double r, u, v, w, p, T;
+};
 
 __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   // one task per CUDA block: the task record is staged in shared memory once
@@ -189,32 +197,47 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   }
   __syncthreads();
   const GhostTask& t = ts;
-  const long long m = (long long)bm.y + threadIdx.x;
-  if (m >= t.items) return;
+  // items per task < 2^31 (a few face layers of one block)
+  const unsigned m = (unsigned)bm.y + threadIdx.x;
+  if ((long long)m >= t.items) return;
   const Consts& c = a.c;
 
   if (t.kind == GK_COPY) {
-    const int o0 = (int)(m % t.n[0]);
-    const long long r = m / t.n[0];
-    const int o1 = (int)(r % t.n[1]);
-    const int o2 = (int)(r / t.n[1]);
+    const unsigned n0 = (unsigned)t.n[0], n1 = (unsigned)t.n[1];
+    const unsigned r = m / n0;
+    const long long o0 = m - r * n0;
+    const unsigned o2u = r / n1;
+    const long long o1 = r - o2u * n1, o2 = o2u;
     const long long doff = t.dst_origin + o0 * t.dst_stride[0] + o1 * t.dst_stride[1] +
                            o2 * t.dst_stride[2];
     const long long soff = t.src_origin + o0 * t.src_stride[0] + o1 * t.src_stride[1] +
                            o2 * t.src_stride[2];
-    double val[6];
+    const bool three = t.nfields == 6;
+    G6 v;
+    v.w = 0.0;
     if (t.src_block >= 0) {
       const DevBlock& sb = a.blocks[t.src_block];
       const double* W = sb.base + (long long)fw(a.cur, 0) * sb.fsz;
-      int f = 0;
-      val[f++] = W[soff];
-      val[f++] = W[sb.fsz + soff];
-      val[f++] = W[2 * sb.fsz + soff];
-      if (t.nfields == 6) val[f++] = W[3 * sb.fsz + soff];
-      val[f++] = W[4 * sb.fsz + soff];
-      val[f++] = cell_T(sb, W, soff, a.t_derived, c);
+      v.r = W[soff];
+      v.u = W[sb.fsz + soff];
+      v.v = W[2 * sb.fsz + soff];
+      if (three) v.w = W[3 * sb.fsz + soff];
+      v.p = W[4 * sb.fsz + soff];
+      v.T = cell_T(sb, W, soff, a.t_derived, c);
     } else {
-      for (int f = 0; f < t.nfields; ++f) val[f] = t.src_buf[f * t.buf_cells + soff];
+      const double* B = t.src_buf + soff;
+      const long long bs = t.buf_cells;
+      v.r = B[0];
+      v.u = B[bs];
+      v.v = B[2 * bs];
+      if (three) {
+        v.w = B[3 * bs];
+        v.p = B[4 * bs];
+        v.T = B[5 * bs];
+      } else {
+        v.p = B[3 * bs];
+        v.T = B[4 * bs];
+      }
     }
     if (t.live_mask) {   // round-2 fields packed by reference: read them now (halo.py:58)
       const DevBlock& lb = a.blocks[t.live_block];
@@ -222,22 +245,33 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       const long long loff = t.live_origin + o0 * t.live_stride[0] + o1 * t.live_stride[1] +
                              o2 * t.live_stride[2];
       const int nf = t.nfields;
-      if (t.live_mask & 1) val[0] = W[loff];
-      if (t.live_mask & (1 << (nf - 2))) val[nf - 2] = W[4 * lb.fsz + loff];
-      if (t.live_mask & (1 << (nf - 1))) val[nf - 1] = cell_T(lb, W, loff, a.t_derived, c);
+      if (t.live_mask & 1) v.r = W[loff];
+      if (t.live_mask & (1 << (nf - 2))) v.p = W[4 * lb.fsz + loff];
+      if (t.live_mask & (1 << (nf - 1))) v.T = cell_T(lb, W, loff, a.t_derived, c);
     }
     if (t.block >= 0) {
       const DevBlock& db = a.blocks[t.block];
       double* W = db.base + (long long)fw(a.cur, 0) * db.fsz;
-      int f = 0;
-      W[doff] = val[f++];
-      W[db.fsz + doff] = val[f++];
-      W[2 * db.fsz + doff] = val[f++];
-      if (t.nfields == 6) W[3 * db.fsz + doff] = val[f++];
-      W[4 * db.fsz + doff] = val[f++];
-      W[5 * db.fsz + doff] = val[f++];
+      W[doff] = v.r;
+      W[db.fsz + doff] = v.u;
+      W[2 * db.fsz + doff] = v.v;
+      if (three) W[3 * db.fsz + doff] = v.w;
+      W[4 * db.fsz + doff] = v.p;
+      W[5 * db.fsz + doff] = v.T;
     } else {
-      for (int f = 0; f < t.nfields; ++f) t.dst_buf[f * t.buf_cells + doff] = val[f];
+      double* B = t.dst_buf + doff;
+      const long long bs = t.buf_cells;
+      B[0] = v.r;
+      B[bs] = v.u;
+      B[2 * bs] = v.v;
+      if (three) {
+        B[3 * bs] = v.w;
+        B[4 * bs] = v.p;
+        B[5 * bs] = v.T;
+      } else {
+        B[3 * bs] = v.p;
+        B[4 * bs] = v.T;
+      }
     }
     return;
   }
@@ -246,14 +280,13 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   const DevBlock& b = a.blocks[t.block];
   const long long fsz = b.fsz;
   double* W = b.base + (long long)fw(a.cur, 0) * fsz;
-  const int u0 = (int)(m % t.tn[0]), u1 = (int)(m / t.tn[0]);
-  int cell[3] = {0, 0, 0};
-  cell[t.ta] = t.tlo[0] + u0;
-  cell[t.tb] = t.tlo[1] + u1;
+  const unsigned tn0 = (unsigned)t.tn[0];
+  const unsigned u1 = m / tn0, u0 = m - u1 * tn0;
+  auto stride = [&](int ax) -> long long { return ax == 0 ? 1 : (ax == 1 ? b.sy : b.sz); };
   const int d = t.axis;
-  const long long st[3] = {1, b.sy, b.sz};
-  cell[d] = 0;
-  const long long base = cell[0] + b.sy * (long long)cell[1] + b.sz * (long long)cell[2];
+  const long long sd = stride(d);
+  const long long base =
+      (long long)(t.tlo[0] + (int)u0) * stride(t.ta) + (long long)(t.tlo[1] + (int)u1) * stride(t.tb);
   const int n = b.n[d];
   // ghost position / mirror interior position of layer L (solver.py:300-304)
   auto gpos = [&](int L) { return t.side == 0 ? -1 - L : n + L; };
@@ -261,7 +294,7 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   const int bc = t.bc_type;
   if (bc == BC_INFLOW) {
     for (int L = 0; L < t.depth; ++L) {
-      const long long o = base + st[d] * gpos(L);
+      const long long o = base + sd * gpos(L);
       W[o] = c.fs_rho;
       W[fsz + o] = c.fs_u;
       W[2 * fsz + o] = c.fs_v;
@@ -270,12 +303,12 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       W[5 * fsz + o] = c.fs_T;
     }
   } else if (bc == BC_OUTFLOW) {
-    const long long oi = base + st[d] * ipos(0);
+    const long long oi = base + sd * ipos(0);
     const double v0 = W[oi], v1 = W[fsz + oi], v2 = W[2 * fsz + oi], v3 = W[3 * fsz + oi],
                  v4 = W[4 * fsz + oi];
     const double v5 = cell_T(b, W, oi, a.t_derived, c);
     for (int L = 0; L < t.depth; ++L) {
-      const long long o = base + st[d] * gpos(L);
+      const long long o = base + sd * gpos(L);
       W[o] = v0;
       W[fsz + o] = v1;
       W[2 * fsz + o] = v2;
@@ -284,13 +317,13 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       W[5 * fsz + o] = v5;
     }
   } else if (bc == BC_SLIP || bc == BC_NOSLIP) {
-    const long long fo = base + st[d] * (t.side == 0 ? 0 : n);
+    const long long fo = base + sd * (t.side == 0 ? 0 : n);
     const double sg = t.side == 0 ? -1.0 : 1.0;
     const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
     const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
     for (int L = 0; L < t.depth; ++L) {
-      const long long og = base + st[d] * gpos(L);
-      const long long oi = base + st[d] * ipos(L);
+      const long long og = base + sd * gpos(L);
+      const long long oi = base + sd * ipos(L);
       const double u = W[fsz + oi], v = W[2 * fsz + oi], w = W[3 * fsz + oi];
       if (bc == BC_SLIP) {
         const double vn = u * nx + v * ny + w * nz;
@@ -310,16 +343,16 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
       W[og] = pg / (c.R * tg);
     }
   } else if (bc == BC_FARFIELD) {
-    const long long fo = base + st[d] * (t.side == 0 ? 0 : n);
+    const long long fo = base + sd * (t.side == 0 ? 0 : n);
     const double sg = t.side == 0 ? -1.0 : 1.0;
     const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
     const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
-    const long long oi = base + st[d] * ipos(0);
+    const long long oi = base + sd * ipos(0);
     const St s{W[oi], W[fsz + oi], W[2 * fsz + oi], W[3 * fsz + oi], W[4 * fsz + oi]};
     const St q = farfield_state(s, nx, ny, nz, c);
     const double tb = q.p / (q.r * c.R);
     for (int L = 0; L < t.depth; ++L) {
-      const long long o = base + st[d] * gpos(L);
+      const long long o = base + sd * gpos(L);
       W[o] = q.r;
       W[fsz + o] = q.u;
       W[2 * fsz + o] = q.v;
@@ -330,7 +363,7 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   } else {   // mms_dirichlet: cached exact values
     const long long nt = (long long)t.tn[0] * t.tn[1];
     for (int L = 0; L < t.depth; ++L) {
-      const long long o = base + st[d] * gpos(L);
+      const long long o = base + sd * gpos(L);
       const double* src = t.dirichlet + (long long)L * 6 * nt + m;
       for (int f = 0; f < 6; ++f) W[f * fsz + o] = src[f * nt];
     }
