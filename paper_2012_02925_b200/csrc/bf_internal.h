@@ -157,8 +157,10 @@ struct GhostTask {
 };
 
 // Ghost launches are block-aligned: CUDA block b covers items
-// [block_map[b].y, +GHOST_BLOCK) of task block_map[b].x (one task per block).
+// [block_map[b].y, +GHOST_SPAN) of task block_map[b].x (one task per block).
 constexpr int GHOST_BLOCK = 128;
+constexpr int GHOST_ITEMS = 4;                       // items per thread
+constexpr int GHOST_SPAN = GHOST_BLOCK * GHOST_ITEMS;  // items per CUDA block
 
 struct GhostArgs {
   const DevBlock* blocks;

@@ -183,9 +183,90 @@ struct G6 {
   double r, u, v, w, p, T;
 };
 
+// Values of one COPY item (source cell -> destination ghost / buffer slot).
+BF_DEV void copy_load(const GhostArgs& a, const GhostTask& t, unsigned m, G6& v, long long& doff) {
+  const Consts& c = a.c;
+  const unsigned n0 = (unsigned)t.n[0], n1 = (unsigned)t.n[1];
+  const unsigned r = m / n0;
+  const long long o0 = m - r * n0;
+  const unsigned o2u = r / n1;
+  const long long o1 = r - o2u * n1, o2 = o2u;
+  doff = t.dst_origin + o0 * t.dst_stride[0] + o1 * t.dst_stride[1] + o2 * t.dst_stride[2];
+  const long long soff = t.src_origin + o0 * t.src_stride[0] + o1 * t.src_stride[1] +
+                         o2 * t.src_stride[2];
+  const bool three = t.nfields == 6;
+  v.w = 0.0;
+  if (t.src_block >= 0) {
+    const DevBlock& sb = a.blocks[t.src_block];
+    const double* W = sb.base + (long long)fw(a.cur, 0) * sb.fsz;
+    v.r = W[soff];
+    v.u = W[sb.fsz + soff];
+    v.v = W[2 * sb.fsz + soff];
+    if (three) v.w = W[3 * sb.fsz + soff];
+    v.p = W[4 * sb.fsz + soff];
+    v.T = cell_T(sb, W, soff, a.t_derived, c);
+  } else {
+    const double* B = t.src_buf + soff;
+    const long long bs = t.buf_cells;
+    v.r = B[0];
+    v.u = B[bs];
+    v.v = B[2 * bs];
+    if (three) {
+      v.w = B[3 * bs];
+      v.p = B[4 * bs];
+      v.T = B[5 * bs];
+    } else {
+      v.p = B[3 * bs];
+      v.T = B[4 * bs];
+    }
+  }
+  if (t.live_mask) {   // round-2 fields packed by reference: read them now (halo.py:58)
+    const DevBlock& lb = a.blocks[t.live_block];
+    const double* W = lb.base + (long long)fw(a.cur, 0) * lb.fsz;
+    const long long loff = t.live_origin + o0 * t.live_stride[0] + o1 * t.live_stride[1] +
+                           o2 * t.live_stride[2];
+    const int nf = t.nfields;
+    if (t.live_mask & 1) v.r = W[loff];
+    if (t.live_mask & (1 << (nf - 2))) v.p = W[4 * lb.fsz + loff];
+    if (t.live_mask & (1 << (nf - 1))) v.T = cell_T(lb, W, loff, a.t_derived, c);
+  }
+}
+
+BF_DEV void copy_store(const GhostArgs& a, const GhostTask& t, const G6& v, long long doff) {
+  const bool three = t.nfields == 6;
+  if (t.block >= 0) {
+    const DevBlock& db = a.blocks[t.block];
+    double* W = db.base + (long long)fw(a.cur, 0) * db.fsz;
+    W[doff] = v.r;
+    W[db.fsz + doff] = v.u;
+    W[2 * db.fsz + doff] = v.v;
+    if (three) W[3 * db.fsz + doff] = v.w;
+    W[4 * db.fsz + doff] = v.p;
+    W[5 * db.fsz + doff] = v.T;
+  } else {
+    double* B = t.dst_buf + doff;
+    const long long bs = t.buf_cells;
+    B[0] = v.r;
+    B[bs] = v.u;
+    B[2 * bs] = v.v;
+    if (three) {
+      B[3 * bs] = v.w;
+      B[4 * bs] = v.p;
+      B[5 * bs] = v.T;
+    } else {
+      B[3 * bs] = v.p;
+      B[4 * bs] = v.T;
+    }
+  }
+}
+
+BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m);
+
+// One task per CUDA block; the block covers GHOST_ITEMS x GHOST_BLOCK items of
+// it (strided by GHOST_BLOCK).  COPY items load all their values before the
+// first store (GHOST_ITEMS x 6 loads in flight per thread).
 __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
-  // one task per CUDA block: the task record is staged in shared memory once
-  __shared__ __align__(16) GhostTask ts;
+  __shared__ __align__(16) GhostTask ts;   // the task record, staged once
   const int2 bm = a.block_map[blockIdx.x];
   {
     static_assert(sizeof(GhostTask) % 8 == 0, "GhostTask words");
@@ -198,84 +279,32 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   __syncthreads();
   const GhostTask& t = ts;
   // items per task < 2^31 (a few face layers of one block)
-  const unsigned m = (unsigned)bm.y + threadIdx.x;
-  if ((long long)m >= t.items) return;
-  const Consts& c = a.c;
-
+  const unsigned m0 = (unsigned)bm.y + threadIdx.x;
+  const unsigned items = (unsigned)t.items;
   if (t.kind == GK_COPY) {
-    const unsigned n0 = (unsigned)t.n[0], n1 = (unsigned)t.n[1];
-    const unsigned r = m / n0;
-    const long long o0 = m - r * n0;
-    const unsigned o2u = r / n1;
-    const long long o1 = r - o2u * n1, o2 = o2u;
-    const long long doff = t.dst_origin + o0 * t.dst_stride[0] + o1 * t.dst_stride[1] +
-                           o2 * t.dst_stride[2];
-    const long long soff = t.src_origin + o0 * t.src_stride[0] + o1 * t.src_stride[1] +
-                           o2 * t.src_stride[2];
-    const bool three = t.nfields == 6;
-    G6 v;
-    v.w = 0.0;
-    if (t.src_block >= 0) {
-      const DevBlock& sb = a.blocks[t.src_block];
-      const double* W = sb.base + (long long)fw(a.cur, 0) * sb.fsz;
-      v.r = W[soff];
-      v.u = W[sb.fsz + soff];
-      v.v = W[2 * sb.fsz + soff];
-      if (three) v.w = W[3 * sb.fsz + soff];
-      v.p = W[4 * sb.fsz + soff];
-      v.T = cell_T(sb, W, soff, a.t_derived, c);
-    } else {
-      const double* B = t.src_buf + soff;
-      const long long bs = t.buf_cells;
-      v.r = B[0];
-      v.u = B[bs];
-      v.v = B[2 * bs];
-      if (three) {
-        v.w = B[3 * bs];
-        v.p = B[4 * bs];
-        v.T = B[5 * bs];
-      } else {
-        v.p = B[3 * bs];
-        v.T = B[4 * bs];
-      }
+    G6 v[GHOST_ITEMS];
+    long long doff[GHOST_ITEMS];
+#pragma unroll
+    for (int q = 0; q < GHOST_ITEMS; ++q) {
+      const unsigned m = m0 + q * GHOST_BLOCK;
+      if (m < items) copy_load(a, t, m, v[q], doff[q]);
     }
-    if (t.live_mask) {   // round-2 fields packed by reference: read them now (halo.py:58)
-      const DevBlock& lb = a.blocks[t.live_block];
-      const double* W = lb.base + (long long)fw(a.cur, 0) * lb.fsz;
-      const long long loff = t.live_origin + o0 * t.live_stride[0] + o1 * t.live_stride[1] +
-                             o2 * t.live_stride[2];
-      const int nf = t.nfields;
-      if (t.live_mask & 1) v.r = W[loff];
-      if (t.live_mask & (1 << (nf - 2))) v.p = W[4 * lb.fsz + loff];
-      if (t.live_mask & (1 << (nf - 1))) v.T = cell_T(lb, W, loff, a.t_derived, c);
-    }
-    if (t.block >= 0) {
-      const DevBlock& db = a.blocks[t.block];
-      double* W = db.base + (long long)fw(a.cur, 0) * db.fsz;
-      W[doff] = v.r;
-      W[db.fsz + doff] = v.u;
-      W[2 * db.fsz + doff] = v.v;
-      if (three) W[3 * db.fsz + doff] = v.w;
-      W[4 * db.fsz + doff] = v.p;
-      W[5 * db.fsz + doff] = v.T;
-    } else {
-      double* B = t.dst_buf + doff;
-      const long long bs = t.buf_cells;
-      B[0] = v.r;
-      B[bs] = v.u;
-      B[2 * bs] = v.v;
-      if (three) {
-        B[3 * bs] = v.w;
-        B[4 * bs] = v.p;
-        B[5 * bs] = v.T;
-      } else {
-        B[3 * bs] = v.p;
-        B[4 * bs] = v.T;
-      }
+#pragma unroll
+    for (int q = 0; q < GHOST_ITEMS; ++q) {
+      const unsigned m = m0 + q * GHOST_BLOCK;
+      if (m < items) copy_store(a, t, v[q], doff[q]);
     }
     return;
   }
+#pragma unroll 1
+  for (int q = 0; q < GHOST_ITEMS; ++q) {
+    const unsigned m = m0 + q * GHOST_BLOCK;
+    if (m < items) bc_item(a, t, m);
+  }
+}
 
+BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m) {
+  const Consts& c = a.c;
   // ---- physical patch: one tangential position, all ghost layers ----------
   const DevBlock& b = a.blocks[t.block];
   const long long fsz = b.fsz;

@@ -872,7 +872,7 @@ int build_tables(bf_ctx* ctx) {
   auto block_map = [&](const std::vector<GhostTask>& ts, int2** dst, int* n) -> int {
     std::vector<int2> m;
     for (size_t ti = 0; ti < ts.size(); ++ti)
-      for (long long it = 0; it < ts[ti].items; it += GHOST_BLOCK)
+      for (long long it = 0; it < ts[ti].items; it += GHOST_SPAN)
         m.push_back(make_int2((int)ti, (int)it));
     *n = (int)m.size();
     if (m.empty()) return BF_OK;
@@ -1066,7 +1066,7 @@ int make_launch(bf_ctx* ctx, std::vector<GhostTask>& ts, bf_ctx::GhostLaunch& L)
   L.d = static_cast<GhostTask*>(p);
   std::vector<int2> m;
   for (size_t ti = 0; ti < ts.size(); ++ti)
-    for (long long it = 0; it < ts[ti].items; it += GHOST_BLOCK)
+    for (long long it = 0; it < ts[ti].items; it += GHOST_SPAN)
       m.push_back(make_int2((int)ti, (int)it));
   L.nmap = (int)m.size();
   CK(cudaMalloc(&p, std::max<size_t>(m.size(), 1) * sizeof(int2)));
