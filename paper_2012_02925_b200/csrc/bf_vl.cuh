@@ -662,6 +662,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
     }
 
     // ---- phase A2: y halves -> shared memory -------------------------------------------
+    // residual (face fluxes already times A); the y part is split as
+    //   (F+_j - F-_j) [own halves, here] + F-_{j+1} - F+_{j-1} [neighbours, phase B2]
+    double R[5];
     bool ylo_ovw = false, yhi_ovw = false;
     double lam = 0.0;   // stage 0: y and z parts of lambda of cell k
     double snd = 0.0;   // stage 0: sound speed of cell k (phases A2 and B1)
@@ -698,6 +701,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       for (int v = 0; v < 5; ++v) {
         sHP[v * NHY + (ty + 1) * TI + tx] = hp[v];
         sHM[v * NHY + ty * TI + tx] = hm[v];
+        R[v] = hp[v] - hm[v];
       }
       if (stage0 && cell_on) {
         snd = sound_speed(w[0], w[4 * PLANE], c);
@@ -710,7 +714,6 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
     }
 
     // ---- phase A3 (3D): z halves of cell k+1, z flux of face k+1 ----------------------
-    double R[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // residual (face fluxes already times A)
     if constexpr (NDIM == 3) {
       mbar_wait(bar_of(k + 2), par_of(k + 2));
       if (cell_on) {
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
         }
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          R[v] = fhi[v] - fzl[v];
+          R[v] += fhi[v] - fzl[v];
           fzl[v] = fhi[v];
           hpz[v] = hp1[v];
         }
@@ -817,9 +820,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
       for (int v = 0; v < 5; ++v) {
         const double* HP = sHP + v * NHY;
         const double* HM = sHM + v * NHY;
-        const double fyh = yhi_ovw ? HP[hi] : HP[hi] + HM[hi];
-        const double fyl = ylo_ovw ? HM[lo] : HP[lo] + HM[lo];
-        double r = R[v] + (fyh - fyl);
+        double r = R[v];
+        if (!yhi_ovw) r += HM[hi];   // overwritten faces: the whole flux is the own half
+        if (!ylo_ovw) r -= HP[lo];
         if (xlo_halo) r -= sXH[v * TJ + ty];
         if (xhi_halo) r += sXH[5 * TJ + v * TJ + ty];
         R[v] = r;
