@@ -15,7 +15,7 @@
 // are lanes of the same warp (shuffles), y neighbours go through shared
 // memory, z neighbours stay in registers while the CTA marches in k.
 // Tile-edge cells outside the tile (2*TJ in x, 2*TI in y per plane) are extra
-// half-flux items done by the first warps.
+// half-flux items done by the last warps (warp 0 issues the TMA groups).
 //
 // Per k-plane: B0 barrier | phase A: halves of plane k (x, y) and the z halves
 // of cell k+1 (own column) | AB barrier | phase B: residual, stage-0 dt and
@@ -594,8 +594,9 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
 #ifndef BF_ABLATE_HALO
 #define BF_ABLATE_HALO 0
 #endif
-    if (!BF_ABLATE_HALO && tid < K::NH) {
-      const int h = tid;
+    // tile-edge items on the LAST warps: warp 0 also issues the TMA groups
+    if (!BF_ABLATE_HALO && tid >= NT - K::NH) {
+      const int h = tid - (NT - K::NH);
       int cx, cy, st, d, fo;
       double sg;
       double g[4];
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
     }
 
     __syncthreads();   // AB: y halves and tile-edge halves of plane k complete
-    if (tid == 0) {
+    if (tid == 32) {   // (warp 1: warp 0 issued the B0 group)
       fence_async_smem();
       if (kk + 1 < kc) issue_geo_yz(k + 1);
       if (kk + 2 < kc) prefetch_l2(k + 2);
