@@ -1,3 +1,4 @@
+"""Pinned host <-> device copy bandwidth on the GPU box (the e2e transfer ceiling)."""
 import torch, time, numpy as np
 torch.cuda.init()
 n = 140_000_000 // 8 * 8
