@@ -395,6 +395,7 @@ struct HostBlock {
 struct TimerPair {
   cudaEvent_t a, b;
   int cls;
+  bool owned_by_graph = false;   // recorded by a captured step: not returned to the pool
 };
 
 }  // namespace
@@ -419,6 +420,12 @@ struct bf_ctx {
   bool split_forced = false;       // BF_SPLIT_TILES=1
   bool exchange_pending = false;   // ev_unpacked must be waited on before boundary tiles
   bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
+  // one RK step as a CUDA graph (standalone Euler ctx), per starting buffer and
+  // profiling mode; a profiled graph records its own timing events
+  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  std::vector<TimerPair> gprof[2];
+  bool capturing = false;
+  bool graph_off = false;          // BF_GRAPH=0, or a capture that did not reproduce
   long long cur_epoch = 0;         // bumped by every stage launch (buffer swap)
   long long synced_cur = -1;       // epoch whose ghosts were synced from the other buffer
   std::vector<HostBlock> blocks;
@@ -477,7 +484,7 @@ struct bf_ctx {
   int t_derived = 0;
   bool psi_valid = false;
   bool have_psi = false;
-  int kc = 16;   // k-chunk per tile (measured: 16 > 32 > 64 on C4, profiles/r01_kc_*.json)
+  int kc = 16;   // k-chunk per tile (32 for the FAST Van Leer kernel: profiles/r01_kc_*.json)
   // errors
   std::string msg;
   int e_kind = 0, e_block = -1, e_stage = 0, e_dir = 0;
@@ -619,13 +626,18 @@ struct ProfScope {
   ProfScope(bf_ctx* c, int k) : ctx(c), cls(k) {
     if (ctx->profiling) {
       a = take_event(ctx);
-      cudaEventRecord(a, ctx->stream);
+      record(a);
     }
+  }
+  // inside a step capture the records become event nodes of the graph
+  void record(cudaEvent_t e) {
+    cudaEventRecordWithFlags(e, ctx->stream,
+                             ctx->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
   ~ProfScope() {
     if (ctx->profiling) {
       cudaEvent_t b = take_event(ctx);
-      cudaEventRecord(b, ctx->stream);
+      record(b);
       ctx->pending.push_back({a, b, cls});
     }
   }
@@ -638,8 +650,10 @@ void drain_profile(bf_ctx* ctx) {
       ctx->prof_ms[p.cls] += ms;
       ctx->prof_launches[p.cls] += 1;
     }
-    ctx->event_pool.push_back(p.a);
-    ctx->event_pool.push_back(p.b);
+    if (!p.owned_by_graph) {
+      ctx->event_pool.push_back(p.a);
+      ctx->event_pool.push_back(p.b);
+    }
   }
   ctx->pending.clear();
 }
@@ -1674,13 +1688,27 @@ void decode_error(bf_ctx* ctx, unsigned long long key) {
   ctx->msg = "non-physical state";
 }
 
-// Host copy of the per-block sums and the error key after a step.
-int collect(bf_ctx* ctx, double* sumsq_out, unsigned long long* key_out) {
+// Host copy of the per-block sums and the error key after a step: the copies
+// (enqueue_collect, part of a captured step) and the host side (finish_collect).
+int enqueue_collect(bf_ctx* ctx) {
   const int nb = (int)ctx->blocks.size();
   CK(cudaMemcpyAsync(ctx->h_pinned, ctx->d_blocksum, sizeof(double) * 5 * nb,
                      cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(ctx->h_pinned + 5 * nb, ctx->d_err, sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, ctx->stream));
+  return BF_OK;
+}
+
+int finish_collect(bf_ctx* ctx, double* sumsq_out, unsigned long long* key_out);
+
+int collect(bf_ctx* ctx, double* sumsq_out, unsigned long long* key_out) {
+  int rc = enqueue_collect(ctx);
+  if (rc) return rc;
+  return finish_collect(ctx, sumsq_out, key_out);
+}
+
+int finish_collect(bf_ctx* ctx, double* sumsq_out, unsigned long long* key_out) {
+  const int nb = (int)ctx->blocks.size();
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->profiling) drain_profile(ctx);
   double s[5] = {0, 0, 0, 0, 0};
@@ -1751,6 +1779,7 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
              !scheme->viscous) ? 32 : 16;
   if (const char* e = std::getenv("BF_KC")) ctx->kc = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("BF_NO_OVERLAP")) ctx->no_overlap = e[0] == '1';
+  if (const char* e = std::getenv("BF_GRAPH")) ctx->graph_off = e[0] == '0';
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
                                                                         cudaStreamNonBlocking) !=
                                                   cudaSuccess) {
@@ -1817,6 +1846,14 @@ void bf_destroy(bf_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (auto& row : ctx->gexec)
+    for (auto& ex : row)
+      if (ex) cudaGraphExecDestroy(ex);
+  for (auto& v : ctx->gprof)
+    for (auto& p : v) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
   {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
@@ -2295,9 +2332,9 @@ int bf_update_ghosts(bf_ctx* ctx) {
   return BF_OK;
 }
 
-int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_out) {
-  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_step before bf_finalize");
-  CK(cudaSetDevice(ctx->device));
+// The device work of one RK step (solver.py:786-814) on ctx->stream, up to the
+// copies of its residual sums and error key.
+int enqueue_step(bf_ctx* ctx, int step_index) {
   const int nst = ctx->sch.rk_stages;
   int rc = reset_error(ctx);
   if (rc) return rc;
@@ -2307,9 +2344,115 @@ int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_ou
     rc = launch_stage_kernel(ctx, k, stage_flags(ctx, step_index, k, nst), rk_alpha(nst, k));
     if (rc) return rc;
   }
+  return enqueue_collect(ctx);
+}
+
+// Host-side sequencing state a step advances (buffer parity, epochs).
+struct StepState {
+  int cur, ghost_buf, t_derived;
+  long long cur_epoch;
+  bool pushed, psi_valid, other_filled, exchange_pending;
+  bool operator==(const StepState& o) const {
+    return cur == o.cur && ghost_buf == o.ghost_buf && t_derived == o.t_derived &&
+           cur_epoch == o.cur_epoch && pushed == o.pushed && psi_valid == o.psi_valid &&
+           other_filled == o.other_filled && exchange_pending == o.exchange_pending;
+  }
+};
+StepState save_state(const bf_ctx* ctx) {
+  return {ctx->cur, ctx->ghost_buf, ctx->t_derived, ctx->cur_epoch,
+          ctx->pushed, ctx->psi_valid, ctx->other_filled, ctx->exchange_pending};
+}
+void load_state(bf_ctx* ctx, const StepState& st) {
+  ctx->cur = st.cur;
+  ctx->ghost_buf = st.ghost_buf;
+  ctx->t_derived = st.t_derived;
+  ctx->cur_epoch = st.cur_epoch;
+  ctx->pushed = st.pushed;
+  ctx->psi_valid = st.psi_valid;
+  ctx->other_filled = st.other_filled;
+  ctx->exchange_pending = st.exchange_pending;
+}
+// What a graph-eligible step does to that state: per stage, ghosts of W[cur]
+// then the buffer swap.
+StepState advanced(StepState st, int nst) {
+  for (int k = 0; k < nst; ++k) {
+    st.ghost_buf = st.cur;
+    st.cur ^= 1;
+    st.cur_epoch += 1;
+  }
+  st.t_derived = 1;
+  return st;
+}
+
+// A step is replayed from a CUDA graph when its launches are the same every
+// step: one rank, inviscid, no thin-block BC ordering, no limiter freeze, no
+// in-kernel push or forced tile split, past the first stage (T derived, both
+// buffers' constant ghosts present).
+bool graph_eligible(const bf_ctx* ctx) {
+  return !ctx->graph_off && ctx->nranks == 1 && !ctx->comm &&
+         !ctx->group && !ctx->sch.viscous && ctx->r1_bc.empty() &&
+         ctx->sch.limiter_freeze_at <= 0 && ctx->t_derived && ctx->other_filled &&
+         !ctx->pushed && !(ctx->push_ok && push_enabled()) && !ctx->split_forced &&
+         ctx->n_unpack == 0;
+}
+
+// Enqueue one step through its graph (captured on first use for this starting
+// buffer).  Returns 1 when the caller must take the plain path instead.
+int enqueue_step_graph(bf_ctx* ctx, int step_index) {
+  const int nst = ctx->sch.rk_stages;
+  const StepState before = save_state(ctx);
+  const int c0 = ctx->cur, pr = ctx->profiling ? 1 : 0;
+  if (!ctx->gexec[c0][pr]) {
+    cudaGraph_t g = nullptr;
+    const size_t npend = ctx->pending.size();
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      ctx->graph_off = true;
+      return 1;
+    }
+    ctx->capturing = true;
+    const int rc = enqueue_step(ctx, step_index);
+    ctx->capturing = false;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+    const StepState after = save_state(ctx);
+    load_state(ctx, before);
+    cudaGetLastError();
+    cudaGraphExec_t ex = nullptr;
+    const bool ok = rc == BF_OK && ce == cudaSuccess && g &&
+                    after == advanced(before, nst) &&
+                    cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    // timing events recorded during the capture belong to the graph
+    std::vector<TimerPair> captured(ctx->pending.begin() + npend, ctx->pending.end());
+    ctx->pending.resize(npend);
+    if (!ok) {
+      cudaGetLastError();
+      for (auto& p : captured) {
+        ctx->event_pool.push_back(p.a);
+        ctx->event_pool.push_back(p.b);
+      }
+      ctx->graph_off = true;
+      return 1;
+    }
+    for (auto& p : captured) p.owned_by_graph = true;
+    if (pr) ctx->gprof[c0] = captured;
+    ctx->gexec[c0][pr] = ex;
+  }
+  CK(cudaGraphLaunch(ctx->gexec[c0][pr], ctx->stream));
+  if (pr) ctx->pending.insert(ctx->pending.end(), ctx->gprof[c0].begin(), ctx->gprof[c0].end());
+  load_state(ctx, advanced(before, nst));
+  return BF_OK;
+}
+
+int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_out) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_step before bf_finalize");
+  CK(cudaSetDevice(ctx->device));
+  int rc = 1;
+  if (graph_eligible(ctx)) rc = enqueue_step_graph(ctx, step_index);
+  if (rc == 1) rc = enqueue_step(ctx, step_index);
+  if (rc) return rc;
   double s[5];
   unsigned long long key;
-  rc = collect(ctx, s, &key);
+  rc = finish_collect(ctx, s, &key);
   if (rc) return rc;
   if (ctx->comm && ctx->nranks > 1) {
     int bad = -1;
