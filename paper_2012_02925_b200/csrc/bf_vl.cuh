@@ -35,6 +35,9 @@
 #ifndef BF_VL_PUSH
 #define BF_VL_PUSH 0
 #endif
+#ifndef BF_VL2D_MINB
+#define BF_VL2D_MINB 2
+#endif
 
 BF_DEV void tma_prefetch4(const void* tmap, int x, int y, int z, int s) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
@@ -320,7 +323,8 @@ struct VCfg {
   // 2 CTAs per SM (TJ <= 8, 3D): Q0 / dt/V are read from L2 (prefetched) instead
   // of staged, to fit two CTAs' shared memory
   static constexpr bool QLDG = NDIM == 3 && TJ <= 8;
-  static constexpr int MINB = QLDG ? 2 : 1;
+  // 2D: one plane per CTA, latency-bound: several CTAs per SM (register cap)
+  static constexpr int MINB = QLDG ? 2 : (NDIM == 2 ? BF_VL2D_MINB : 1);
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
   static constexpr int OPS = r16(OQ + (QLDG ? 5 * (NT / 32) : 6 * NT));   // PushSmem
   static constexpr int OBAR = r16(OPS + (BF_VL_PUSH ? (int)((sizeof(PushSmem) + 7) / 8) : 0));
