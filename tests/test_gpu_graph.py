@@ -45,3 +45,28 @@ def test_graph_replay_matches_oracle_3d(monkeypatch):
     cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
     ref, got = run_pair(plan, cfg, fs, 6, init="perturbed", precision="fast")
     compare(ref, got, fs, bitwise=False)
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_graph_reused_after_reupload(precision):
+    """The graphs captured in a first run replay correctly after the state is
+    uploaded again (buffer parity and derived-T state reset by the upload)."""
+    from paper_2012_02925_b200 import stepper
+    plan = planning.decompose(geometry.inlet_ramp_2d(1), 2, 2)
+    fs = cases.freestream_for("inlet_ramp_2d", GAS, 2)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.5, rk_stages=1)
+    gpu = stepper.GpuContext(plan, [c.id for c in plan.children], GAS, cfg, fs,
+                             precision=precision)
+    try:
+        runs = []
+        for _ in range(2):
+            gpu.upload_initial("uniform")
+            st = stepper.GpuRankStepper(gpu, cfg)
+            hist = [st.step(k + 1)[0] for k in range(6)]
+            fields = {c.id: gpu.download(c.id, "p") for c in plan.children}
+            runs.append((np.array(hist), fields))
+        np.testing.assert_array_equal(runs[0][0], runs[1][0])
+        for cid in runs[0][1]:
+            np.testing.assert_array_equal(runs[0][1][cid], runs[1][1][cid])
+    finally:
+        gpu.close()
