@@ -1,5 +1,7 @@
 #!/bin/bash
 # A/B timing of library variants on the bench workload: tools/abl.sh name...
+# (one untimed run first: the first bench on a fresh box reads a few % slow)
+timeout 300 python bench.py --skip-cpu --skip-e2e --steps 5 > /dev/null 2>&1
 for v in "$@"; do
   lib=paper_2012_02925_b200/libbfgpu.so
   [ "$v" != "base" ] && lib=paper_2012_02925_b200/libbfgpu_$v.so
