@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <cstdlib>
 #include <array>
 #include <set>
@@ -382,7 +383,8 @@ struct HostBlock {
   long long lead = 0, sy = 0, sz = 0, origin = 0, fsz = 0;
   int nslots = 0;
   double* arena = nullptr;
-  std::vector<double*> owned;  // allocations to free
+  std::vector<double*> owned;  // allocations to free (the arena, back to the arena cache)
+  size_t arena_bytes = 0;
   DevBlock dev{};
   std::vector<unsigned char> bface_h[6];
   unsigned char* bface_d[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -588,6 +590,85 @@ void unpack_axes(int face, const int amap[6], int peer_face, int perm[3], bool f
     perm[a] = amap[2 * a];
     flip[a] = (a == ax) ? (face_side(face) == face_side(peer_face)) : (amap[2 * a + 1] < 0);
   }
+}
+
+// Process-wide cache of block arenas: bf_destroy returns a context's arenas
+// here and the next context on the same device reuses them (best fit within
+// 25%) instead of paying the driver's page mapping of multi-GB allocations
+// again.  Bounded; bf_release_cache hands everything back to the driver, and a
+// failing cudaMalloc releases the cache and retries.
+struct ArenaCache {
+  struct Entry {
+    int dev;
+    size_t bytes;
+    void* p;
+  };
+  std::mutex m;
+  std::vector<Entry> free;
+  size_t held = 0;
+};
+ArenaCache& arena_cache() {
+  static ArenaCache c;
+  return c;
+}
+constexpr size_t ARENA_CACHE_MAX = 32ull << 30;
+
+void release_arena_cache(int dev) {   // dev < 0: all devices
+  ArenaCache& c = arena_cache();
+  std::lock_guard<std::mutex> g(c.m);
+  int cur = -1;
+  cudaGetDevice(&cur);
+  std::vector<ArenaCache::Entry> keep;
+  for (auto& e : c.free) {
+    if (dev >= 0 && e.dev != dev) {
+      keep.push_back(e);
+      continue;
+    }
+    cudaSetDevice(e.dev);
+    cudaFree(e.p);
+    c.held -= e.bytes;
+  }
+  c.free.swap(keep);
+  if (cur >= 0) cudaSetDevice(cur);
+}
+
+void* arena_alloc(int dev, size_t bytes) {
+  ArenaCache& c = arena_cache();
+  {
+    std::lock_guard<std::mutex> g(c.m);
+    int best = -1;
+    for (size_t q = 0; q < c.free.size(); ++q) {
+      const auto& e = c.free[q];
+      if (e.dev == dev && e.bytes >= bytes && e.bytes - bytes <= bytes / 4 &&
+          (best < 0 || e.bytes < c.free[best].bytes))
+        best = (int)q;
+    }
+    if (best >= 0) {
+      void* p = c.free[best].p;
+      c.held -= c.free[best].bytes;
+      c.free.erase(c.free.begin() + best);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
+  cudaGetLastError();
+  release_arena_cache(dev);
+  p = nullptr;
+  if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+void arena_free(int dev, void* p, size_t bytes) {
+  ArenaCache& c = arena_cache();
+  std::lock_guard<std::mutex> g(c.m);
+  if (c.held + bytes > ARENA_CACHE_MAX) {
+    cudaFree(p);
+    return;
+  }
+  c.free.push_back({dev, bytes, p});
+  c.held += bytes;
 }
 
 double* dalloc(bf_ctx* ctx, size_t n, int* err) {
@@ -1859,7 +1940,7 @@ void bf_destroy(bf_ctx* ctx) {
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   }
   for (auto& hb : ctx->blocks) {
-    for (double* p : hb.owned) cudaFree(p);
+    for (double* p : hb.owned) arena_free(ctx->device, p, hb.arena_bytes);
     for (int f = 0; f < 6; ++f)
       if (hb.bface_d[f]) cudaFree(hb.bface_d[f]);
   }
@@ -1937,9 +2018,13 @@ int add_block_arena(bf_ctx* ctx, int block_id, const int dims[3], int ghost_dept
   const int vis0 = visc ? FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0) : -1;
   const int nfield = FSRC + (hb.has_src ? 5 : 0) + (want_psi ? 10 * ndim : 0) + (visc ? NVIS : 0);
   int err = 0;
-  hb.arena = dalloc(ctx, (size_t)nfield * hb.fsz, &err);
-  if (err) return err;
+  hb.arena_bytes = sizeof(double) * (size_t)nfield * hb.fsz;
+  hb.arena = static_cast<double*>(arena_alloc(ctx->device, hb.arena_bytes));
+  if (!hb.arena)
+    return fail(ctx, BF_ECUDA, "cudaMalloc(%zu bytes) failed for block %d", hb.arena_bytes,
+                block_id);
   hb.owned.push_back(hb.arena);
+  (void)err;
   CK(cudaMemset(hb.arena, 0, sizeof(double) * (size_t)nfield * hb.fsz));
   DevBlock& d = hb.dev;
   for (int a = 0; a < 3; ++a) d.n[a] = hb.n[a];
@@ -2087,7 +2172,8 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   }
   CK(cudaStreamSynchronize(st));
   if (hbad != ~0ull) {
-    for (void* p : hb.owned) cudaFree(p);
+    for (double* p : hb.owned) arena_free(ctx->device, p, hb.arena_bytes);
+    hb.owned.clear();
     const unsigned long long k = hbad % (unsigned long long)hb.n[2];
     const unsigned long long r = hbad / (unsigned long long)hb.n[2];
     const unsigned long long j = r % (unsigned long long)hb.n[1], i = r / (unsigned long long)hb.n[1];
@@ -2849,6 +2935,8 @@ int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* 
   *total_ms = ctx->prof_ms[kernel_class];
   return BF_OK;
 }
+
+void bf_release_cache(int device) { release_arena_cache(device); }
 
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction) {
   if (!ctx) return -1;
