@@ -1,0 +1,34 @@
+"""Block arenas recycled across contexts (bf_release_cache): a
+context built on cached arenas (stale contents) and one built after the
+cache was released give bitwise-identical runs."""
+
+import numpy as np
+import pytest
+
+from paper_2012_02925_b200 import cases, geometry, native, planning
+from paper_2012_02925_b200.model import FIELD_NAMES, GasModel, SchemeConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def test_recycled_arenas_do_not_leak_state():
+    from paper_2012_02925_b200.stepper import iterate_gpu
+    gas = GasModel()
+    plan = planning.decompose(geometry.multiblock_box_3d(2), 4, 3)
+    sched = planning.reorder_boundaries(plan)
+    fs = cases.freestream_for("multiblock_box_3d", gas, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    runs = []
+    for release in (True, False, False):
+        if release:
+            native.lib().bf_release_cache(-1)
+        r = iterate_gpu(plan, sched, gas, cfg, fs, 3, init="perturbed", precision="exact")
+        runs.append((r.history.copy(),
+                     {cid: {n: v.fields[n].copy() for n in FIELD_NAMES}
+                      for cid, v in r.solvers.items()}))
+    for h, f in runs[1:]:
+        np.testing.assert_array_equal(h, runs[0][0])
+        for cid in f:
+            for n in FIELD_NAMES:
+                np.testing.assert_array_equal(f[cid][n], runs[0][1][cid][n])
+    native.lib().bf_release_cache(-1)
