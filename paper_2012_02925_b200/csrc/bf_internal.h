@@ -157,10 +157,14 @@ struct GhostTask {
 };
 
 // Ghost launches are block-aligned: CUDA block b covers items
-// [block_map[b].y, +GHOST_SPAN) of task block_map[b].x (one task per block).
+// [block_map[b].y, +GHOST_BLOCK * ipt) of task block_map[b].x (one task per block).
 constexpr int GHOST_BLOCK = 128;
-constexpr int GHOST_ITEMS = 4;                       // items per thread
-constexpr int GHOST_SPAN = GHOST_BLOCK * GHOST_ITEMS;  // items per CUDA block
+constexpr int GHOST_ITEMS = 4;                       // items per thread (large launches)
+constexpr int GHOST_SPAN = GHOST_BLOCK * GHOST_ITEMS;  // items per CUDA block (large launches)
+// Small launches (fewer items than a few full-occupancy waves of GHOST_SPAN
+// blocks, e.g. 2D grids) use one item per thread: more blocks, shorter chains.
+constexpr long long GHOST_SMALL_ITEMS = 148LL * 4 * GHOST_SPAN;
+inline int ghost_ipt(long long total_items) { return total_items >= GHOST_SMALL_ITEMS ? GHOST_ITEMS : 1; }
 
 struct GhostArgs {
   const DevBlock* blocks;
@@ -171,6 +175,7 @@ struct GhostArgs {
   int cur;              // W buffer being filled
   int t_derived;        // interior T is p/(rho R) (after the first update)
   int extended;         // GK_BC: ghost round 2 (tangential range widened, solver.py:285-305)
+  int ipt;              // items per thread (1 .. GHOST_ITEMS), as the block map was cut
   long long total_items;
   Consts c;
 };

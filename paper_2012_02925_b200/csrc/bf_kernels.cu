@@ -262,8 +262,8 @@ BF_DEV void copy_store(const GhostArgs& a, const GhostTask& t, const G6& v, long
 
 BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m);
 
-// One task per CUDA block; the block covers GHOST_ITEMS x GHOST_BLOCK items of
-// it (strided by GHOST_BLOCK).  COPY items load all their values before the
+// One task per CUDA block; the block covers ipt x GHOST_BLOCK items of it
+// (strided by GHOST_BLOCK; ipt = GHOST_ITEMS for large launches, 1 for small).  COPY items load all their values before the
 // first store (GHOST_ITEMS x 6 loads in flight per thread).
 __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   __shared__ __align__(16) GhostTask ts;   // the task record, staged once
@@ -287,17 +287,17 @@ __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
 #pragma unroll
     for (int q = 0; q < GHOST_ITEMS; ++q) {
       const unsigned m = m0 + q * GHOST_BLOCK;
-      if (m < items) copy_load(a, t, m, v[q], doff[q]);
+      if (q < a.ipt && m < items) copy_load(a, t, m, v[q], doff[q]);
     }
 #pragma unroll
     for (int q = 0; q < GHOST_ITEMS; ++q) {
       const unsigned m = m0 + q * GHOST_BLOCK;
-      if (m < items) copy_store(a, t, v[q], doff[q]);
+      if (q < a.ipt && m < items) copy_store(a, t, v[q], doff[q]);
     }
     return;
   }
 #pragma unroll 1
-  for (int q = 0; q < GHOST_ITEMS; ++q) {
+  for (int q = 0; q < a.ipt; ++q) {
     const unsigned m = m0 + q * GHOST_BLOCK;
     if (m < items) bc_item(a, t, m);
   }

@@ -454,6 +454,7 @@ struct bf_ctx {
   int2* d_map_fill = nullptr;      // ghost launch block -> (task, first item)
   int2* d_map_unpack = nullptr;
   int nmap_fill = 0, nmap_unpack = 0;
+  int ipt_fill = 1, ipt_unpack = 1;   // ghost items per thread of those launches
   int n_unpack = 0;
   long long items_unpack = 0;
   std::vector<GhostTask> h_tasks_fill, h_tasks_unpack;
@@ -465,6 +466,7 @@ struct bf_ctx {
     int2* map = nullptr;
     int ntasks = 0, nmap = 0;
     long long items = 0;
+    int ipt = 1;
   };
   GhostLaunch r2_pack;
   std::vector<GhostLaunch> r1_bc;   // thin blocks: round-1 BCs in canonical order
@@ -964,10 +966,10 @@ int build_tables(bf_ctx* ctx) {
   ctx->items_unpack = acc;
   ctx->n_fill = (int)fill.size();
   ctx->n_unpack = (int)unp.size();
-  auto block_map = [&](const std::vector<GhostTask>& ts, int2** dst, int* n) -> int {
+  auto block_map = [&](const std::vector<GhostTask>& ts, int2** dst, int* n, int ipt) -> int {
     std::vector<int2> m;
     for (size_t ti = 0; ti < ts.size(); ++ti)
-      for (long long it = 0; it < ts[ti].items; it += GHOST_SPAN)
+      for (long long it = 0; it < ts[ti].items; it += (long long)GHOST_BLOCK * ipt)
         m.push_back(make_int2((int)ti, (int)it));
     *n = (int)m.size();
     if (m.empty()) return BF_OK;
@@ -977,8 +979,10 @@ int build_tables(bf_ctx* ctx) {
     *dst = static_cast<int2*>(p);
     return BF_OK;
   };
-  if (int rc = block_map(fill, &ctx->d_map_fill, &ctx->nmap_fill)) return rc;
-  if (int rc = block_map(unp, &ctx->d_map_unpack, &ctx->nmap_unpack)) return rc;
+  ctx->ipt_fill = ghost_ipt(ctx->items_fill);
+  ctx->ipt_unpack = ghost_ipt(ctx->items_unpack);
+  if (int rc = block_map(fill, &ctx->d_map_fill, &ctx->nmap_fill, ctx->ipt_fill)) return rc;
+  if (int rc = block_map(unp, &ctx->d_map_unpack, &ctx->nmap_unpack, ctx->ipt_unpack)) return rc;
   if (!fill.empty()) {
     void* p = nullptr;
     CK(cudaMalloc(&p, fill.size() * sizeof(GhostTask)));
@@ -1159,9 +1163,10 @@ int make_launch(bf_ctx* ctx, std::vector<GhostTask>& ts, bf_ctx::GhostLaunch& L)
   CK(cudaMalloc(&p, ts.size() * sizeof(GhostTask)));
   CK(cudaMemcpy(p, ts.data(), ts.size() * sizeof(GhostTask), cudaMemcpyHostToDevice));
   L.d = static_cast<GhostTask*>(p);
+  L.ipt = ghost_ipt(L.items);
   std::vector<int2> m;
   for (size_t ti = 0; ti < ts.size(); ++ti)
-    for (long long it = 0; it < ts[ti].items; it += GHOST_SPAN)
+    for (long long it = 0; it < ts[ti].items; it += (long long)GHOST_BLOCK * L.ipt)
       m.push_back(make_int2((int)ti, (int)it));
   L.nmap = (int)m.size();
   CK(cudaMalloc(&p, std::max<size_t>(m.size(), 1) * sizeof(int2)));
@@ -1362,6 +1367,7 @@ int run_ghost_launch(bf_ctx* ctx, const bf_ctx::GhostLaunch& L, int extended) {
   g.cur = ctx->cur;
   g.t_derived = ctx->t_derived;
   g.extended = extended;
+  g.ipt = L.ipt;
   g.c = ctx->c;
   CK(ghost_fn(ctx)(g, ctx->stream));
   return BF_OK;
@@ -1546,6 +1552,7 @@ GhostArgs ghost_args(bf_ctx* ctx, bool unpack) {
   g.nlaunch = unpack ? ctx->nmap_unpack : ctx->nmap_fill;
   g.ntasks = unpack ? ctx->n_unpack : ctx->n_fill;
   g.total_items = unpack ? ctx->items_unpack : ctx->items_fill;
+  g.ipt = unpack ? ctx->ipt_unpack : ctx->ipt_fill;
   g.cur = ctx->cur;
   g.t_derived = ctx->t_derived;
   g.c = ctx->c;
