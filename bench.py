@@ -281,10 +281,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         ev0.record(stream)
-        for k in range(args.steps):
-            st.step(args.warmup + k + 1)
+        # the drop-in's step loop (iterate_gpu): steps driven from C, each one
+        # returning its residual norms to the host
+        done = len(st.run(args.warmup + 1, args.steps))
         ev1.record(stream)
         torch.cuda.synchronize()
+    if done != args.steps:
+        raise SystemExit(f"bench: the history guard stopped the run after {done} steps")
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -441,8 +444,7 @@ def e2e_run(plan, children, gas, cfg, fs, init, device, rank, world, args, dist,
         gpu.upload(cid, f6)      # conserved variables derived on the device
     mark("upload")
     st = stepper.GpuRankStepper(gpu, cfg)
-    for k in range(args.steps):
-        st.step(k + 1)       # each step ends with the D2H of its residual norms
+    st.run(1, args.steps)    # each step ends with the D2H of its residual norms
     mark("steps")
     out = {cid: [gpu.download(cid, n, out=outs[cid][k]) for k, n in enumerate(FIELD_NAMES)]
            for cid in host}

@@ -188,10 +188,19 @@ int bf_update_ghosts(bf_ctx* ctx);
    blocks in id order of sum(R^2) from the first stage; when the ctx has an NCCL
    communicator the rank-ordered sum over all ranks (exchange.py:294-309). */
 int bf_step(bf_ctx* ctx, int step_index, double* sumsq_out, long long* ncells_out);
-/* nsteps consecutive steps without per-step host synchronisation; per-step
-   norms land in hist_out[nsteps*5] (sqrt of the rank-ordered sums).  Returns at
-   the first step with a non-physical state (bf_error_info names it). */
+/* nsteps consecutive steps driven from C (no return to the caller between
+   steps); per-step norms land in hist_out[nsteps*5] (sqrt of the rank-ordered
+   sums).  Returns at the first step with a non-physical state (bf_error_info
+   names it). */
 int bf_run(bf_ctx* ctx, int first_step, int nsteps, double* hist_out, int* steps_done);
+/* solver.iterate's loop (solver.py:914-936) driven from C: up to max_steps
+   steps, after each one the history guards of solver.py:836-855 (residual floor,
+   divergence factor, residual target; has_* = 0 disables a criterion).  status:
+   0 ran max_steps, 1 converged at the last step, 2 diverged at the last step
+   (the caller raises DivergenceError exactly as the guard does). */
+int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, double target,
+               int has_floor, double floor_, double divergence_factor, double* hist_out,
+               int* steps_done, int* status);
 
 /* --- state access --------------------------------------------------------- */
 /* Padded Fortran array of the block's field `what` (BF_FIELD_*) exactly as the

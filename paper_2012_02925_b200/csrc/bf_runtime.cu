@@ -2580,6 +2580,57 @@ int bf_run(bf_ctx* ctx, int first_step, int nsteps, double* hist_out, int* steps
   return BF_OK;
 }
 
+// check_history_guards (solver.py:836-855) on the norms of step `step`:
+// 0 continue, 1 converged (floor / target reached), 2 diverged (the caller
+// raises).  numpy semantics: max propagates NaN, comparisons with NaN fail.
+static int history_guard(const double* hist, int step, int has_target, double target,
+                         int has_floor, double floor_, double factor) {
+  auto npmax = [](const double* x) {
+    double m = x[0];
+    for (int v = 1; v < 5; ++v)
+      if (std::isnan(x[v]) || x[v] > m || std::isnan(m)) m = std::isnan(m) ? m : x[v];
+    return m;
+  };
+  const double* h = hist + 5 * (size_t)step;
+  if (has_floor && npmax(h) <= floor_) return 1;
+  const double* b = hist;
+  const double bmax = npmax(b);
+  bool any = false, bad = false;
+  double rmax = 0.0;
+  for (int v = 0; v < 5; ++v) {
+    if (!(b[v] > 1e-12 * bmax)) continue;
+    const double r = h[v] / b[v];
+    if (!std::isfinite(r)) bad = true;
+    rmax = any ? (r > rmax ? r : rmax) : r;
+    any = true;
+  }
+  if (!any) return 0;
+  if (bad || rmax > factor) return 2;
+  return (has_target && rmax <= target) ? 1 : 0;
+}
+
+int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, double target,
+               int has_floor, double floor_, double divergence_factor, double* hist_out,
+               int* steps_done, int* status) {
+  if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_iterate before bf_finalize");
+  *steps_done = 0;
+  *status = 0;
+  for (int s = 0; s < max_steps; ++s) {
+    double ss[5];
+    int rc = bf_step(ctx, first_step + s, ss, nullptr);
+    if (rc) return rc;
+    for (int v = 0; v < 5; ++v) hist_out[5 * s + v] = std::sqrt(ss[v]);
+    *steps_done = s + 1;
+    const int g = history_guard(hist_out, s, has_target, target, has_floor, floor_,
+                                divergence_factor);
+    if (g) {
+      *status = g;
+      break;
+    }
+  }
+  return BF_OK;
+}
+
 int bf_download(bf_ctx* ctx, int block_id, int what, double* out) {
   if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_download before bf_finalize");
   if (!ctx->index_of.count(block_id)) return fail(ctx, BF_EINVAL, "unknown block %d", block_id);

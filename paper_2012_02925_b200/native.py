@@ -71,6 +71,7 @@ PROTOTYPES = {
     "bf_update_ghosts": (_I, [_P]),
     "bf_step": (_I, [_P, _I, _PD, _PLL]),
     "bf_run": (_I, [_P, _I, _I, _PD, _PI]),
+    "bf_iterate": (_I, [_P, _I, _I, _I, C.c_double, _I, C.c_double, C.c_double, _PD, _PI, _PI]),
     "bf_download": (_I, [_P, _I, _I, _PD]),
     "bf_error_info": (_I, [_P, _PI, _PI, _PI, _PI, _PLL]),
     "bf_nccl_unique_id": (_I, [_P]),

@@ -367,6 +367,20 @@ class GpuContext:
         self._check(self.L.bf_step(self.ctx, int(step_index), out, C.byref(n)))
         return np.array(out[:], dtype=float), int(n.value)
 
+    def iterate(self, first_step, max_steps, residual_target=None, residual_floor=None,
+                divergence_factor=1e6):
+        """bf_iterate: up to max_steps steps with the history guards evaluated in C
+        after each; returns (norms[steps, 5], status) — status 1 converged, 2
+        diverged at the last step, 0 ran max_steps."""
+        hist = np.zeros((max(int(max_steps), 1), 5))
+        done, status = C.c_int(), C.c_int()
+        self._check(self.L.bf_iterate(
+            self.ctx, int(first_step), int(max_steps), int(residual_target is not None),
+            float(residual_target or 0.0), int(residual_floor is not None),
+            float(residual_floor or 0.0), float(divergence_factor), native.dptr(hist),
+            C.byref(done), C.byref(status)))
+        return hist[:done.value].copy(), status.value
+
     def download(self, cid, what, out=None):
         """One array of a child (BF_FIELD_* selector or field name); `out`, when
         given, is a preallocated Fortran float64 array of the right shape
@@ -534,6 +548,20 @@ class GpuRankStepper:
             v.frozen = fz is not None and step_index > fz
         return sumsq, ncells
 
+    def run(self, first_step, max_steps, residual_target=None, residual_floor=None):
+        """Steps first_step .. while the history guards allow, driven from C
+        (GpuContext.iterate); returns the norms of the steps taken."""
+        fz = self.config.limiter_freeze_at
+        try:
+            hist, _ = self.gpu.iterate(first_step, max_steps, residual_target, residual_floor)
+        finally:
+            self._invalidate()
+        if len(hist):
+            last = first_step + len(hist) - 1
+            for v in self.solvers.values():
+                v.frozen = fz is not None and last > fz
+        return hist
+
     def _invalidate(self):
         for v in self.solvers.values():
             v.invalidate()
@@ -612,13 +640,13 @@ def iterate_gpu(plan, schedule, gas, config, freestream, max_steps, residual_tar
                      schedule=schedule)
     gpu.upload_initial(init)
     stepper = GpuRankStepper(gpu, config)
-    history, converged = [], False
-    for step in range(max_steps):
-        sumsq, _ = stepper.step(step + 1)
-        history.append(residual_norms(sumsq))
-        if check_history_guards(history, step, residual_target, residual_floor=residual_floor):
-            converged = True
-            break
+    # the step loop and its guards run in C (bf_iterate: no return to Python
+    # between steps); the guard is re-evaluated here on the last step so a
+    # divergence raises exactly as solver.py:836-855 does
+    history = list(stepper.run(1, max_steps, residual_target, residual_floor))
+    converged = bool(history) and check_history_guards(history, len(history) - 1,
+                                                       residual_target,
+                                                       residual_floor=residual_floor)
     return IterationResult(solvers=stepper.solvers, history=np.array(history),
                            steps=len(history), converged=converged)
 
