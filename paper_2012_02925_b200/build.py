@@ -21,7 +21,8 @@ LIB = PKG / "libbfgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                 "-Xcompiler", "-ffp-contract=off", "-I", str(PKG.parent / "include")]
+                 "-Xcompiler", "-ffp-contract=off", "-I", str(PKG.parent / "include")] + \
+    os.environ.get("BF_NVCC_EXTRA", "").split()   # extra nvcc flags (experiment variants)
 
 
 def _run(cmd):
