@@ -316,11 +316,13 @@ def main():
             traffic = None
 
     # e2e through the public API with host buffers (rank 0 / N=1 only)
+    # the measured context is done: release it before the end-to-end run builds its own
+    # (its block arenas are then recycled instead of mapped afresh by the driver)
+    gpu.close()
     e2e = None
     if not args.skip_e2e:
         e2e = e2e_run(plan, my_children, gas, cfg, fs, init, local, rank, world, args, dist,
                       setups)
-    gpu.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:

@@ -237,9 +237,10 @@ int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* 
 /* Device bytes the last bf_upload_fields / bf_download moved (for e2e accounting). */
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction /*0 h2d, 1 d2h*/);
 
-/* Block arenas of destroyed contexts are kept for reuse by the next context on
-   the same device (bounded; a failing allocation releases them first).  Hand
-   them back to the driver: device >= 0 one device, < 0 all. */
+/* Block arenas of destroyed contexts (and the staging buffers' stream-ordered
+   pool) are kept for reuse by the next context on the same device (bounded; a
+   failing arena allocation releases them first).  Hand them back to the
+   driver: device >= 0 one device, < 0 all. */
 void bf_release_cache(int device);
 
 /* Host-only lowering probe (no GPU needed): the affine index map the device

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1942,10 +1943,8 @@ void bf_destroy(bf_ctx* ctx) {
       cudaEventDestroy(p.a);
       cudaEventDestroy(p.b);
     }
-  {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-  }
+  // (the stream-ordered staging pool keeps its memory, like the arena cache:
+  // bf_release_cache returns both)
   for (auto& hb : ctx->blocks) {
     for (double* p : hb.owned) arena_free(ctx->device, p, hb.arena_bytes);
     for (int f = 0; f < 6; ++f)
@@ -2308,6 +2307,15 @@ int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int
 int bf_finalize(bf_ctx* ctx) {
   if (!ctx) return BF_EINVAL;
   if (ctx->finalized) return BF_OK;
+  static const bool trace = std::getenv("BF_TRACE_FINALIZE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "bf_finalize %-12s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   CK(cudaSetDevice(ctx->device));
   if (ctx->sch.viscous)
     for (auto& hb : ctx->blocks)
@@ -2315,8 +2323,10 @@ int bf_finalize(bf_ctx* ctx) {
         return fail(ctx, BF_EINVAL, "viscous run: block %d has no bf_add_viscous_geometry", hb.id);
   int rc = build_tables(ctx);
   if (rc) return rc;
+  mark("tables");
   rc = build_push(ctx);
   if (rc) return rc;
+  mark("push");
   if (ctx->sch.viscous) {
     rc = build_round2(ctx);
     if (rc) return rc;
@@ -2345,8 +2355,10 @@ int bf_finalize(bf_ctx* ctx) {
   }
   rc = build_tiles(ctx);
   if (rc) return rc;
+  mark("tiles");
   rc = build_tensor_maps(ctx);
   if (rc) return rc;
+  mark("tmaps");
   std::vector<DevBlock> devs;
   for (auto& hb : ctx->blocks) devs.push_back(hb.dev);
   void* p = nullptr;
@@ -2366,6 +2378,7 @@ int bf_finalize(bf_ctx* ctx) {
   ctx->d_gather = static_cast<double*>(p);
   CK(cudaMallocHost(&p, sizeof(double) * (5 * ctx->blocks.size() + 2)));
   ctx->h_pinned = static_cast<double*>(p);
+  mark("buffers");
   ctx->finalized = true;
   return BF_OK;
 }
@@ -2994,7 +3007,18 @@ int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* 
   return BF_OK;
 }
 
-void bf_release_cache(int device) { release_arena_cache(device); }
+void bf_release_cache(int device) {
+  release_arena_cache(device);
+  int n = 0, cur = -1;
+  cudaGetDeviceCount(&n);
+  cudaGetDevice(&cur);
+  for (int d = 0; d < n; ++d) {
+    if (device >= 0 && d != device) continue;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
+  if (cur >= 0) cudaSetDevice(cur);
+}
 
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction) {
   if (!ctx) return -1;
