@@ -730,13 +730,12 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
         stepper = GpuRankStepper(gpu, config)
         dist.barrier()
         t0 = time.perf_counter()
-        for step in range(max_steps):
-            sumsq, _ = stepper.step(step + 1)
-            history.append(residual_norms(sumsq))
-            if check_history_guards(history, step, residual_target,
-                                    residual_floor=residual_floor):
-                converged = True
-                break
+        # step loop and guards in C (bf_iterate; the guards see the rank-ordered
+        # global norms, so every rank stops at the same step)
+        history = list(stepper.run(1, max_steps, residual_target, residual_floor))
+        converged = bool(history) and check_history_guards(history, len(history) - 1,
+                                                           residual_target,
+                                                           residual_floor=residual_floor)
         solve = time.perf_counter() - t0
         from .distributed import assemble_parent_fields, local_interiors
         parts = [None] * nr
