@@ -78,6 +78,7 @@ extern "C" {
 
 typedef struct bf_ctx bf_ctx;
 typedef struct bf_group bf_group;
+typedef struct bf_loopback bf_loopback;
 
 typedef struct bf_gas {            /* physics.py:47-90 */
   double gamma;
@@ -217,6 +218,20 @@ int bf_error_info(const bf_ctx* ctx, int* kind, int* block_id, int* stage, int* 
    bf_nccl_init before bf_finalize. */
 int bf_nccl_unique_id(void* out128);
 int bf_nccl_init(bf_ctx* ctx, const void* id128);
+/* Loopback transport: the NCCL calls of the path (grouped ncclSend/ncclRecv of
+   the halo messages, ncclAllGather of the residual record) served inside ONE
+   process whose ranks are host threads, one bf_ctx each, on any GPUs (several
+   may share one).  Same matching, ordering and completion semantics as NCCL:
+   the runtime's exchange / interior-boundary overlap / rank-ordered residual
+   code runs unchanged with it bound in place of libnccl (exchange.py:599-682
+   runs its ranks as threads the same way).  bf_loopback_init replaces
+   bf_nccl_init (before bf_finalize); the world must outlive its contexts.  A
+   rank that stops calling makes its peers fail with BF_ENCCL after
+   BF_LOOPBACK_TIMEOUT seconds (default 120) or at bf_loopback_abort. */
+bf_loopback* bf_loopback_create(int nranks);
+int bf_loopback_init(bf_ctx* ctx, bf_loopback* world);
+void bf_loopback_abort(bf_loopback* world);
+void bf_loopback_destroy(bf_loopback* world);
 /* In-process group: several ctxs (ranks) driven in lock step by one host
    thread; remote links become device-to-device pushes into the peer's
    receive buffers (peer access over NVLink when the ctxs sit on different

@@ -27,6 +27,7 @@
 
 #include "../../include/bfgpu.h"
 #include "bf_internal.h"
+#include "bf_loopback.h"
 
 namespace bf {
 namespace bf_exact {
@@ -97,6 +98,22 @@ NcclApi load_nccl() {
 
 NcclApi& nccl() {
   static NcclApi api = load_nccl();
+  return api;
+}
+
+// The same entry points bound to the in-process transport (bf_loopback.h).
+const NcclApi& loopback_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    a.ok = true;
+    a.Send = bf_lb::Send;
+    a.Recv = bf_lb::Recv;
+    a.GroupStart = bf_lb::GroupStart;
+    a.GroupEnd = bf_lb::GroupEnd;
+    a.AllGather = bf_lb::AllGather;
+    a.GetErrorString = bf_lb::GetErrorString;
+    return a;
+  }();
   return api;
 }
 
@@ -496,6 +513,8 @@ struct bf_ctx {
   long long e_idx[3] = {0, 0, 0};
   // comm
   ncclComm_t comm = nullptr;
+  const NcclApi* net = nullptr;    // transport bound to comm: libnccl or the loopback
+  bf_lb::Rank* lb_rank = nullptr;  // loopback: what comm points to (owned)
   bf_group* group = nullptr;
   // profiling
   bool profiling = false;
@@ -514,6 +533,8 @@ struct bf_group {
 };
 
 namespace {
+
+const NcclApi& net(const bf_ctx* ctx) { return ctx && ctx->net ? *ctx->net : nccl(); }
 
 int fail(bf_ctx* ctx, int code, const char* fmt, ...) {
   char buf[1024];
@@ -537,7 +558,7 @@ int fail(bf_ctx* ctx, int code, const char* fmt, ...) {
   do {                                                                                        \
     ncclResult_t r_ = (call);                                                                 \
     if (r_ != ncclSuccess)                                                                    \
-      return fail(ctx, BF_ENCCL, "%s failed: %s (%s:%d)", #call, nccl().GetErrorString(r_), \
+      return fail(ctx, BF_ENCCL, "%s failed: %s (%s:%d)", #call, net(ctx).GetErrorString(r_), \
                   __FILE__, __LINE__);                                                        \
   } while (0)
 
@@ -1396,13 +1417,13 @@ int ghosts_round2(bf_ctx* ctx) {
   if (remote) {
     if (!ctx->comm)
       return fail(ctx, BF_EINVAL, "rank %d has remote links but no communicator", ctx->rank);
-    NK(nccl().GroupStart());
+    NK(net(ctx).GroupStart());
     for (HostLink* L : remote_links_sorted(ctx)) {
       const size_t cnt = (size_t)L->nfields * L->cells2;
-      NK(nccl().Send(L->send2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
-      NK(nccl().Recv(L->recv2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+      NK(net(ctx).Send(L->send2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+      NK(net(ctx).Recv(L->recv2, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
     }
-    NK(nccl().GroupEnd());
+    NK(net(ctx).GroupEnd());
   }
   for (auto& L : ctx->r2_unpack) {
     rc = run_ghost_launch(ctx, L, 0);
@@ -1587,13 +1608,13 @@ std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx) {
 int nccl_exchange(bf_ctx* ctx) {
   auto rl = remote_links_sorted(ctx);
   if (rl.empty()) return BF_OK;
-  NK(nccl().GroupStart());
+  NK(net(ctx).GroupStart());
   for (HostLink* L : rl) {
     const size_t cnt = (size_t)L->nfields * L->cells;
-    NK(nccl().Send(L->send, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
-    NK(nccl().Recv(L->recv, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    NK(net(ctx).Send(L->send, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
+    NK(net(ctx).Recv(L->recv, cnt, ncclDouble, L->peer_rank, ctx->comm, ctx->stream));
   }
-  NK(nccl().GroupEnd());
+  NK(net(ctx).GroupEnd());
   return BF_OK;
 }
 
@@ -1821,7 +1842,7 @@ int rank_allgather(bf_ctx* ctx, double* sumsq, unsigned long long* key, int* bad
   for (int v = 0; v < 5; ++v) rec[v] = sumsq[v];
   std::memcpy(&rec[5], key, sizeof(double));
   CK(cudaMemcpyAsync(ctx->d_rank6, rec, sizeof rec, cudaMemcpyHostToDevice, ctx->stream));
-  NK(nccl().AllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
+  NK(net(ctx).AllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
   std::vector<double> all((size_t)6 * ctx->nranks);
   CK(cudaMemcpyAsync(all.data(), ctx->d_gather, sizeof(double) * all.size(),
                      cudaMemcpyDeviceToHost, ctx->stream));
@@ -1934,7 +1955,11 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
 void bf_destroy(bf_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  // every stream that may still touch the arenas (an aborted overlapped step can
+  // leave an unpack queued on comm_stream) drains before they are recycled
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+  if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   for (auto& row : ctx->gexec)
     for (auto& ex : row)
       if (ex) cudaGraphExecDestroy(ex);
@@ -1976,7 +2001,8 @@ void bf_destroy(bf_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
-  if (ctx->comm) nccl().CommDestroy(ctx->comm);
+  if (ctx->lb_rank) delete ctx->lb_rank;
+  else if (ctx->comm) nccl().CommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_filled) cudaEventDestroy(ctx->ev_filled);
@@ -2775,6 +2801,33 @@ int bf_nccl_init(bf_ctx* ctx, const void* id128) {
   NK(nccl().CommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
   return BF_OK;
 }
+
+// ---- loopback transport (bf_loopback.h) -------------------------------------------
+
+bf_loopback* bf_loopback_create(int nranks) {
+  if (nranks < 1) return nullptr;
+  return reinterpret_cast<bf_loopback*>(new bf_lb::World(nranks));
+}
+
+int bf_loopback_init(bf_ctx* ctx, bf_loopback* world) {
+  if (!ctx || !world) return BF_EINVAL;
+  auto* w = reinterpret_cast<bf_lb::World*>(world);
+  if (ctx->finalized) return fail(ctx, BF_EINVAL, "bf_loopback_init after bf_finalize");
+  if (ctx->comm) return fail(ctx, BF_EINVAL, "context already has a communicator");
+  if (w->n != ctx->nranks)
+    return fail(ctx, BF_EINVAL, "loopback world has %d ranks, context expects %d", w->n,
+                ctx->nranks);
+  ctx->lb_rank = new bf_lb::Rank{w, ctx->rank, 0};
+  ctx->comm = reinterpret_cast<ncclComm_t>(ctx->lb_rank);
+  ctx->net = &loopback_api();
+  return BF_OK;
+}
+
+void bf_loopback_abort(bf_loopback* world) {
+  if (world) bf_lb::abort(reinterpret_cast<bf_lb::World*>(world));
+}
+
+void bf_loopback_destroy(bf_loopback* world) { delete reinterpret_cast<bf_lb::World*>(world); }
 
 // ---- in-process groups --------------------------------------------------------
 

@@ -76,6 +76,10 @@ PROTOTYPES = {
     "bf_error_info": (_I, [_P, _PI, _PI, _PI, _PI, _PLL]),
     "bf_nccl_unique_id": (_I, [_P]),
     "bf_nccl_init": (_I, [_P, _P]),
+    "bf_loopback_create": (_P, [_I]),
+    "bf_loopback_init": (_I, [_P, _P]),
+    "bf_loopback_abort": (None, [_P]),
+    "bf_loopback_destroy": (None, [_P]),
     "bf_group_create": (_P, [C.POINTER(_P), _I]),
     "bf_group_destroy": (None, [_P]),
     "bf_group_update_ghosts": (_I, [_P]),

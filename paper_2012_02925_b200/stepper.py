@@ -690,16 +690,24 @@ def native_counters(plan, rounds=1):
 
 def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, max_steps=100,
                         residual_target=None, init="uniform", timeout_s=5.0,
-                        residual_floor=None, precision="auto", devices=None, metrics_fn=None):
+                        residual_floor=None, precision="auto", devices=None, metrics_fn=None,
+                        transport="loopback"):
     """exchange.run_distributed on GPUs (exchange.py:599-682).
 
     * torch.distributed initialised with world_size == plan.np_ranks: this
       process runs rank = dist.get_rank() on cuda:LOCAL_RANK, halos over NCCL,
       the residual sum over ranks in rank order; fields are gathered to every
       rank.
-    * otherwise: every rank is a context of one in-process group, rank r on
-      device devices[r % len(devices)] (all on device 0 by default), halos as
-      device-to-device copies driven in lock step.
+    * otherwise every rank lives in this process, rank r on device
+      devices[r % len(devices)] (all on device 0 by default):
+      - transport="loopback" (default): one host thread per rank, as the
+        reference's run_distributed spawns them (exchange.py:647-651), each
+        driving its own context through the NCCL code path of the runtime
+        (grouped send/recv of the halo messages on the comm stream overlapped
+        with the interior tiles, rank-ordered allgather of the residual) with
+        the in-process transport of bf_loopback.h bound instead of libnccl;
+      - transport="group": all ranks driven in lock step from this thread,
+        halos as device-to-device copies (bf_group_*).
     """
     import os
     nr = plan.np_ranks
@@ -746,6 +754,11 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
                                  converged=converged, counters=native_counters(plan),
                                  solve_seconds=solve)
 
+    if transport == "loopback":
+        return _run_loopback(plan, schedule, gas, config, freestream, max_steps, residual_target,
+                             init, residual_floor, precision, devices, metrics_fn)
+    if transport != "group":
+        raise bridged(ConfigError)(f"unknown transport {transport!r}")
     devs = list(devices) if devices is not None else [0]
     gpus = [GpuContext(plan, [c.id for c in plan.rank_children(r)], gas, config, freestream,
                        device=devs[r % len(devs)], rank=r, nranks=nr, precision=precision,
@@ -782,3 +795,73 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
     return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
                              converged=converged, counters=native_counters(plan),
                              solve_seconds=solve)
+
+
+def _run_loopback(plan, schedule, gas, config, freestream, max_steps, residual_target, init,
+                  residual_floor, precision, devices, metrics_fn):
+    """run_distributed_gpu with one host thread per rank over the loopback
+    transport (see run_distributed_gpu)."""
+    import threading
+    nr = plan.np_ranks
+    devs = list(devices) if devices is not None else [0]
+    L = native.lib()
+    world = L.bf_loopback_create(nr)
+    if not world:
+        raise NativeLibraryError("bf_loopback_create failed")
+    gpus = []
+    try:
+        for r in range(nr):
+            g = GpuContext(plan, [c.id for c in plan.rank_children(r)], gas, config, freestream,
+                           device=devs[r % len(devs)], rank=r, nranks=nr, precision=precision,
+                           metrics_fn=metrics_fn, schedule=schedule)
+            gpus.append(g)
+            g._check(L.bf_loopback_init(g.ctx, world))
+        for g in gpus:
+            g.upload_initial(init)
+        steppers = [GpuRankStepper(g, config) for g in gpus]
+        results, errors = [None] * nr, {}
+        # solver time starts once every rank is set up (exchange.py:620-655)
+        barrier = threading.Barrier(nr + 1)
+
+        def worker(r):
+            try:
+                barrier.wait()
+                results[r] = steppers[r].run(1, max_steps, residual_target, residual_floor)
+            except BaseException as exc:  # noqa: BLE001 — stop the others, re-raise below
+                errors[r] = exc
+                L.bf_loopback_abort(world)
+
+        threads = [threading.Thread(target=worker, args=(r,), name=f"gpu-rank-{r}")
+                   for r in range(nr)]
+        for t in threads:
+            t.start()
+        barrier.wait()
+        t0 = time.perf_counter()
+        for t in threads:
+            t.join()
+        solve = time.perf_counter() - t0
+        if errors:
+            # the first failing rank's own error (the others only saw the abort)
+            import re
+
+            def secondary(e):   # a peer's echo of another rank's failure
+                return ("loopback transport" in str(e) or
+                        re.fullmatch(r"rank \d+: non-physical state", str(e)) is not None)
+            raise errors[min(errors, key=lambda r: (secondary(errors[r]), r))]
+        history = [np.asarray(h) for h in results[0]]
+        for r in range(1, nr):   # every rank saw the same rank-ordered global norms
+            if len(results[r]) != len(history) or not np.array_equal(np.asarray(results[r]),
+                                                                     np.asarray(results[0])):
+                raise NativeLibraryError(f"rank {r} residual history differs from rank 0")
+        converged = bool(history) and check_history_guards(history, len(history) - 1,
+                                                           residual_target,
+                                                           residual_floor=residual_floor)
+        views = {cid: v for st in steppers for cid, v in st.solvers.items()}
+        fields = _gather_parent_fields(plan, views)
+        return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
+                                 converged=converged, counters=native_counters(plan),
+                                 solve_seconds=solve)
+    finally:
+        for g in gpus:
+            g.close()
+        L.bf_loopback_destroy(world)
