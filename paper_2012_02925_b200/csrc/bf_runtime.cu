@@ -433,12 +433,16 @@ struct bf_ctx {
   // comm_stream while the stage kernel runs the tiles that read no remote ghost
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_filled = nullptr, ev_unpacked = nullptr;
+  cudaEvent_t ev_bd = nullptr;     // boundary tiles of the stage done (comm_stream)
   int* d_tiles_in = nullptr;       // tile ids reading no remote-received ghost cell
   int* d_tiles_bd = nullptr;       // the others (launched after the unpack)
   int n_tiles_in = 0, n_tiles_bd = 0;
   bool split_tiles = false;        // interior / boundary tile lists built
   bool split_forced = false;       // BF_SPLIT_TILES=1
-  bool exchange_pending = false;   // ev_unpacked must be waited on before boundary tiles
+  bool exchange_pending = false;   // messages + unpack queued on comm_stream this stage
+  bool hide_fill = false;          // one-rank ctx: ghost fill on comm_stream beside the
+                                   // interior tiles (BF_HIDE_GHOSTS=1; measured slower)
+  bool fill_pending = false;       // this stage's ghost fill is queued on comm_stream
   bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
   // one RK step as a CUDA graph (standalone Euler ctx), per starting buffer and
   // profiling mode; a profiled graph records its own timing events
@@ -1514,9 +1518,20 @@ int build_tiles(bf_ctx* ctx) {
     // (exercised on one GPU by the tests).
     const char* e = std::getenv("BF_SPLIT_TILES");
     const bool force = e && e[0] == '1';
+    // BF_HIDE_GHOSTS=1 (one-rank ctx): every block face carries a ghost fill
+    // (connected copy or physical patch), so tiles touching any face wait for
+    // the fill on the comm stream and the others run beside it.  Measured
+    // slower (C4 stage span 1.257 vs 1.100 + 0.101 ms): a stage CTA holds a
+    // whole SM (64K registers), so the latency-bound fill only gets the SMs
+    // that retiring tiles free, one at a time — off by default.
+    const char* h = std::getenv("BF_HIDE_GHOSTS");
+    bool has_remote = false;
+    for (auto& L : ctx->links) has_remote = has_remote || L.send != nullptr;
+    ctx->hide_fill = (h && h[0] == '1') && !force && !has_remote && ctx->ndim == 3 &&
+                     !ctx->sch.viscous && ctx->r1_bc.empty() && !(ctx->push_ok && push_enabled());
     std::vector<std::array<bool, 6>> remote(ctx->blocks.size());
-    for (auto& r : remote) r.fill(force);
-    bool any = force;
+    for (auto& r : remote) r.fill(force || ctx->hide_fill);
+    bool any = force || ctx->hide_fill;
     for (auto& L : ctx->links)
       if (L.send) {
         remote[ctx->index_of[L.block]][L.face] = true;
@@ -1552,6 +1567,7 @@ int build_tiles(bf_ctx* ctx) {
       CK(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
       CK(cudaEventCreateWithFlags(&ctx->ev_filled, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ctx->ev_unpacked, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_bd, cudaEventDisableTiming));
     }
   }
   void* p = nullptr;
@@ -1641,12 +1657,28 @@ int ghosts_solo(bf_ctx* ctx) {
     if (r0) return r0;
     ctx->synced_cur = ctx->cur_epoch;
   }
+  if (ctx->hide_fill && ctx->split_tiles && !ctx->pushed) {
+    // the fill goes to comm_stream after everything queued so far (the previous
+    // stage, both of its launches); the next stage's interior tiles run beside
+    // it and its boundary tiles follow it there (launch_stage_kernel)
+    CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_filled, 0));
+    cudaStream_t saved = ctx->stream;
+    ctx->stream = ctx->comm_stream;
+    const int rc = fill_ghosts(ctx);
+    ctx->stream = saved;
+    if (rc) return rc;
+    ctx->fill_pending = true;
+    ctx->ghost_buf = ctx->cur;
+    return BF_OK;
+  }
   int rc = fill_ghosts(ctx);
   if (rc) return rc;
   if (ctx->n_unpack && ctx->comm && ctx->split_tiles && !ctx->no_overlap && !ctx->sch.viscous &&
       ctx->r1_bc.empty()) {
     // messages and unpack on the comm stream; the interior tiles of the next stage
-    // launch run meanwhile (launch_stage_kernel waits on ev_unpacked)
+    // run meanwhile on the main stream, its boundary tiles follow the unpack on
+    // the comm stream (launch_stage_kernel)
     CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_filled, 0));
     cudaStream_t saved = ctx->stream;
@@ -1737,22 +1769,30 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
     // two launches only when they buy an overlap (NCCL messages in flight) or
     // when forced; the split costs tile-order L2 locality and a second tail
     const bool split = ctx->split_tiles &&
-                       (ctx->split_forced || (ctx->comm && ctx->n_unpack && !ctx->no_overlap));
+                       (ctx->split_forced || ctx->exchange_pending || ctx->fill_pending);
     if (!split) {
       CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
     } else {
-      // interior tiles first; the boundary tiles after the exchange has landed
+      // interior tiles (no ghost they read is written this stage) on the main
+      // stream; boundary tiles on the comm stream behind the ghost work queued
+      // there (messages + unpack, or the hidden fill) — the two launches run
+      // concurrently and join before anything that follows the stage
+      if (!ctx->exchange_pending && !ctx->fill_pending) {   // forced split: ghosts in line
+        CK(cudaEventRecord(ctx->ev_filled, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_filled, 0));
+      }
       StageArgs b = a;
       b.tile_list = ctx->d_tiles_in;
       b.ntiles = ctx->n_tiles_in;
-      CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->stream));
-      if (ctx->exchange_pending) {
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_unpacked, 0));
-        ctx->exchange_pending = false;
-      }
+      if (b.ntiles) CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->stream));
       b.tile_list = ctx->d_tiles_bd;
       b.ntiles = ctx->n_tiles_bd;
-      CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->stream));
+      if (b.ntiles)
+        CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->comm_stream));
+      CK(cudaEventRecord(ctx->ev_bd, ctx->comm_stream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_bd, 0));
+      ctx->exchange_pending = false;
+      ctx->fill_pending = false;
     }
   }
   if (flags & F_STAGE0) {
@@ -2007,6 +2047,7 @@ void bf_destroy(bf_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_filled) cudaEventDestroy(ctx->ev_filled);
   if (ctx->ev_unpacked) cudaEventDestroy(ctx->ev_unpacked);
+  if (ctx->ev_bd) cudaEventDestroy(ctx->ev_bd);
   cudaFree(ctx->d_tiles_in);
   cudaFree(ctx->d_tiles_bd);
   delete ctx;
@@ -2460,6 +2501,11 @@ int bf_update_ghosts(bf_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   int rc = ghosts_solo(ctx);
   if (rc) return rc;
+  if (ctx->exchange_pending || ctx->fill_pending) {   // ghosts still landing on comm_stream
+    CK(cudaEventRecord(ctx->ev_unpacked, ctx->comm_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_unpacked, 0));
+    ctx->exchange_pending = ctx->fill_pending = false;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   return BF_OK;
 }
@@ -2483,16 +2529,18 @@ int enqueue_step(bf_ctx* ctx, int step_index) {
 struct StepState {
   int cur, ghost_buf, t_derived;
   long long cur_epoch;
-  bool pushed, psi_valid, other_filled, exchange_pending;
+  bool pushed, psi_valid, other_filled, exchange_pending, fill_pending;
   bool operator==(const StepState& o) const {
     return cur == o.cur && ghost_buf == o.ghost_buf && t_derived == o.t_derived &&
            cur_epoch == o.cur_epoch && pushed == o.pushed && psi_valid == o.psi_valid &&
-           other_filled == o.other_filled && exchange_pending == o.exchange_pending;
+           other_filled == o.other_filled && exchange_pending == o.exchange_pending &&
+           fill_pending == o.fill_pending;
   }
 };
 StepState save_state(const bf_ctx* ctx) {
   return {ctx->cur, ctx->ghost_buf, ctx->t_derived, ctx->cur_epoch,
-          ctx->pushed, ctx->psi_valid, ctx->other_filled, ctx->exchange_pending};
+          ctx->pushed, ctx->psi_valid, ctx->other_filled, ctx->exchange_pending,
+          ctx->fill_pending};
 }
 void load_state(bf_ctx* ctx, const StepState& st) {
   ctx->cur = st.cur;
@@ -2503,6 +2551,7 @@ void load_state(bf_ctx* ctx, const StepState& st) {
   ctx->psi_valid = st.psi_valid;
   ctx->other_filled = st.other_filled;
   ctx->exchange_pending = st.exchange_pending;
+  ctx->fill_pending = st.fill_pending;
 }
 // What a graph-eligible step does to that state: per stage, ghosts of W[cur]
 // then the buffer swap.
