@@ -3,16 +3,21 @@
 Workload at N=1 (BASELINE.json configs[3]): multiblock_box_3d
 level 15 = 256^3 cells in 4 parent blocks, one rank (aggregate -> 4 children),
 Van Leer flux + Van Albada limiter, MUSCL eps=1 kappa=-1, RK2, CFL 0.8,
-farfield M=0.8395, perturbed-freestream initial state.  With --gpus N>1
-(torchrun, one rank per GPU, NCCL halos) the weak-scaling sweep C5 is run:
-256^3 cells per GPU (level 15 + log2 N).
+farfield M=0.8395, perturbed-freestream initial state.  With --gpus N>1, one
+process per GPU (torchrun; started by this script itself when WORLD_SIZE is
+unset), NCCL halos: --scaling weak (default) = C5, 256^3 cells per GPU (level
+15 + log2 N); --scaling strong = C4 (256^3 cells) over N GPUs.
 
 Printed: ONE JSON line (rank 0).  `value` = total interior cells x K RK steps
 / device time of the K steps (CUDA events on the launching stream, barrier +
-synchronize on both sides, max over ranks) / 1e6.  See DESIGN.md §5 for the
-roofline arithmetic and the CPU baseline.
+synchronize on both sides, max over ranks) / 1e6, the median of --repeats
+timed regions of K steps each (spread reported, >1% flagged; the reference's
+bench.py:53-69 rule).  `--impl reference` times the reference package itself
+(blockflow, installed in baseline/_ref) on the host cores on a bounded sample
+of the same workload.  See DESIGN.md §5 for the roofline arithmetic.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--scaling weak|strong]
+                  [--impl reference] [--flux van_leer|roe]
 """
 
 from __future__ import annotations
@@ -106,56 +111,202 @@ def build_case(level, np_ranks, flux="van_leer"):
     return cases.c4_box(level=level, np_ranks=np_ranks, flux=flux, cfl=0.8)
 
 
-def workload_config(level, nranks, ncells, precision, kc):
+def workload_level(n_gpus, scaling):
+    """C4 (level 15 = 256^3 cells) at one GPU and under strong scaling; C5 weak
+    scaling: 256^3 cells per GPU, level 15 + log2 N (bench.py WEAK_GROWTH = 2
+    cells per level step for multiblock_box_3d)."""
+    if n_gpus == 1 or scaling == "strong":
+        return 15
+    return 15 + int(round(math.log2(n_gpus)))
+
+
+def workload_config(n_gpus, scaling, flux="van_leer"):
+    """The `config` object of the line — the same for both arms (the reference
+    arm runs a bounded sample of exactly this workload, described in its
+    cpu_baseline.sample)."""
+    level = workload_level(n_gpus, scaling)
+    cells = 16777216 * 2 ** (level - 15)
+    if n_gpus == 1:
+        name = "C4 multiblock_box_3d L15 (256^3 cells), 1 GPU"
+    elif scaling == "strong":
+        name = f"C4 strong scaling: multiblock_box_3d L15 (256^3 cells) over {n_gpus} GPUs"
+    else:
+        name = f"C5 weak scaling: multiblock_box_3d L{level} ({cells} cells, 256^3 per GPU)"
     return {
-        "workload": ("C4 multiblock_box_3d L15 (256^3 cells), 1 GPU" if nranks == 1 else
-                     f"C5 weak scaling: multiblock_box_3d L{level} ({ncells} cells, 256^3 per GPU)"),
-        "grid_level": level, "cells": ncells, "ranks": nranks,
-        "scheme": "van_leer flux + van_albada limiter, MUSCL eps=1 kappa=-1, RK2, CFL 0.8",
+        "workload": name, "grid_level": level, "cells": cells, "ranks": n_gpus,
+        "scheme": f"{flux} flux + van_albada limiter, MUSCL eps=1 kappa=-1, RK2, CFL 0.8",
         "bcs": "farfield (M=0.8395, alpha=3.06 deg) + connected block interfaces",
-        "init": "freestream with interior rho,p x (1+0.01 N(0,1)), seed 0",
-        "precision": precision, "kc": kc,
+        "init": "freestream with interior rho,p x (1+0.01 N(0,1))",
         "l2": "inputs larger than L2 (device state ~4.6 GB per 256^3 cells vs 126 MB L2)",
-        "parallelism": f"block decomposition over {nranks} rank(s)" + (", NCCL halos" if nranks > 1 else ""),
+        "parallelism": (f"blocks partitioned over {n_gpus} rank(s) (decomp.aggregate / decompose)"
+                        + (", NCCL halos" if n_gpus > 1 else "")),
     }
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle (numpy restatement of the reference) on host cores
+# The reference on the host cores: blockflow itself (baseline/_ref)
 # ---------------------------------------------------------------------------
 
-def cpu_sample(level=9, steps=3, threads=1):
-    """MCUPS of the CPU oracle on multiblock_box_3d L`level` (bounded sample of
-    the same workload: same scheme, BCs and IC).  threads>1 runs the
-    reference's threaded-rank driver (exchange.run_distributed analogue)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def sample_np(level):
+    """The sample's decomposition: children of 64^3 cells (64 at C4's L15)."""
+    return 64 * 2 ** (level - 15)
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "blockflow"))
+
+
+def _ref_modules():
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from blockflow import decomp, halo, mesh, physics, solver
+    return decomp, halo, mesh, physics, solver
+
+
+_SAMPLE = {}
+
+
+def _sample_setup(level, flux):
+    """Reference objects of the workload: grid, 64-child plan, gas, scheme, freestream."""
+    decomp, halo, mesh, physics, solver = _ref_modules()
+    grid = mesh.generate_case_grid("multiblock_box_3d", level)
+    plan = decomp.decompose(grid, sample_np(level), 3)
+    gas = physics.GasModel()
+    fs = solver.FreestreamState.from_mach(gas, 0.8395, 315979.763, 255.556, 3.06, 3)
+    cfg = solver.SchemeConfig(flux=flux, limiter="van_albada", epsilon=1.0, kappa=-1.0,
+                              rk_stages=2, cfl=0.8)
+    _SAMPLE.update(plan=plan, gas=gas, fs=fs, cfg=cfg)
+
+
+def _perturbed(block, fs, gas, seed):
+    rng = np.random.default_rng(seed)
+    f = {n: block.allocate_field(getattr(fs, n)) for n in ("rho", "u", "v", "w", "p", "T")}
+    inner = block.interior()
+    for n in ("rho", "p"):
+        base = f[n][inner]
+        f[n][inner] = base * (1.0 + 0.01 * rng.standard_normal(base.shape))
+    f["T"][inner] = f["p"][inner] / (f["rho"][inner] * gas.R)
+    return f
+
+
+def _sample_worker(cid, nsteps, barrier, errq):
+    """One host core: blockflow's own RankStepper.step on child `cid` of the
+    workload's grid (BlockSolver limiters / MUSCL / flux / residual / dt /
+    RK update, halo.copy_local ghost exchange, physical BCs)."""
+    try:
+        _, halo, _, _, solver = _ref_modules()
+        plan, gas, fs, cfg = (_SAMPLE[k] for k in ("plan", "gas", "fs", "cfg"))
+        s = solver.build_block_solvers(plan, gas, cfg, fs, child_ids=[cid])[cid]
+        s.init_uniform()
+        f = _perturbed(s.block, fs, gas, cid)
+        for n, arr in f.items():
+            s.fields[n][...] = arr
+        s.sync_conserved()
+        # connected ghosts come from the neighbours' initial state (each core
+        # owns one child; the copies themselves are the reference's)
+        links = []
+        for spec in plan.boundaries[cid]:
+            if spec.kind != "connected":
+                continue
+            nb = spec.neighbor_block
+            peer = next(p for p in plan.boundaries[nb] if p.kind == "connected" and
+                        p.link_id == spec.link_id and (nb != cid or p.face != spec.face))
+            blk = plan.child_block(nb)
+            links.append((spec, peer, blk, _perturbed(blk, fs, gas, nb)))
+
+        def exchange(round_no):
+            for spec, peer, blk, fields in links:
+                halo.copy_local(fields, s.fields, spec, peer, blk.dims, blk.ghost,
+                                s.block.dims, s.block.ghost, round_no)
+
+        stepper = solver.RankStepper({cid: s}, exchange, cfg)
+        barrier.wait()
+        for k in range(nsteps):
+            stepper.step(k + 1)
+            barrier.wait()
+    except BaseException as exc:  # noqa: BLE001
+        errq.put(f"child {cid}: {exc!r}")
+        barrier.abort()
+
+
+def reference_sample(level, steps, warmup, flux="van_leer", procs=None):
+    """MCUPS of the reference package (blockflow, baseline/_ref) on the host
+    cores, on a bounded sample of the workload: the workload's grid (level)
+    decomposed into SAMPLE_NP children of equal size, one child per core, each
+    core running blockflow's RankStepper.step on its child; a step ends when
+    every core finished it.  Returns (MCUPS, info)."""
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    _sample_setup(level, flux)
+    plan = _SAMPLE["plan"]
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    procs = procs or max(1, min(ncpu, len(plan.children)))
+    cids = [c.id for c in plan.children][:procs]
+    cells = sum(plan.child_block(c).cell_count() for c in cids)
+    nchild = len(plan.children)
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(procs + 1)
+    errq = ctx.Queue()
+    ps = [ctx.Process(target=_sample_worker, args=(c, warmup + steps, barrier, errq))
+          for c in cids]
+    for p in ps:
+        p.start()
+    try:
+        barrier.wait(timeout=600)                 # every core set up
+        setup = time.perf_counter() - t0
+        for _ in range(warmup):
+            barrier.wait(timeout=600)
+        t1 = time.perf_counter()
+        for _ in range(steps):
+            barrier.wait(timeout=600)
+        dt = time.perf_counter() - t1
+    except Exception as exc:  # noqa: BLE001
+        msg = errq.get() if not errq.empty() else repr(exc)
+        for p in ps:
+            p.kill()
+        raise RuntimeError(f"reference sample failed: {msg}") from exc
+    for p in ps:
+        p.join()
+    child = plan.child_block(cids[0])
+    info = {"cells_per_step": cells, "procs": procs, "steps": steps, "warmup": warmup,
+            "seconds": dt, "setup_s": setup, "child_dims": list(child.dims),
+            "sample": (f"blockflow {_ref_version()} (the reference package, baseline/_ref) "
+                       f"RankStepper.step on {procs} of the {nchild} children "
+                       f"({'x'.join(map(str, child.dims))} cells each) of "
+                       f"multiblock_box_3d L{level} (decomp.decompose, np={nchild}), one child "
+                       f"per host core (forked processes), {steps} timed RK2 steps after "
+                       f"{warmup} warm-up; connected ghosts copied (halo.copy_local) from the "
+                       f"neighbours' initial state; {cells} cells per step; "
+                       f"CPU {cpu_model()}, {ncpu} cores visible")}
+    return cells * steps / dt / 1e6, info
+
+
+def _ref_version():
+    try:
+        from importlib.metadata import version
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        return version("blockflow")
+    except Exception:  # noqa: BLE001
+        return "?"
+
+
+def port_sample(level=11, steps=2, threads=1):
+    """Fallback when baseline/_ref is absent: the oracle port (numpy
+    restatement of the reference) on a smaller grid of the same family."""
     import oracle
-    from paper_2012_02925_b200 import cases, planning
+    from paper_2012_02925_b200 import cases
     plan, sched, gas, cfg, fs, _ = cases.c4_box(level=level, np_ranks=threads)
     ncells = plan.grid.total_cells()
-    blocks = oracle.build_blocks(plan, gas, cfg, fs)
-    rng = np.random.default_rng(0)
-    for cid in sorted(blocks):
-        f = cases.perturbed_state(blocks[cid].block, fs, gas, rng)
-        for n, arr in f.items():
-            blocks[cid].fields[n][...] = arr
-        blocks[cid].sync_conserved()
-    if threads == 1:
-        st = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
-        st.step(1)      # warm-up
-        t0 = time.perf_counter()
-        c0 = os.times()
-        for k in range(steps):
-            st.step(k + 2)
-        dt = time.perf_counter() - t0
-        c1 = os.times()
-    else:
-        c0 = os.times()
-        res = oracle.run_threaded(plan, sched, gas, cfg, fs, steps, init="perturbed", warmup=1)
-        dt = res.solve_seconds
-        c1 = os.times()
-    busy = ((c1.user - c0.user) + (c1.system - c0.system)) / max(dt, 1e-9)
-    return ncells * steps / dt / 1e6, {"cells": ncells, "steps": steps, "seconds": dt,
-                                       "cores_busy": round(busy, 2)}
+    res = oracle.run_threaded(plan, sched, gas, cfg, fs, steps, init="perturbed", warmup=1)
+    dt = res.solve_seconds
+    return ncells * steps / dt / 1e6, {
+        "procs": threads, "sample": f"oracle port (numpy restatement of blockflow, "
+                                    f"{threads} rank threads) on multiblock_box_3d L{level} "
+                                    f"({ncells} cells), {steps} RK2 steps; CPU {cpu_model()}"}
 
 
 def cpu_model():
@@ -173,31 +324,23 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    nthreads = min(os.cpu_count() or 1, 8)
-    level = 9
-    from paper_2012_02925_b200 import cases
-    plan, sched, gas, cfg, fs, _ = cases.c4_box(level=level, np_ranks=nthreads)
-    ncells = plan.grid.total_cells()
-    import oracle
-    # set-up and warm-up steps untimed; timed steps of the threaded reference driver
-    c0 = os.times()
-    res = oracle.run_threaded(plan, sched, gas, cfg, fs, args.steps, init="perturbed",
-                              warmup=args.warmup)
-    c1 = os.times()
-    dt = res.solve_seconds
-    busy = ((c1.user - c0.user) + (c1.system - c0.system)) / max(c1.elapsed - c0.elapsed, 1e-9)
-    value = ncells * args.steps / dt / 1e6
+    level = workload_level(args.gpus, args.scaling)
+    if reference_available():
+        value, info = reference_sample(level, args.steps, args.warmup, args.flux)
+        kind = "reference"
+    else:
+        value, info = port_sample(steps=args.steps)
+        kind = "port"
+    ms = info["seconds"] / args.steps * 1e3 if "seconds" in info else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(15, 1, 16777216, "numpy (reference arithmetic)", None),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
-                         "cores_busy": round(busy, 2),
-                         "sample": f"multiblock_box_3d L{level} ({ncells} cells), {nthreads} "
-                                   f"rank threads (run_distributed analogue), {args.steps} RK2 "
-                                   f"steps; CPU {cpu_model()}"},
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.scaling == "strong" and args.gpus > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.gpus, args.scaling, args.flux),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["procs"], "kind": kind,
+                         "sample": info["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -208,23 +351,69 @@ def run_reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawn_ranks(args):
+    """--gpus N outside a torchrun world: one process per GPU via torchrun."""
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are "
+                         f"visible\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _comm_evidence(plan, rank, world, dist):
+    """Per-rank NCCL facts: remote endpoints and halo bytes per stage."""
+    from paper_2012_02925_b200.distributed import remote_links
+    from paper_2012_02925_b200.topology import halo_regions
+    mine = remote_links(plan, rank)
+    nbytes = 0
+    for cid, spec, _, _ in mine:
+        blk = plan.child_block(cid)
+        send, _ = halo_regions(spec, blk.dims, blk.ghost, 1)
+        nbytes += int(np.prod([hi - lo for lo, hi in send])) * (3 + plan.grid.ndim) * 8
+    rec = {"rank": rank, "peers": sorted({p for _, _, p, _ in mine}), "messages_per_stage": len(mine),
+           "send_bytes_per_stage": nbytes}
+    parts = [None] * world
+    dist.all_gather_object(parts, rec)
+    return {"backend": "nccl", "nranks": world, "per_rank": parts}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--level", type=int, default=None)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = C5 (256^3 cells per GPU), strong = C4 (256^3 in total)")
+    ap.add_argument("--flux", default="van_leer", choices=["van_leer", "roe"])
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="timed regions of K steps each; the line reports the median")
     ap.add_argument("--precision", default="fast", choices=["fast", "exact"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4"],
-                    help="c4 (default, BASELINE configs[3]) is the bench line; c1-c3 are "
+                    help="c4 (default, BASELINE configs[3]/[4]) is the bench line; c1-c3 are "
                          "informational runs of the other BASELINE configs on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn_ranks(args)
     args.warmup = max(args.warmup, 3)
+    args.repeats = max(args.repeats, 1)
 
     import torch
     from paper_2012_02925_b200 import stepper
@@ -232,6 +421,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} device(s) visible")
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -239,9 +433,9 @@ def main():
         dist.init_process_group("nccl", init_method="env://")
     else:
         torch.cuda.set_device(0)
-    level = args.level if args.level is not None else 15 + int(round(math.log2(world)))
+    level = workload_level(world, args.scaling)
     if args.workload == "c4":
-        plan, sched, gas, cfg, fs, init = build_case(level, world)
+        plan, sched, gas, cfg, fs, init = build_case(level, world, args.flux)
     else:
         from paper_2012_02925_b200 import cases
         if world > 1:
@@ -258,6 +452,7 @@ def main():
     t_setup = time.perf_counter() - t_setup
     gpu = stepper.GpuContext(plan, my_children, gas, cfg, fs, device=local, rank=rank,
                              nranks=world, precision=args.precision, setups=setups)
+    comm = None
     if world > 1:
         import ctypes as C
         box = [None]
@@ -267,58 +462,59 @@ def main():
             box = [bytes(buf.raw)]
         dist.broadcast_object_list(box, src=0)
         gpu._check(gpu.L.bf_nccl_init(gpu.ctx, (C.c_char * 128).from_buffer_copy(box[0])))
+        comm = _comm_evidence(plan, rank, world, dist)
     gpu.upload_initial(init)
     stream = torch.cuda.current_stream()
     gpu.set_stream(stream.cuda_stream)
     st = stepper.GpuRankStepper(gpu, cfg)
 
-    for k in range(args.warmup):
-        st.step(k + 1)
+    first = 1
+    st.run(first, args.warmup)
+    first += args.warmup
     gpu.set_profiling(True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
     with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        # the drop-in's step loop (iterate_gpu): steps driven from C, each one
-        # returning its residual norms to the host
-        done = len(st.run(args.warmup + 1, args.steps))
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if done != args.steps:
-        raise SystemExit(f"bench: the history guard stopped the run after {done} steps")
-    if dist:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    stats = {cls: gpu.kernel_stats(cls) for cls in range(4)}
+        for _ in range(args.repeats):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            # the drop-in's step loop (iterate_gpu): steps driven from C, each one
+            # returning its residual norms to the host
+            done = len(st.run(first, args.steps))
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if done != args.steps:
+                raise SystemExit(f"bench: the history guard stopped the run after {done} steps")
+            first += args.steps
+            if dist:
+                dist.barrier()
+            ms = ev0.elapsed_time(ev1)
+            if dist:
+                t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            times.append(ms)
+    ms = statistics.median(times)
+    spread = (max(times) - min(times)) / ms
+    stats = {cls: gpu.kernel_stats(cls) for cls in range(5)}
     gpu.set_profiling(False)
     value = ncells * args.steps / (ms / 1e3) / 1e6
     n_stage, ms_stage = stats[0]
-    launches = sum(n for n, _ in stats.values())
+    launches_per_region = stats[4][0] / args.repeats
     peak, peak_kind = _peaks()
-    alg_bytes = (ALG_BYTES_3D if plan.grid.ndim == 3 else ALG_BYTES_2D) * my_cells
+    B = ALG_BYTES_3D if plan.grid.ndim == 3 else ALG_BYTES_2D
+    alg_bytes = B * my_cells
     avg_stage_s = ms_stage / max(n_stage, 1) / 1e3
     achieved = alg_bytes / avg_stage_s / 1e9
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "stage_kernel_traffic.json")
-    if os.path.exists(prof_path):
-        try:
-            with open(prof_path) as f:
-                pj = json.load(f)
-            if pj.get("cells") == my_cells and pj.get("precision") == args.precision:
-                traffic = pj.get("dram_bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            traffic = None
+    traffic, traffic_src = measured_traffic(my_cells, args.precision, args.flux)
 
-    # e2e through the public API with host buffers (rank 0 / N=1 only)
-    # the measured context is done: release it before the end-to-end run builds its own
-    # (its block arenas are then recycled instead of mapped afresh by the driver)
+    # e2e through the public API with host buffers: the measured context is
+    # released first, and so is the arena cache — the e2e context pays the cold
+    # device allocation a first-time caller of iterate_gpu pays
     gpu.close()
+    stepper.native.lib().bf_release_cache(-1)
     e2e = None
     if not args.skip_e2e:
         e2e = e2e_run(plan, my_children, gas, cfg, fs, init, local, rank, world, args, dist,
@@ -326,47 +522,90 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        v, info = cpu_sample(level=11, steps=3, threads=1)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"CPU oracle (numpy restatement of blockflow.solver.iterate, 1 thread) "
-                         f"on multiblock_box_3d L11 ({info['cells']} cells, same scheme/BCs/IC), "
-                         f"{info['steps']} timed RK2 steps after 1 warm-up, {info['seconds']:.1f} s; "
-                         f"CPU {cpu_model()}"}
+        if reference_available():
+            v, info = reference_sample(level, 2, 1, args.flux)
+            kind = "reference"
+        else:
+            v, info = port_sample()
+            kind = "port"
+        cpu = {"value": v, "unit": UNIT, "cores": info["procs"], "kind": kind,
+               "sample": info["sample"]}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": (workload_config(level, world, ncells, args.precision, gpu_kc())
+            "scaling": "strong" if args.scaling == "strong" and world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": (workload_config(world, args.scaling, args.flux)
                        if args.workload == "c4" else
                        {"workload": {"c1": "C1 inlet ramp 2D 128x64, 1 block",
                                      "c2": "C2 ramp channel 2D 4 x 512x256 connected blocks",
                                      "c3": "C3 3D MMS cube 128^3 (Roe, no limiter), one block"
                                      }[args.workload] + " (informational)",
-                        "cells": ncells, "precision": args.precision}),
+                        "cells": ncells}),
+            "build": {"precision": args.precision, "kc": gpu_kc(), "flux": args.flux,
+                      "lib": "paper_2012_02925_b200/libbfgpu.so (sm_100a)",
+                      "sources_sha": sources_sha()},
+            "repeats": {"n": args.repeats, "ms": times, "median_ms": ms,
+                        "spread": spread, "spread_over_1pct": spread > 0.01},
             "residual_evals_per_s": value * 1e6 * cfg.rk_stages,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_source": peak_kind,
-                         "kernel": "stage_kernel (fused limiter+MUSCL+flux+residual+dt+RK update)",
+                         "kernel": "stage kernel (fused limiter+MUSCL+flux+residual+dt+RK update)",
                          "alg_bytes_per_launch": alg_bytes,
+                         "alg_bytes_per_cell": B,
                          "avg_launch_ms": avg_stage_s * 1e3,
-                         "stage_share_of_step": ms_stage / max(ms, 1e-9)},
-            "step_roofline_frac": (value * 1e6 * 2 * (ALG_BYTES_3D if plan.grid.ndim == 3 else ALG_BYTES_2D)
-                                   / world / 1e9) / peak,
-            "kernel_ms": {"stage": ms_stage, "ghost_fill": stats[1][1], "unpack": stats[2][1],
-                          "reduce": stats[3][1]},
-            "gpu_launches": launches,
+                         "stage_share_of_step": ms_stage / args.repeats / max(ms, 1e-9)},
+            "step_roofline_frac": (value * 1e6 * cfg.rk_stages * B / world / 1e9) / peak,
+            "kernel_ms_per_region": {"stage": ms_stage / args.repeats,
+                                     "ghost_fill": stats[1][1] / args.repeats,
+                                     "unpack": stats[2][1] / args.repeats,
+                                     "reduce": stats[3][1] / args.repeats},
+            "gpu_launches": int(round(launches_per_region)),
             "host_setup_s": t_setup,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if comm:
+            line["comm"] = comm
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def sources_sha():
+    """Hash of the CUDA sources the library was built from (ties an ncu traffic
+    capture to the build it measured)."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2012_02925_b200", "csrc")
+    for name in sorted(os.listdir(csrc)):
+        with open(os.path.join(csrc, name), "rb") as f:
+            h.update(name.encode() + f.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(cells, precision, flux):
+    """DRAM bytes per stage-kernel launch from the ncu --set full capture of
+    THIS build (profiles/stage_kernel_traffic.json records the sources hash it
+    was captured from); None when the capture is of another build."""
+    path = os.path.join(ROOT, "profiles", "stage_kernel_traffic.json")
+    try:
+        with open(path) as f:
+            pj = json.load(f)
+    except Exception:  # noqa: BLE001
+        return None, "no capture"
+    if pj.get("cells") != cells or pj.get("precision") != precision or \
+            pj.get("flux", "van_leer") != flux:
+        return None, "capture of another workload"
+    if pj.get("sources_sha") != sources_sha():
+        return None, f"capture of another build ({pj.get('sources_sha')})"
+    return pj.get("dram_bytes_per_launch"), pj.get("source")
 
 
 def gpu_kc():

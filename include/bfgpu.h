@@ -246,7 +246,10 @@ int bf_group_step(bf_group* grp, int step_index, double* sumsq_out, int* failed_
    caller's CUDA events bracket the work; NULL restores the ctx's own stream. */
 int bf_set_stream(bf_ctx* ctx, void* cuda_stream);
 /* Per-kernel-class CUDA-event timing: enable, then read {launches, total_ms}
-   for class 0 = stage kernel, 1 = ghost/pack kernel, 2 = unpack, 3 = reduce. */
+   for class 0 = stage kernel (an interior/boundary split stage counts once, its span
+   from the first launch to the join of both), 1 = ghost/pack kernel, 2 = unpack (and the
+   viscous face-flux kernel), 3 = reduce; class 4 = every kernel launch inside those
+   scopes (launches) and the sum of the four classes (total_ms). */
 int bf_set_profiling(bf_ctx* ctx, int on);
 int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* total_ms);
 /* Device bytes the last bf_upload_fields / bf_download moved (for e2e accounting). */

@@ -415,6 +415,7 @@ struct HostBlock {
 struct TimerPair {
   cudaEvent_t a, b;
   int cls;
+  int kernels = 1;               // kernel launches inside the timed scope
   bool owned_by_graph = false;   // recorded by a captured step: not returned to the pool
 };
 
@@ -525,6 +526,7 @@ struct bf_ctx {
   std::vector<TimerPair> pending;
   std::vector<cudaEvent_t> event_pool;
   long long prof_launches[4] = {0, 0, 0, 0};
+  long long prof_kernels = 0;      // kernel launches in all timed scopes
   double prof_ms[4] = {0, 0, 0, 0};
   long long bytes_h2d = 0, bytes_d2h = 0;
 };
@@ -731,6 +733,7 @@ cudaEvent_t take_event(bf_ctx* ctx) {
 struct ProfScope {
   bf_ctx* ctx;
   int cls;
+  int kernels = 1;
   cudaEvent_t a = nullptr;
   ProfScope(bf_ctx* c, int k) : ctx(c), cls(k) {
     if (ctx->profiling) {
@@ -747,7 +750,7 @@ struct ProfScope {
     if (ctx->profiling) {
       cudaEvent_t b = take_event(ctx);
       record(b);
-      ctx->pending.push_back({a, b, cls});
+      ctx->pending.push_back({a, b, cls, kernels});
     }
   }
 };
@@ -758,6 +761,7 @@ void drain_profile(bf_ctx* ctx) {
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
       ctx->prof_ms[p.cls] += ms;
       ctx->prof_launches[p.cls] += 1;
+      ctx->prof_kernels += p.kernels;
     }
     if (!p.owned_by_graph) {
       ctx->event_pool.push_back(p.a);
@@ -1789,6 +1793,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
       b.ntiles = ctx->n_tiles_bd;
       if (b.ntiles)
         CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, b, ctx->comm_stream));
+      ps.kernels = (ctx->n_tiles_in > 0) + (ctx->n_tiles_bd > 0);
       CK(cudaEventRecord(ctx->ev_bd, ctx->comm_stream));
       CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_bd, 0));
       ctx->exchange_pending = false;
@@ -3096,14 +3101,20 @@ int bf_set_profiling(bf_ctx* ctx, int on) {
     ctx->prof_launches[k] = 0;
     ctx->prof_ms[k] = 0.0;
   }
+  ctx->prof_kernels = 0;
   return BF_OK;
 }
 
 int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* total_ms) {
-  if (!ctx || kernel_class < 0 || kernel_class > 3) return BF_EINVAL;
+  if (!ctx || kernel_class < 0 || kernel_class > 4) return BF_EINVAL;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   drain_profile(ctx);
+  if (kernel_class == 4) {   // every kernel launched inside a timed scope
+    *launches = ctx->prof_kernels;
+    *total_ms = ctx->prof_ms[0] + ctx->prof_ms[1] + ctx->prof_ms[2] + ctx->prof_ms[3];
+    return BF_OK;
+  }
   *launches = ctx->prof_launches[kernel_class];
   *total_ms = ctx->prof_ms[kernel_class];
   return BF_OK;

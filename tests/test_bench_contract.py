@@ -1,6 +1,8 @@
 """bench.py keeps the driver's JSON-line contract.
 
-CPU: the reference arm (`--impl reference`, the oracle on the host cores).
+CPU: the reference arm (`--impl reference`: the reference package from
+baseline/_ref on the host cores, on a sample of the same workload), the
+config object shared by both arms, --gpus N failing loudly without N GPUs.
 GPU: the native arm on the C4 workload, short run."""
 
 import json
@@ -27,6 +29,9 @@ def _run(args, timeout):
 
 def test_reference_arm_line():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], 600)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.workload_config(1, "weak")   # the native arm's config
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "MCUPS"
     cb = d["cpu_baseline"]
@@ -36,9 +41,30 @@ def test_reference_arm_line():
                         "d2h_bytes_per_step": 0}
 
 
+def test_config_shared_and_sized():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.workload_config(1, "weak")["cells"] == 256 ** 3
+    assert bench.workload_config(8, "weak")["cells"] == 8 * 256 ** 3     # C5: L18
+    assert bench.workload_config(8, "strong")["cells"] == 256 ** 3       # C4 over 8
+    assert bench.workload_level(4, "weak") == 17 and bench.sample_np(17) == 256
+
+
+def test_multi_gpu_request_fails_loudly_without_gpus():
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("two GPUs visible: the spawn path would run")
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "1"], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode != 0 and "only" in out.stderr and "visible" in out.stderr
+
+
 @pytest.mark.gpu
 def test_native_arm_line():
-    d = _run(["--steps", "3", "--warmup", "3", "--skip-cpu"], 900)
+    d = _run(["--steps", "3", "--warmup", "3", "--skip-cpu", "--repeats", "3"], 900)
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["higher_is_better"] is True and d["dtype"] == "f64"
@@ -50,3 +76,8 @@ def test_native_arm_line():
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert "workload" in d["config"]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.workload_config(1, "weak")
+    rep = d["repeats"]
+    assert rep["n"] >= 3 and len(rep["ms"]) == rep["n"] and rep["median_ms"] > 0
