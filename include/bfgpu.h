@@ -261,6 +261,13 @@ long long bf_transfer_bytes(const bf_ctx* ctx, int direction /*0 h2d, 1 d2h*/);
    driver: device >= 0 one device, < 0 all. */
 void bf_release_cache(int device);
 
+/* Host-only probe (no GPU needed): the order in which a rank issues its remote
+   endpoints' messages inside one NCCL group (remote_links_sorted: by peer rank,
+   then link tag, then own block id).  order_out[q] = index into the inputs of
+   the q-th message.  Used by the CPU tests against distributed.remote_links. */
+int bf_probe_remote_order(int n, const int* peer_rank, const int* tag, const int* block,
+                          int* order_out);
+
 /* Host-only lowering probe (no GPU needed): the affine index map the device
    unpack applies for one connected endpoint — for each recv-box cell (i-fastest,
    count = product of recv extents), the partner-send-box linear index it reads.

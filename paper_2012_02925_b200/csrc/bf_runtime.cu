@@ -1613,14 +1613,22 @@ int launch_unpack(bf_ctx* ctx) {
   return BF_OK;
 }
 
+// Message issue order of a rank's remote endpoints: (peer rank, link tag, own
+// block id) — both endpoints of a link see the same (tag) and their peer's
+// rank, so NCCL pairs each send with the matching receive.  Mirrored by
+// distributed.remote_links (checked by tests/test_abi.py via bf_probe_remote_order).
+bool remote_before(int peer_a, int tag_a, int block_a, int peer_b, int tag_b, int block_b) {
+  if (peer_a != peer_b) return peer_a < peer_b;
+  if (tag_a != tag_b) return tag_a < tag_b;
+  return block_a < block_b;
+}
+
 std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx) {
   std::vector<HostLink*> out;
   for (auto& L : ctx->links)
     if (L.send) out.push_back(&L);
-  std::sort(out.begin(), out.end(), [](const HostLink* a, const HostLink* b) {
-    if (a->peer_rank != b->peer_rank) return a->peer_rank < b->peer_rank;
-    if (a->tag != b->tag) return a->tag < b->tag;
-    return a->block < b->block;
+  std::stable_sort(out.begin(), out.end(), [](const HostLink* a, const HostLink* b) {
+    return remote_before(a->peer_rank, a->tag, a->block, b->peer_rank, b->tag, b->block);
   });
   return out;
 }
@@ -3136,6 +3144,18 @@ void bf_release_cache(int device) {
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction) {
   if (!ctx) return -1;
   return direction == 0 ? ctx->bytes_h2d : ctx->bytes_d2h;
+}
+
+int bf_probe_remote_order(int n, const int* peer_rank, const int* tag, const int* block,
+                          int* order_out) {
+  if (n < 0 || (n > 0 && (!peer_rank || !tag || !block || !order_out))) return BF_EINVAL;
+  std::vector<int> idx(n);
+  for (int q = 0; q < n; ++q) idx[q] = q;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    return remote_before(peer_rank[a], tag[a], block[a], peer_rank[b], tag[b], block[b]);
+  });
+  for (int q = 0; q < n; ++q) order_out[q] = idx[q];
+  return BF_OK;
 }
 
 int bf_probe_unpack_map(const int own_dims[3], int ghost_depth, int ndim, int face,

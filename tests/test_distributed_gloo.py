@@ -181,3 +181,31 @@ def test_rank_ordered_sum_matches_reference_fabric(ref):
     [t.join() for t in ts]
     from paper_2012_02925_b200 import distributed as D
     np.testing.assert_array_equal(D.rank_ordered_sum(parts), res[0])
+
+
+def test_cpp_remote_order_matches_python():
+    """The C++ issue order (remote_links_sorted, exercised through
+    bf_probe_remote_order on the endpoints in GpuContext's bf_add_link order)
+    equals distributed.remote_links — the order the gloo runs above use."""
+    import ctypes as C
+    from paper_2012_02925_b200 import cases, geometry, native
+    from paper_2012_02925_b200 import distributed as D
+    L = native.lib()
+    for grid, npr in ((geometry.multiblock_box_3d(2), 8), (geometry.c_annulus_2d(1), 4),
+                      (geometry.multiblock_box_3d(1), 3), (geometry.multiblock_box_3d(3), 2)):
+        plan = cases.make_plan(grid, npr)
+        for r in range(plan.np_ranks):
+            added = []   # (cid, spec, peer_rank, tag) in bf_add_link call order
+            for c in sorted(plan.rank_children(r), key=lambda c: c.id):
+                for s in plan.boundaries[c.id]:
+                    if s.kind == "connected" and plan.child(s.neighbor_block).rank != r:
+                        added.append((c.id, s, plan.child(s.neighbor_block).rank,
+                                      int(s.link_id)))
+            n = len(added)
+            out = (C.c_int * max(n, 1))()
+            assert L.bf_probe_remote_order(n, native.ints([a[2] for a in added]),
+                                           native.ints([a[3] for a in added]),
+                                           native.ints([a[0] for a in added]), out) == 0
+            got = [(added[out[q]][0], added[out[q]][2], added[out[q]][3]) for q in range(n)]
+            want = [(cid, peer, tag) for cid, _, peer, tag in D.remote_links(plan, r)]
+            assert got == want, (r, got, want)
