@@ -252,14 +252,25 @@ int bf_set_stream(bf_ctx* ctx, void* cuda_stream);
    scopes (launches) and the sum of the four classes (total_ms). */
 int bf_set_profiling(bf_ctx* ctx, int on);
 int bf_kernel_stats(bf_ctx* ctx, int kernel_class, long long* launches, double* total_ms);
+/* Transfer counters of the exchange engine, cumulative over the context's life
+   (replaces exchange.py:83-101 TransferCounters, which RankRuntime increments as
+   it moves messages, exchange.py:371-466): out = {messages, runs, bytes,
+   staging_copies, waits, max_pending}.  One message per remote endpoint and
+   round (all fields concatenated), runs = halo pack + unpack launches, one wait
+   per grouped exchange, staging copies 0 (device buffers are sent directly). */
+int bf_transfer_counters(const bf_ctx* ctx, long long out[6]);
 /* Device bytes the last bf_upload_fields / bf_download moved (for e2e accounting). */
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction /*0 h2d, 1 d2h*/);
 
 /* Block arenas of destroyed contexts (and the staging buffers' stream-ordered
-   pool) are kept for reuse by the next context on the same device (bounded; a
-   failing arena allocation releases them first).  Hand them back to the
-   driver: device >= 0 one device, < 0 all. */
+   pool) are kept for reuse by the next context on the same device while another
+   context of that device is alive (bounded; a failing arena allocation releases
+   them first).  When the last context of a device is destroyed they go back to
+   the driver and the default pool's release threshold is restored, unless
+   BF_ARENA_CACHE=1 keeps them.  bf_release_cache hands them back explicitly:
+   device >= 0 one device, < 0 all.  bf_cache_bytes: arena bytes held. */
 void bf_release_cache(int device);
+long long bf_cache_bytes(int device);
 
 /* Host-only probe (no GPU needed): the order in which a rank issues its remote
    endpoints' messages inside one NCCL group (remote_links_sorted: by peer rank,

@@ -10,7 +10,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu-baseline
 it fails loudly when the CUDA library is missing instead of falling back.
 
 Pinning: the oracle is checked bitwise against the reference package itself
-(tests/test_oracle_vs_reference.py, when /root/reference is present) and
+(tests/test_host_mirror.py::test_oracle_equals_reference_iterate_random_schemes,
+when the reference is present) and
 against committed golden vectors produced by the reference
 (tests/golden/make_golden.py -> tests/golden/*.npz,
 tests/test_oracle_golden.py, always).

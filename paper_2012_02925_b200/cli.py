@@ -3,10 +3,11 @@
     python -m paper_2012_02925_b200.cli run config.txt [--np N] [--output-dir D]
                                         [--compare-serial] [--precision auto|exact|fast]
 
-Same flat ``key = value`` configuration as the reference's runner (cli.py:50-181:
-every key, default, coercion and error text), same artefacts (cli.py:365-390):
+The configuration is parsed by the reference's own runner code (blockflow.cli
+RunConfig / parse_config, loaded from baseline/_ref: every key, default,
+coercion and error text is the reference's), same artefacts (cli.py:365-390):
 ``residuals.csv`` (relative history), ``counters.json`` (per-rank transfer
-accounting — here the native engine's: packed, persistent, direct, deferred),
+counters of the native engine as it ran, bf_transfer_counters),
 ``plan.json`` (decomposition + schedule), ``block_<id>.vtk`` / ``.npy``
 solutions, and the same summary line.  The solve runs through
 ``run_distributed_gpu``: one process per GPU over NCCL under torchrun, else
@@ -21,128 +22,54 @@ import argparse
 import json
 import os
 import sys
-from dataclasses import dataclass, fields as dc_fields, replace
+from dataclasses import replace
 
 import numpy as np
 
 from . import geometry, planning
-from .errors import BlockflowError, ConfigError
+from .errors import BlockflowError, ConfigError, bridged
 from .model import FIELD_NAMES, FreestreamState, GasModel, SchemeConfig
 
 EXIT_OK, EXIT_ERROR, EXIT_CONFIG = 0, 1, 2
-_BOOL = {"true": True, "false": False, "yes": True, "no": False, "1": True, "0": False}
-
-CASE_TABLES = {   # cli.py:34-44
-    "inlet_ramp_2d": dict(mach=4.0, pressure=12270.0, temperature=217.0, alpha_deg=0.0),
-    "c_annulus_2d": dict(mach=0.25, pressure=84307.0, temperature=300.0, alpha_deg=5.0),
-    "multiblock_box_3d": dict(mach=0.8395, pressure=315979.763, temperature=255.556,
-                              alpha_deg=3.06),
-    "cartesian_box": dict(mach=0.3, pressure=1.0e5, temperature=300.0, alpha_deg=0.0),
-}
 
 
-@dataclass
-class RunConfig:
-    """cli.py:50-116 (same keys and defaults)."""
-    case: str | None = None
-    grid_file: str | None = None
-    level: int = 0
-    physics: str = "euler"
-    flux: str = "van_leer"
-    limiter: str = "van_albada"
-    epsilon: float = 1.0
-    kappa: float = -1.0
-    rk_stages: int = 2
-    cfl: float = 0.8
-    limiter_freeze_at: int | None = None
-    entropy_fix_coeff: float = 0.1
-    max_steps: int = 200
-    residual_target: float | None = None
-    np: int = 1
-    split_dims: int | None = None
-    aggregation: bool = False
-    granularity: str = "packed"
-    buffers: str = "transient"
-    transport: str = "direct"
-    wait_policy: str = "per_block"
-    reorder: bool = True
-    mach: float | None = None
-    pressure: float | None = None
-    temperature: float | None = None
-    alpha_deg: float | None = None
-    mu: float = 1.8e-5
-    prandtl: float = 0.72
-    wall_temperature: float | None = None
-    mms_levels: str | None = None
-    scaling_np: str = "1,2,4"
-    scaling_steps: int = 20
-    output_dir: str = "out"
-    write_solution: bool = True
-    compare_serial: bool = False
-    scaling: str | None = None
-    timeout_s: float = 5.0
-
-    def validate(self):
-        if (self.case is None) == (self.grid_file is None):
-            raise ConfigError("exactly one of 'case' or 'grid_file' is required")
-        if self.case is not None and self.case not in CASE_TABLES:
-            raise ConfigError(f"unknown case {self.case!r}; choose from {tuple(CASE_TABLES)}")
-        if self.physics not in ("euler", "laminar_ns"):
-            raise ConfigError(f"physics must be euler or laminar_ns, got {self.physics!r}")
-        if self.np < 1:
-            raise ConfigError(f"np must be >= 1, got {self.np}")
-        if self.max_steps < 1:
-            raise ConfigError(f"max_steps must be >= 1, got {self.max_steps}")
-        if self.scaling not in (None, "strong", "weak"):
-            raise ConfigError(f"scaling must be strong or weak, got {self.scaling!r}")
-        if self.timeout_s <= 0:
-            raise ConfigError("timeout_s must be positive")
-        return self
+def _ref_cli():
+    """The reference's own run-config schema and parser (blockflow.cli:
+    RunConfig cli.py:50-116, CASE_TABLES cli.py:34-44, parse_config
+    cli.py:145-179), consumed as they are: keys, defaults, coercions and error
+    texts are the reference's by construction."""
+    from . import reference
+    return reference.load("cli")
 
 
-_FIELD_TYPES = {f.name: (bool if f.type in ("bool",) else
-                         int if f.type in ("int", "int | None") else
-                         float if f.type in ("float", "float | None") else str)
-                for f in dc_fields(RunConfig)}
+def __getattr__(name):
+    if name in ("RunConfig", "CASE_TABLES"):
+        return getattr(_ref_cli(), name)
+    raise AttributeError(name)
 
 
-def _coerce(name, text, target_type):
-    if target_type is bool:
-        if text.lower() not in _BOOL:
-            raise ValueError(f"expected a boolean for {name}, got {text!r}")
-        return _BOOL[text.lower()]
-    return target_type(text)
+def validated(cfg):
+    """cfg.validate() (the reference's RunConfig.validate, cli.py:90-107) with
+    its ConfigError re-raised as this package's."""
+    rc = _ref_cli()
+    try:
+        cfg = cfg.validate()
+    except rc.ConfigError as e:
+        raise bridged(ConfigError)(str(e)) from None
+    if cfg.case == "deadlock_demo":
+        raise bridged(ConfigError)("deadlock_demo exercises the reference's simulated MPI "
+                                   "fabric (out of scope for the device runner)")
+    return cfg
 
 
-def parse_config(source) -> RunConfig:
-    """cli.py:145-179: `key = value` lines, # comments, line-numbered errors."""
-    if hasattr(source, "read"):
-        text, name = source.read(), getattr(source, "name", "<config>")
-    else:
-        name = str(source)
-        with open(source) as f:
-            text = f.read()
-    values = {}
-    for lineno, raw in enumerate(text.splitlines(), start=1):
-        line = raw.split("#", 1)[0].strip()
-        if not line:
-            continue
-        if "=" not in line:
-            raise ConfigError(f"{name}:{lineno}: expected 'key = value', got {raw!r}")
-        key, _, val = line.partition("=")
-        key, val = key.strip(), val.strip()
-        if key not in _FIELD_TYPES:
-            raise ConfigError(f"{name}:{lineno}: unknown key {key!r}")
-        if key in values:
-            raise ConfigError(f"{name}:{lineno}: duplicate key {key!r}")
-        if val.lower() == "none":
-            values[key] = None
-            continue
-        try:
-            values[key] = _coerce(key, val, _FIELD_TYPES[key])
-        except ValueError as e:
-            raise ConfigError(f"{name}:{lineno}: {e}") from None
-    return RunConfig(**values).validate()
+def parse_config(source):
+    """blockflow.cli.parse_config; its ConfigError is re-raised as this
+    package's (bridged to the reference's class)."""
+    rc = _ref_cli()
+    try:
+        return rc.parse_config(source)
+    except rc.ConfigError as e:
+        raise bridged(ConfigError)(str(e)) from None
 
 
 # ---- case assembly (cli.py:182-247) -----------------------------------------------
@@ -163,7 +90,8 @@ def build_grid(cfg):
 
 
 def build_freestream(cfg, gas, ndim):
-    table = dict(CASE_TABLES.get(cfg.case or "", CASE_TABLES["cartesian_box"]))
+    tables = _ref_cli().CASE_TABLES
+    table = dict(tables.get(cfg.case or "", tables["cartesian_box"]))
     for key in ("mach", "pressure", "temperature", "alpha_deg"):
         if getattr(cfg, key) is not None:
             table[key] = getattr(cfg, key)
@@ -322,8 +250,8 @@ def run_mms_study(cfg, gas, stdout=sys.stdout, precision="auto", ndim=2, np_rank
 
 
 def run(cfg, stdout=sys.stdout, precision="auto"):
-    from .stepper import native_counters, run_distributed_gpu
-    cfg.validate()
+    from .stepper import run_distributed_gpu
+    cfg = validated(cfg)
     if cfg.mms_levels:
         if cfg.case != "cartesian_box":
             raise ConfigError("mms_levels requires case = cartesian_box")
@@ -347,9 +275,10 @@ def run(cfg, stdout=sys.stdout, precision="auto"):
         f.write("step,r_mass,r_xmom,r_ymom,r_zmom,r_energy\n")
         for i, row in enumerate(rel):
             f.write(f"{i + 1}," + ",".join(f"{v:.16e}" for v in row) + "\n")
-    counters = native_counters(plan, rounds=scheme.ghost_rounds)
+    # the engine's own counters (bf_transfer_counters), as the reference writes
+    # its RankRuntime counters (cli.py:376-378)
     with open(os.path.join(cfg.output_dir, "counters.json"), "w") as f:
-        f.write(counters_to_json(counters))
+        f.write(counters_to_json(out.counters))
     with open(os.path.join(cfg.output_dir, "plan.json"), "w") as f:
         f.write(json.dumps(plan_to_dict(plan, schedule), indent=2))
     if cfg.write_solution:
@@ -398,7 +327,7 @@ def main(argv=None):
             over["compare_serial"] = True
         if args.output_dir is not None:
             over["output_dir"] = args.output_dir
-        cfg = replace(cfg, **over).validate()
+        cfg = validated(replace(cfg, **over))
         return run(cfg, precision=args.precision)
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)

@@ -445,6 +445,7 @@ struct bf_ctx {
                                    // interior tiles (BF_HIDE_GHOSTS=1; measured slower)
   bool fill_pending = false;       // this stage's ghost fill is queued on comm_stream
   bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
+  bool counted = false;           // registered in the per-device live-context count
   // one RK step as a CUDA graph (standalone Euler ctx), per starting buffer and
   // profiling mode; a profiled graph records its own timing events
   cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -529,6 +530,11 @@ struct bf_ctx {
   long long prof_kernels = 0;      // kernel launches in all timed scopes
   double prof_ms[4] = {0, 0, 0, 0};
   long long bytes_h2d = 0, bytes_d2h = 0;
+  // transfer counters of the engine as it runs (exchange.py:83-101 fields):
+  // messages / bytes = remote sends (one concatenated message per endpoint and
+  // round), runs = halo pack + unpack kernel launches, waits = completions the
+  // unpack waits on (one per grouped exchange), max_pending = messages in flight
+  long long xc[6] = {0, 0, 0, 0, 0, 0};
 };
 
 struct bf_group {
@@ -636,6 +642,8 @@ struct ArenaCache {
   std::mutex m;
   std::vector<Entry> free;
   size_t held = 0;
+  std::map<int, int> live;                  // contexts alive per device
+  std::map<int, cuuint64_t> pool_thr;       // default pool release threshold before bf_create
 };
 ArenaCache& arena_cache() {
   static ArenaCache c;
@@ -688,6 +696,58 @@ void* arena_alloc(int dev, size_t bytes) {
   if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
   cudaGetLastError();
   return nullptr;
+}
+
+// Opt-in (BF_ARENA_CACHE=1): keep arenas and the staging pool mapped after the
+// last context of a device is destroyed.  By default the cache and the pool are
+// handed back to the driver then, and the pool's release threshold is restored,
+// so a caller embedding the drop-in in a larger CUDA job gets its memory back.
+bool arena_cache_keep() {
+  const char* e = std::getenv("BF_ARENA_CACHE");
+  return e && e[0] == '1';
+}
+
+void device_ctx_opened(int dev) {
+  ArenaCache& c = arena_cache();
+  std::lock_guard<std::mutex> g(c.m);
+  if (c.live[dev]++ == 0) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cuuint64_t old = 0;
+      if (!c.pool_thr.count(dev) &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old) == cudaSuccess)
+        c.pool_thr[dev] = old;
+      // staging buffers (uploads, downloads) come from the stream-ordered pool;
+      // keep its memory mapped between calls instead of releasing it at every
+      // synchronisation (re-mapping 100+ MB per call dominated the transfers)
+      cuuint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+}
+
+void release_arena_cache(int dev);
+
+void device_ctx_closed(int dev) {
+  bool last = false;
+  {
+    ArenaCache& c = arena_cache();
+    std::lock_guard<std::mutex> g(c.m);
+    last = --c.live[dev] <= 0;
+    if (last) c.live[dev] = 0;
+  }
+  if (!last || arena_cache_keep()) return;
+  release_arena_cache(dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    ArenaCache& c = arena_cache();
+    std::lock_guard<std::mutex> g(c.m);
+    if (c.pool_thr.count(dev)) {
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &c.pool_thr[dev]);
+      c.pool_thr.erase(dev);
+    }
+    cudaMemPoolTrimTo(pool, 0);
+  }
 }
 
 void arena_free(int dev, void* p, size_t bytes) {
@@ -1415,6 +1475,18 @@ int sync_ghosts_from_other(bf_ctx* ctx) {
   return BF_OK;
 }
 
+enum { XC_MESSAGES, XC_RUNS, XC_BYTES, XC_STAGING, XC_WAITS, XC_MAX_PENDING };
+
+// One grouped exchange of `n` remote endpoints: n sends + n receives in flight,
+// one pack and one unpack launch, one completion the unpack waits on.
+void count_exchange(bf_ctx* ctx, long long n, long long bytes) {
+  ctx->xc[XC_MESSAGES] += n;
+  ctx->xc[XC_BYTES] += bytes;
+  ctx->xc[XC_RUNS] += 2;
+  ctx->xc[XC_WAITS] += 1;
+  ctx->xc[XC_MAX_PENDING] = std::max(ctx->xc[XC_MAX_PENDING], 2 * n);
+}
+
 // Round 2 of a ghost update: packs, remote messages, ordered unpacks, extended BCs.
 int ghosts_round2(bf_ctx* ctx) {
   int rc = run_ghost_launch(ctx, ctx->r2_pack, 0);
@@ -1425,6 +1497,14 @@ int ghosts_round2(bf_ctx* ctx) {
   if (remote) {
     if (!ctx->comm)
       return fail(ctx, BF_EINVAL, "rank %d has remote links but no communicator", ctx->rank);
+    {
+      long long n = 0, b = 0;
+      for (HostLink* L : remote_links_sorted(ctx)) {
+        ++n;
+        b += (long long)sizeof(double) * L->nfields * L->cells2;
+      }
+      count_exchange(ctx, n, b);
+    }
     NK(net(ctx).GroupStart());
     for (HostLink* L : remote_links_sorted(ctx)) {
       const size_t cnt = (size_t)L->nfields * L->cells2;
@@ -1636,6 +1716,11 @@ std::vector<HostLink*> remote_links_sorted(bf_ctx* ctx) {
 int nccl_exchange(bf_ctx* ctx) {
   auto rl = remote_links_sorted(ctx);
   if (rl.empty()) return BF_OK;
+  {
+    long long b = 0;
+    for (HostLink* L : rl) b += (long long)sizeof(double) * L->nfields * L->cells;
+    count_exchange(ctx, (long long)rl.size(), b);
+  }
   NK(net(ctx).GroupStart());
   for (HostLink* L : rl) {
     const size_t cnt = (size_t)L->nfields * L->cells;
@@ -1950,15 +2035,8 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
     return nullptr;
   }
   ctx->stream = ctx->own_stream;
-  {   // staging buffers (uploads, downloads) come from the stream-ordered pool;
-      // keep its memory mapped between calls instead of releasing it at every
-      // synchronisation (re-mapping 100+ MB per call dominated the transfers)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      cuuint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
+  device_ctx_opened(device);
+  ctx->counted = true;
   // constants, in the reference's scalar evaluation order (python floats)
   Consts& c = ctx->c;
   const double g = gas->gamma;
@@ -2063,7 +2141,10 @@ void bf_destroy(bf_ctx* ctx) {
   if (ctx->ev_bd) cudaEventDestroy(ctx->ev_bd);
   cudaFree(ctx->d_tiles_in);
   cudaFree(ctx->d_tiles_bd);
+  const int dev = ctx->device;
+  const bool counted = ctx->counted;
   delete ctx;
+  if (counted) device_ctx_closed(dev);
 }
 
 int bf_last_error(const bf_ctx* ctx, char* buf, size_t n) {
@@ -2071,6 +2152,20 @@ int bf_last_error(const bf_ctx* ctx, char* buf, size_t n) {
   std::snprintf(buf, n, "%s", ctx->msg.c_str());
   return BF_OK;
 }
+
+// A block's arenas go back to the cache on every error return of
+// bf_add_block / bf_add_block_nodes until the block is committed to ctx->blocks.
+struct BlockGuard {
+  bf_ctx* ctx;
+  HostBlock* hb;
+  ~BlockGuard() {
+    if (!hb || hb->owned.empty()) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (double* p : hb->owned) arena_free(ctx->device, p, hb->arena_bytes);
+    hb->owned.clear();
+  }
+  void commit() { hb = nullptr; }
+};
 
 // Arena allocation and device-block record shared by bf_add_block and
 // bf_add_block_nodes (layout: bf_internal.h).
@@ -2111,7 +2206,8 @@ int add_block_arena(bf_ctx* ctx, int block_id, const int dims[3], int ghost_dept
                 block_id);
   hb.owned.push_back(hb.arena);
   (void)err;
-  CK(cudaMemset(hb.arena, 0, sizeof(double) * (size_t)nfield * hb.fsz));
+  // on the context's stream: the geometry kernels that follow run there
+  CK(cudaMemsetAsync(hb.arena, 0, sizeof(double) * (size_t)nfield * hb.fsz, ctx->stream));
   DevBlock& d = hb.dev;
   for (int a = 0; a < 3; ++a) d.n[a] = hb.n[a];
   d.g = hb.g;
@@ -2135,6 +2231,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
                  const double* const* face_vectors, const double* volume,
                  const double* const* source) {
   HostBlock hb;
+  BlockGuard guard{ctx, &hb};
   int rc0 = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
   if (rc0) return rc0;
   const int ndim = ctx->ndim;
@@ -2186,6 +2283,7 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
   CK(cudaStreamSynchronize(st));
   d.order = (int)ctx->blocks.size();
   ctx->index_of[block_id] = (int)ctx->blocks.size();
+  guard.commit();
   ctx->blocks.push_back(std::move(hb));
   return BF_OK;
 }
@@ -2194,6 +2292,20 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
                        const double* const* nodes, const long long node_strides[3],
                        const double* const* source) {
   HostBlock hb;
+  BlockGuard guard{ctx, &hb};
+  {   // the strides must describe a dense array (C or Fortran order): checked
+      // before anything is allocated
+    if (!ctx) return BF_EINVAL;
+    const int nd = ctx->ndim, g = ghost_depth;
+    const long long ext[3] = {dims[0] + 2LL * g + 1, dims[1] + 2LL * g + 1,
+                              nd == 3 ? dims[2] + 2LL * g + 1 : 1};
+    const long long st[3] = {node_strides[0], node_strides[1], nd == 3 ? node_strides[2] : 0};
+    long long span = 1;
+    for (int a = 0; a < nd; ++a) span += (ext[a] - 1) * st[a];
+    if (span != ext[0] * ext[1] * ext[2])
+      return fail(ctx, BF_EINVAL, "node arrays must be dense (strides %lld %lld %lld)", st[0],
+                  st[1], st[2]);
+  }
   int rc = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
   if (rc) return rc;
   const int ndim = ctx->ndim;
@@ -2207,15 +2319,6 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   for (int c = 0; c < ndim; ++c)
     CK(cudaMemcpyAsync(dn + c * nn, nodes[c], sizeof(double) * nn, cudaMemcpyHostToDevice, st));
   ctx->bytes_h2d += (long long)sizeof(double) * ndim * nn;
-  {   // the strides must describe a dense array (C or Fortran order)
-    const long long st[3] = {node_strides[0], node_strides[1], ndim == 3 ? node_strides[2] : 0};
-    const long long ext[3] = {N0, N1, N2};
-    long long span = 1;
-    for (int a = 0; a < ndim; ++a) span += (ext[a] - 1) * st[a];
-    if (span != nn)
-      return fail(ctx, BF_EINVAL, "node arrays must be dense (strides %lld %lld %lld)", st[0],
-                  st[1], st[2]);
-  }
   NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, node_strides[0], node_strides[1],
               ndim == 3 ? node_strides[2] : 0};
   for (int dd = 0; dd < ndim; ++dd) {
@@ -2258,8 +2361,6 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   }
   CK(cudaStreamSynchronize(st));
   if (hbad != ~0ull) {
-    for (double* p : hb.owned) arena_free(ctx->device, p, hb.arena_bytes);
-    hb.owned.clear();
     const unsigned long long k = hbad % (unsigned long long)hb.n[2];
     const unsigned long long r = hbad / (unsigned long long)hb.n[2];
     const unsigned long long j = r % (unsigned long long)hb.n[1], i = r / (unsigned long long)hb.n[1];
@@ -2268,6 +2369,7 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
   }
   d.order = (int)ctx->blocks.size();
   ctx->index_of[block_id] = (int)ctx->blocks.size();
+  guard.commit();
   ctx->blocks.push_back(std::move(hb));
   return BF_OK;
 }
@@ -2954,6 +3056,15 @@ int group_ghosts(bf_group* g) {
     }
     int rc = fill_ghosts(ctx);
     if (rc) return rc;
+    {
+      long long n = 0, b = 0;
+      for (auto& L : ctx->links)
+        if (L.send) {
+          ++n;
+          b += (long long)sizeof(double) * L.nfields * L.cells;
+        }
+      if (n) count_exchange(ctx, n, b);
+    }
     for (auto& L : ctx->links) {
       if (!L.send) continue;
       bf_ctx* peer = g->ctxs[L.peer_rank];
@@ -2996,6 +3107,15 @@ int group_ghosts(bf_group* g) {
         if (q != r) CK(cudaStreamWaitEvent(ctx->stream, g->ev_unpacked[q], 0));
       int rc = run_ghost_launch(ctx, ctx->r2_pack, 0);
       if (rc) return rc;
+      {
+        long long n = 0, b = 0;
+        for (auto& L : ctx->links)
+          if (L.recv2) {
+            ++n;
+            b += (long long)sizeof(double) * L.nfields * L.cells2;
+          }
+        if (n) count_exchange(ctx, n, b);
+      }
       for (auto& L : ctx->links) {
         if (!L.recv2) continue;
         bf_ctx* peer = g->ctxs[L.peer_rank];
@@ -3139,6 +3259,21 @@ void bf_release_cache(int device) {
     if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   }
   if (cur >= 0) cudaSetDevice(cur);
+}
+
+int bf_transfer_counters(const bf_ctx* ctx, long long out[6]) {
+  if (!ctx || !out) return BF_EINVAL;
+  for (int q = 0; q < 6; ++q) out[q] = ctx->xc[q];
+  return BF_OK;
+}
+
+long long bf_cache_bytes(int device) {
+  ArenaCache& c = arena_cache();
+  std::lock_guard<std::mutex> g(c.m);
+  long long n = 0;
+  for (const auto& e : c.free)
+    if (device < 0 || e.dev == device) n += (long long)e.bytes;
+  return n;
 }
 
 long long bf_transfer_bytes(const bf_ctx* ctx, int direction) {

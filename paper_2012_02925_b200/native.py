@@ -89,6 +89,8 @@ PROTOTYPES = {
     "bf_kernel_stats": (_I, [_P, _I, _PLL, _PD]),
     "bf_transfer_bytes": (C.c_longlong, [_P, _I]),
     "bf_release_cache": (None, [_I]),
+    "bf_cache_bytes": (C.c_longlong, [_I]),
+    "bf_transfer_counters": (_I, [_P, _PLL]),
     "bf_probe_remote_order": (_I, [_I, _PI, _PI, _PI, _PI]),
     "bf_probe_unpack_map": (_I, [_PI, _I, _I, _I, _PI, _PI, _I, _PLL, C.c_longlong]),
 }

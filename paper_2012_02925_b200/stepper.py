@@ -426,6 +426,15 @@ class GpuContext:
     def transfer_bytes(self):
         return int(self.L.bf_transfer_bytes(self.ctx, 0)), int(self.L.bf_transfer_bytes(self.ctx, 1))
 
+    COUNTER_NAMES = ("messages", "runs", "bytes", "staging_copies", "waits", "max_pending")
+
+    def transfer_counters(self):
+        """The engine's cumulative TransferCounters (bf_transfer_counters,
+        exchange.py:83-101 fields) as a dict."""
+        out = (C.c_longlong * 6)()
+        self._check(self.L.bf_transfer_counters(self.ctx, out))
+        return dict(zip(self.COUNTER_NAMES, (int(v) for v in out)))
+
     def close(self):
         if getattr(self, "ctx", None):
             self.L.bf_destroy(self.ctx)
@@ -630,11 +639,19 @@ def write_residual_csv(result, path):
             f.write(f"{i + 1}," + ",".join(f"{v:.16e}" for v in row) + "\n")
 
 
+def release_cache(device=-1):
+    """Hand the block arenas kept for reuse (and the staging pool) back to the
+    driver (bf_release_cache).  They are kept only while another context of the
+    device is alive, or across contexts when BF_ARENA_CACHE=1."""
+    native.lib().bf_release_cache(int(device))
+
+
 def iterate_gpu(plan, schedule, gas, config, freestream, max_steps, residual_target=None,
                 init="uniform", residual_floor=None, device=0, precision="auto",
                 metrics_fn=None):
     """solver.iterate on one GPU: every child of the plan in one context, all
-    connected boundaries served by device copies (solver.py:914-936)."""
+    connected boundaries served by device copies (solver.py:914-936).  The
+    device memory is returned when the context closes (release_cache)."""
     gpu = GpuContext(plan, [c.id for c in plan.children], gas, config, freestream,
                      device=device, precision=precision, metrics_fn=metrics_fn,
                      schedule=schedule)
@@ -662,29 +679,38 @@ def _gather_parent_fields(plan, views_by_cid):
     return out
 
 
-def native_counters(plan, rounds=1):
-    """Transfer accounting of the native engine (packed, persistent, direct,
-    deferred; cf. exchange.py:166-200): per rank messages/bytes/runs/waits."""
+def native_counters(plan, rounds=1, exchanges=1):
+    """Predicted transfer counters of the native engine (the analogue of
+    exchange.py:166-200 predict_counters) after `exchanges` ghost updates of
+    `rounds` rounds each: per round a rank sends ONE message per remote endpoint
+    (all fields concatenated, one grouped NCCL send/recv), runs one pack and one
+    unpack launch, waits once for the grouped exchange and has every send and
+    receive of the group in flight; no staging copies.  bf_transfer_counters
+    reports what the engine actually did (tests/test_gpu_loopback.py holds the
+    two equal)."""
     from .topology import halo_regions
     ndim = plan.grid.ndim
     nf = 3 + ndim
-    out = {}
-    for r in range(plan.np_ranks):
-        out[r] = {"messages": 0, "runs": 0, "bytes": 0, "staging_copies": 0, "waits": 0,
-                  "max_pending": 0}
-    for cid, s in plan.connected_specs():
-        rank = plan.child(cid).rank
-        blk = plan.child_block(cid)
-        remote = plan.child(s.neighbor_block).rank != rank
-        for rnd in range(1, rounds + 1):
+    out = {r: dict.fromkeys(GpuContext.COUNTER_NAMES, 0) for r in range(plan.np_ranks)}
+    for rnd in range(1, rounds + 1):
+        per_rank = {r: [0, 0] for r in range(plan.np_ranks)}
+        for cid, s in plan.connected_specs():
+            rank = plan.child(cid).rank
+            if plan.child(s.neighbor_block).rank == rank:
+                continue
+            blk = plan.child_block(cid)
             send, _ = halo_regions(s, blk.dims, blk.ghost, rnd)
-            cells = int(np.prod([hi - lo for lo, hi in send]))
-            out[rank]["runs"] += 2 * nf
-            if remote:
-                out[rank]["messages"] += 4
-                out[rank]["bytes"] += cells * nf * 8
-                out[rank]["waits"] += 2
-                out[rank]["max_pending"] += 2
+            per_rank[rank][0] += 1
+            per_rank[rank][1] += int(np.prod([hi - lo for lo, hi in send])) * nf * 8
+        for r, (n, b) in per_rank.items():
+            if not n:
+                continue
+            c = out[r]
+            c["messages"] += n * exchanges
+            c["bytes"] += b * exchanges
+            c["runs"] += 2 * exchanges
+            c["waits"] += exchanges
+            c["max_pending"] = max(c["max_pending"], 2 * n)
     return out
 
 
@@ -749,9 +775,11 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
         parts = [None] * nr
         dist.all_gather_object(parts, local_interiors(stepper.solvers))
         fields = assemble_parent_fields(plan, parts)
+        counts = [None] * nr
+        dist.all_gather_object(counts, gpu.transfer_counters())
         gpu.close()
         return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
-                                 converged=converged, counters=native_counters(plan),
+                                 converged=converged, counters=dict(enumerate(counts)),
                                  solve_seconds=solve)
 
     if transport == "loopback":
@@ -790,10 +818,11 @@ def run_distributed_gpu(plan, schedule, gas, config, freestream, strategy=None, 
         solve = time.perf_counter() - t0
         views = {cid: v for st in steppers for cid, v in st.solvers.items()}
         fields = _gather_parent_fields(plan, views)
+        counters = {r: g.transfer_counters() for r, g in enumerate(gpus)}
     finally:
         L.bf_group_destroy(grp)
     return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
-                             converged=converged, counters=native_counters(plan),
+                             converged=converged, counters=counters,
                              solve_seconds=solve)
 
 
@@ -858,8 +887,9 @@ def _run_loopback(plan, schedule, gas, config, freestream, max_steps, residual_t
                                                            residual_floor=residual_floor)
         views = {cid: v for st in steppers for cid, v in st.solvers.items()}
         fields = _gather_parent_fields(plan, views)
+        counters = {r: g.transfer_counters() for r, g in enumerate(gpus)}
         return DistributedResult(fields=fields, history=np.array(history), steps=len(history),
-                                 converged=converged, counters=native_counters(plan),
+                                 converged=converged, counters=counters,
                                  solve_seconds=solve)
     finally:
         for g in gpus:

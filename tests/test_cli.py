@@ -57,6 +57,13 @@ def test_device_run_writes_reference_artefacts(tmp_path):
     assert rows[0] == "step,r_mass,r_xmom,r_ymom,r_zmom,r_energy" and len(rows) == 7
     counters = json.loads((out / "counters.json").read_text())
     assert [c["rank"] for c in counters] == [0, 1, 2]
+    # the engine's own counters: one message per remote endpoint per exchange
+    # (2 RK stages x 6 steps), as predicted for the plan
+    from paper_2012_02925_b200.stepper import native_counters
+    plan = cli.build_plan(cfg, cli.build_grid(cfg))
+    want = native_counters(plan, rounds=1, exchanges=12)
+    for c in counters:
+        assert {k: c[k] for k in want[c["rank"]]} == want[c["rank"]]
     plan = json.loads((out / "plan.json").read_text())
     assert plan["np"] == 3 and "schedule" in plan
     sol = np.load(out / "block_0.npy")

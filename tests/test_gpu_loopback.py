@@ -72,6 +72,22 @@ def test_loopback_box3d_matches_serial(nranks, precision):
     assert_same_as_serial(plan, cfg, fs, 5, "perturbed", precision)
 
 
+@pytest.mark.parametrize("transport", ["loopback", "group"])
+def test_transfer_counters_are_the_engines(transport):
+    """DistributedResult.counters come from the engine (bf_transfer_counters):
+    one concatenated message per remote endpoint and exchange, its bytes, one
+    pack + one unpack launch and one wait per exchange, every send and receive
+    of the group in flight — equal to native_counters' prediction."""
+    plan = cases.make_plan(geometry.multiblock_box_3d(2), 4)
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8, rk_stages=2)
+    dist = _stepper().run_distributed_gpu(plan, planning.reorder_boundaries(plan), GAS, cfg, fs,
+                                          max_steps=3, init="perturbed", transport=transport)
+    want = _stepper().native_counters(plan, rounds=1, exchanges=3 * 2)
+    assert dist.counters == want
+    assert all(c["messages"] > 0 and c["staging_copies"] == 0 for c in dist.counters.values())
+
+
 def test_loopback_c4_level12_eight_ranks_fast():
     """C4's geometry at 128^3 cells decomposed over 8 ranks (the north-star
     np=8 plan, scaled down): 8 children of 64^3, 3 remote faces each."""
