@@ -1,0 +1,117 @@
+"""Parity on the benchmarked configuration and the remaining reference behaviours
+(VERDICT r1 "what's missing" 6 and "what's weak" 1):
+
+* the FAST build (the one bench.py times) against the CPU oracle on the C4
+  geometry itself at level 13 (4.2M cells in the 4 parents), 2 RK2 steps;
+* a long horizon: C1 (the SPEC case) for 2000 steps in FAST against the oracle —
+  state within 1e-12 of the freestream scale and |dH_k| <= 1e-12 H_1 at every
+  step (per-step |dH_k|/H_k drifts past 1e-12 in any non-bitwise
+  build from step ~1000 on, §0 finding 5);
+* the C2 subsonic variant (M = 0.5, farfield ends), full size;
+* the C3 order-of-accuracy study at 32^3 / 64^3 / 128^3 on 8 blocks
+  (cli.py:410-434), the 128^3 case also at np = 1 (1 -> 8 blocks);
+* the Roe a^2 <= 0 error (physics.py:213-217), same text as the oracle."""
+
+import io
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2012_02925_b200 import cases, cli, geometry, planning
+from paper_2012_02925_b200.errors import NonPhysicalStateError
+from paper_2012_02925_b200.model import FIELD_NAMES, FreestreamState, GasModel, SchemeConfig
+
+from test_gpu_parity import _gpu, _init_perturbed, compare, history_close, run_pair
+
+pytestmark = pytest.mark.gpu
+GAS = GasModel()
+
+
+@pytest.mark.slow
+def test_c4_level13_fast_vs_oracle():
+    plan, sched, gas, cfg, fs, init = cases.c4_box(level=13, np_ranks=1)
+    assert plan.grid.total_cells() == 4 * 1024 * 1024
+    ref, got = run_pair(plan, cfg, fs, 2, init=init, precision="fast", gas=gas)
+    compare(ref, got, fs, bitwise=False)
+
+
+@pytest.mark.slow
+def test_c1_fast_2000_steps_vs_oracle():
+    plan, sched, gas, cfg, fs, init = cases.c1_inlet()
+    steps = 2000
+    ref = oracle.iterate(plan, sched, gas, cfg, fs, steps, init=init)
+    got = _gpu().iterate_gpu(plan, sched, gas, cfg, fs, steps, init=init, precision="fast")
+    assert got.steps == ref.steps == steps
+    history_close(got.history, ref.history, 1e-12)
+    compare(ref, got, fs, bitwise=False, check_q=False)
+    # the run really moved: the residual fell by orders of magnitude
+    assert np.all(ref.history[-1][[0, 1, 3]] < 1e-2 * ref.history[0][[0, 1, 3]])
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_c2_subsonic_full_size_vs_oracle(precision):
+    plan, sched, gas, cfg, fs, init = cases.c2_channel(subsonic=True)
+    assert plan.grid.total_cells() == 4 * 512 * 256
+    assert any(s.kind == "physical" and s.bc_type == "farfield"
+               for specs in plan.boundaries.values() for s in specs)
+    ref, got = run_pair(plan, cfg, fs, 3, init=init, precision=precision, gas=gas)
+    compare(ref, got, fs, bitwise=False, check_q=False)
+
+
+def test_c3_order_study_32_64_128_on_8_blocks():
+    """cli.py:410-434 on the 3D cube split into 8 children:
+    the converged L2 solution error falls at second order."""
+    cfg = cli.RunConfig(case="cartesian_box", flux="roe", limiter="none", cfl=0.5,
+                        max_steps=20000, residual_target=1e-8, mms_levels="32,64,128")
+    buf = io.StringIO()
+    out = cli.run_mms_study(cfg, cli.build_gas(cfg), buf, precision="fast", ndim=3, np_ranks=8)
+    assert all(conv for _, _, _, conv in out), buf.getvalue()
+    errs = [e for _, e, _, _ in out]
+    orders = [np.log(a / b) / np.log(2.0) for a, b in zip(errs, errs[1:])]
+    assert min(orders) > 1.9, buf.getvalue()
+    # 1 -> 8 blocks: the same converged solution from one 128^3 block
+    from dataclasses import replace
+    one = cli.run_mms_study(replace(cfg, mms_levels="128"),
+                            cli.build_gas(cfg), io.StringIO(), precision="fast", ndim=3,
+                            np_ranks=1)
+    np.testing.assert_allclose(one[0][1], errs[-1], rtol=1e-9)
+
+
+def _roe_a2_state(block, fs):
+    """Uniform u = 1000 m/s with p = 1e-20 in a patch of cells: the face states
+    pass the positivity check but the Roe-averaged h - |u|^2/2 cancels to 0."""
+    f = {n: block.allocate_field(getattr(fs, n)) for n in FIELD_NAMES}
+    g = block.ghost[0]
+    sl = (slice(g + 5, g + 10), slice(g + 3, g + 7), slice(None))
+    f["u"][sl] = 1000.0
+    f["v"][sl] = 0.0
+    f["rho"][sl] = 1.0
+    f["p"][sl] = 1e-20
+    f["T"][sl] = f["p"][sl] / (f["rho"][sl] * GAS.R)
+    return f
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_roe_nonpositive_sound_speed_message(precision):
+    grid = geometry.inlet_ramp_2d(0)
+    plan = planning.decompose(grid, 1, 2)
+    cfg = SchemeConfig(flux="roe", limiter="none", epsilon=0.0, cfl=0.5)
+    fs = cases.freestream_for("inlet_ramp_2d", GAS, 2)
+    st = _gpu()
+    gpu = st.GpuContext(plan, [0], GAS, cfg, fs, precision=precision)
+    gpu.finalize()
+    f = _roe_a2_state(plan.child_block(0), fs)
+    gpu.upload(0, [f[n] for n in FIELD_NAMES])
+    with pytest.raises(NonPhysicalStateError, match="Roe-averaged state") as ei:
+        st.GpuRankStepper(gpu, cfg).step(1)
+    gpu.close()
+    blocks = oracle.build_blocks(plan, GAS, cfg, fs)
+    for n, arr in f.items():
+        blocks[0].fields[n][...] = arr
+    blocks[0].sync_conserved()
+    sched = planning.reorder_boundaries(plan)
+    ost = oracle.OracleStepper(blocks, oracle.make_serial_exchange(plan, sched, blocks), cfg)
+    with pytest.raises(NonPhysicalStateError) as eo:
+        ost.step(1)
+    assert str(ei.value) == str(eo.value)
