@@ -150,6 +150,7 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
 #include "bf_stage.cuh"
 #if !BF_EXACT
 #include "bf_vl.cuh"
+#include "bf_roe.cuh"
 #endif
 
 // ---------------------------------------------------------------------------
@@ -562,11 +563,27 @@ bool vl_push_compiled() { return BF_VL_PUSH != 0; }
 bool vl_active(int flux, int flags) {
   return flux == FLUX_VAN_LEER && !(flags & (F_PSI_LOAD | F_PSI_STORE)) && !vl_disabled();
 }
+
+// FAST Roe with limiters computed in-kernel runs the face-owner kernel
+// (bf_roe.cuh); BF_ROE_SPLIT=0 keeps it on the reference-order kernel.
+static bool roe_split_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BF_ROE_SPLIT");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool roe_split_active(int flux, int flags) {
+  return flux == FLUX_ROE && !(flags & (F_PSI_LOAD | F_PSI_STORE)) && !roe_split_disabled();
+}
 #endif
 
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s) {
 #if !BF_EXACT
   if (vl_active(flux, a.flags) && !a.c.viscous) return launch_vl(ndim, lim, a, s);
+  if (roe_split_active(flux, a.flags) && !a.c.viscous) return launch_roe(ndim, lim, a, s);
 #endif
   if (ndim == 3)
     return flux == FLUX_ROE ? launch_stage_l<3, FLUX_ROE>(lim, a, s)

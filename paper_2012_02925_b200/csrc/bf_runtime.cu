@@ -2021,10 +2021,9 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   ctx->device = device;
   ctx->rank = rank;
   ctx->nranks = nranks;
-  // k-chunk per tile: 32 for the cell-split kernel (FAST Van Leer, inviscid; C4: 1.251 vs
-  // 1.273 ms at 16), 16 for the reference-order kernel (profiles/r01_kc_*.json)
-  ctx->kc = (scheme->precision != BF_PRECISION_EXACT && scheme->flux == FLUX_VAN_LEER &&
-             !scheme->viscous) ? 32 : 16;
+  // k-chunk per tile: 32 for the cell-split / face-owner kernels (FAST, inviscid; C4 Van
+  // Leer: 1.251 vs 1.273 ms at 16), 16 for the reference-order kernel (profiles/r01_kc_*.json)
+  ctx->kc = (scheme->precision != BF_PRECISION_EXACT && !scheme->viscous) ? 32 : 16;
   if (const char* e = std::getenv("BF_KC")) ctx->kc = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("BF_NO_OVERLAP")) ctx->no_overlap = e[0] == '1';
   if (const char* e = std::getenv("BF_GRAPH")) ctx->graph_off = e[0] == '0';

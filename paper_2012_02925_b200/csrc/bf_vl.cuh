@@ -50,6 +50,9 @@ BF_DEV void tma_prefetch4(const void* tmap, int x, int y, int z, int s) {
 // the Van Albada limiter quotient, whose error enters the face states as
 // (error) x (eps/4) x D, i.e. ~1e-14 of the cell-to-cell difference.
 BF_DEV double frcp1(double b) {
+#ifdef BF_VA_RCP_FULL
+  return frcp(b);
+#endif
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   return fma(r, fma(-b, r, 1.0), r);

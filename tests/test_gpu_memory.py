@@ -38,9 +38,11 @@ def test_recycled_arenas_do_not_leak_state(monkeypatch):
 
 def test_cache_released_with_last_context(monkeypatch):
     from paper_2012_02925_b200 import stepper
+    import gc
     monkeypatch.delenv("BF_ARENA_CACHE", raising=False)
+    gc.collect()                   # contexts of earlier tests (results keep them alive)
     gas = GasModel()
-    plan = planning.decompose(geometry.multiblock_box_3d(2), 1, 3)
+    plan = cases.make_plan(geometry.multiblock_box_3d(2), 1)
     sched = planning.reorder_boundaries(plan)
     fs = cases.freestream_for("multiblock_box_3d", gas, 3)
     cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
