@@ -177,7 +177,24 @@ struct GhostArgs {
   int extended;         // GK_BC: ghost round 2 (tangential range widened, solver.py:285-305)
   int ipt;              // items per thread (1 .. GHOST_ITEMS), as the block map was cut
   long long total_items;
+  const int* stop;      // batched iterate: a set flag makes the launch a no-op (null: never)
   Consts c;
+};
+
+// Device-side state of a batched iterate (bf_iterate): the guard kernel at the
+// end of every step sums the per-block sum(R^2) in block order, writes the
+// step's norms and evaluates check_history_guards (solver.py:836-855); a
+// fired guard or a recorded non-physical state sets `stop`, which turns the
+// remaining launches of the batch into no-ops.
+struct RunState {
+  int stop;
+  int steps;            // steps of the batch completed (guard evaluated)
+  int status;           // 0 running, 1 converged, 2 diverged, 3 non-physical state
+  int has_base;         // base = the call's first-step norms
+  unsigned long long key;   // error key of status 3
+  double base[5];
+  int has_target, has_floor, ignore_errors, pad;
+  double target, floor_, factor;
 };
 
 // Ghost values pushed by the stage kernel (bf_vl.cuh): when a cell's new
@@ -233,6 +250,7 @@ struct StageArgs {
   const int* push_range;        // [nblocks][6 faces][begin, end) into push_rules
   int push;
   int t_derived;        // interior T is p/(rho R) (viscous dt reads T)
+  const int* stop;      // batched iterate: a set flag makes the launch a no-op (null: never)
   Consts c;
 };
 

@@ -268,6 +268,7 @@ BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m);
 // first store (GHOST_ITEMS x 6 loads in flight per thread).
 __global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
   __shared__ __align__(16) GhostTask ts;   // the task record, staged once
+  if (a.stop && *a.stop) return;           // batched iterate stopped (RunState)
   const int2 bm = a.block_map[blockIdx.x];
   {
     static_assert(sizeof(GhostTask) % 8 == 0, "GhostTask words");
@@ -608,6 +609,71 @@ cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s) {
 cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
   if (nlaunch == 0) return cudaSuccess;
   viscous_kernel<<<(unsigned)nlaunch, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// End of a batched-iterate step (RunState, bf_internal.h): the norms of the
+// step from the per-block sums in block order (as finish_collect sums them on
+// the host) and check_history_guards (solver.py:836-855) as history_guard in
+// bf_runtime.cu evaluates it, with numpy's NaN semantics.
+__global__ void guard_kernel(const double* blocksum, int nb, const unsigned long long* err,
+                             RunState* rs, double* hist) {
+  if (threadIdx.x != 0 || rs->stop) return;
+  const int s = rs->steps;
+  const unsigned long long key = *err;
+  if (key != ~0ull && !rs->ignore_errors) {   // non-physical state in this step
+    rs->key = key;
+    rs->status = 3;
+    rs->stop = 1;
+    return;
+  }
+  double h[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b)
+    for (int v = 0; v < 5; ++v) h[v] = h[v] + blocksum[5 * b + v];
+  for (int v = 0; v < 5; ++v) {
+    h[v] = sqrt(h[v]);
+    hist[5 * s + v] = h[v];
+  }
+  if (!rs->has_base) {
+    for (int v = 0; v < 5; ++v) rs->base[v] = h[v];
+    rs->has_base = 1;
+  }
+  rs->steps = s + 1;
+  auto npmax = [](const double* x) {
+    double m = x[0];
+    for (int v = 1; v < 5; ++v)
+      if (isnan(x[v]) || x[v] > m || isnan(m)) m = isnan(m) ? m : x[v];
+    return m;
+  };
+  int g = 0;
+  if (rs->has_floor && npmax(h) <= rs->floor_) {
+    g = 1;
+  } else {
+    const double* bs = rs->base;
+    const double bmax = npmax(bs);
+    bool any = false, bad = false;
+    double rmax = 0.0;
+    for (int v = 0; v < 5; ++v) {
+      if (!(bs[v] > 1e-12 * bmax)) continue;
+      const double r = h[v] / bs[v];
+      if (!isfinite(r)) bad = true;
+      rmax = any ? (r > rmax ? r : rmax) : r;
+      any = true;
+    }
+    if (any) {
+      if (bad || rmax > rs->factor) g = 2;
+      else if (rs->has_target && rmax <= rs->target) g = 1;
+    }
+  }
+  if (g) {
+    rs->status = g;
+    rs->stop = 1;
+  }
+}
+
+cudaError_t launch_guard(const double* blocksum, int nb, const unsigned long long* err,
+                         RunState* rs, double* hist, cudaStream_t s) {
+  guard_kernel<<<1, 32, 0, s>>>(blocksum, nb, err, rs, hist);
   return cudaGetLastError();
 }
 

@@ -127,7 +127,11 @@ struct RCfg {
   static constexpr int OFY = r16(OFX + 4 * NFX);
   static constexpr int OZG = r16(OFY + 4 * NFY);         // [2][4][TJ][TI] z faces (3D)
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
-  static constexpr int OBAR = r16(OQ + 6 * NT);
+  // cell k's high-side z state (the left state of face k+1/2), thread-private:
+  // carried along k in shared memory instead of 5 registers
+  static constexpr int OZQ = r16(OQ + 6 * NT);
+  static constexpr int ORS = r16(OZQ + (NDIM == 3 ? 5 * NT : 0));   // [NT/32][5] sum(R^2)
+  static constexpr int OBAR = r16(ORS + 5 * (NT / 32));
   static constexpr int TOTAL = OBAR + 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr int MINB = (NDIM == 2) ? BF_VL2D_MINB : 1;
@@ -140,6 +144,7 @@ struct RCfg {
 template <int NDIM, int LIM, bool K1, bool S0>
 __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
     roe_stage_kernel(const __grid_constant__ StageArgs a) {
+  if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   using K = RCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
   constexpr int NFX = K::NFX, NFY = K::NFY, NYF = K::NYF;
@@ -151,6 +156,8 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
   double* const sFY = smem + K::OFY;
   double* const sZG = smem + K::OZG;
   double* const sQ = smem + K::OQ;
+  double* const sZQ = smem + K::OZQ + threadIdx.x;   // [5] at stride NT
+  double* const sRS = smem + K::ORS;
   unsigned long long* const bars = reinterpret_cast<unsigned long long*>(smem + K::OBAR);
   // bars[0..2]: plane ring, bars[3]: y/z geometry group, bars[4]: x geometry + Q0 / dt group
 
@@ -258,15 +265,14 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
   };
 
   // ---- state carried along k (3D) ---------------------------------------------------
-  double zqL[5] = {0, 0, 0, 0, 0};   // left state of face k+1/2 (cell k's high side)
   double fzl[5] = {0, 0, 0, 0, 0};   // z flux of face k-1/2 (times A), the low face of cell k
   double lamz = 0.0;                 // z part of the stage-0 lambda of cell k
-  double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
   if (tid == 0) {
     for (int q = 0; q < 5; ++q) mbar_init(bars + q, 1);
     fence_mbar_init();
   }
+  if (stage0 && tid < 5 * (NT / 32)) sRS[tid] = 0.0;
   __syncthreads();
   if (tid == 0) {
     if constexpr (NDIM == 3) {
@@ -302,13 +308,14 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
     mbar_wait(bar_of(k0), par_of(k0));
     mbar_wait(bar_of(k0 + 1), par_of(k0 + 1));
     if (cell_on) {
-      double wc[5], wd[5], qLm[5], qR0[5];
+      double wc[5], wd[5], qLm[5], qR0[5], zqL[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         wc[v] = slot_of(k0)[v * PLANE + s0];
         wd[v] = slot_of(k0 + 1)[v * PLANE + s0];
         qLm[v] = recon_side<LIM, K1, true>(wa[v], wb[v], wc[v], c);   // cell k0-1, high side
         vl_recon<LIM, K1>(wb[v], wc[v], wd[v], c, zqL[v], qR0[v]);    // cell k0, both sides
+        sZQ[v * NT] = zqL[v];
       }
       const bool ok = roe_face(qLm, qR0, g0[0], g0[1], g0[2], g0[3], c, fzl);
       check_face(2, qLm, qR0, ok, lin_z(i, j, k0));
@@ -460,12 +467,14 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
       if (cell_on) {
         const double* p1 = slot_of(k + 1) + s0;
         const double* p2 = slot_of(k + 2) + s0;
-        double w0[5], wc[5], qR1[5], qL1[5];
+        double w0[5], wc[5], qR1[5], qL1[5], zqL[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           w0[v] = w[v * PLANE];
           wc[v] = p1[v * PLANE];
           vl_recon<LIM, K1>(w0[v], wc[v], p2[v * PLANE], c, qL1[v], qR1[v]);   // cell k+1
+          zqL[v] = sZQ[v * NT];
+          sZQ[v * NT] = qL1[v];
         }
         const double* glo = zslot(k + 1) + tid;   // face k+1/2
         double fhi[5];
@@ -486,7 +495,6 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
         for (int v = 0; v < 5; ++v) {
           R[v] += fhi[v] - fzl[v];
           fzl[v] = fhi[v];
-          zqL[v] = qL1[v];
         }
         if (stage0) {
           const double* ghi = zslot(k + 2) + tid;
@@ -549,8 +557,6 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
       }
       double dtv;
       if (stage0) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) rsum[v] = fma(R[v], R[v], rsum[v]);
         dtv = c.cfl * frcp(lam);
         b.base[(long long)FDTV * fsz + co] = dtv;
       } else {
@@ -578,23 +584,23 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
         for (int v = 0; v < 5; ++v) b.base[(long long)(FQ + v) * fsz + co] = qn[v];
       }
     }
+    if (stage0) {   // sum(R^2) of the plane: warp tree, accumulated per warp (fixed order)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        double x = cell_on ? R[v] * R[v] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
+        if ((tid & 31) == 0) sRS[(tid >> 5) * 5 + v] += x;
+      }
+    }
   }
 
   // ---- deterministic per-tile sum(R^2) ----------------------------------------
   if (stage0) {
     __syncthreads();
-    double* red = sQ;   // free after the last phase B: [NT/32][5]
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      double x = rsum[v];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
-      if ((tid & 31) == 0) red[(tid >> 5) * 5 + v] = x;
-    }
-    __syncthreads();
     if (tid < 5) {
       double x = 0.0;
-      for (int q = 0; q < NT / 32; ++q) x += red[q * 5 + tid];
+      for (int q = 0; q < NT / 32; ++q) x += sRS[q * 5 + tid];
       a.partial[(long long)tile_id * 5 + tid] = x;
     }
   }

@@ -36,6 +36,8 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s);
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
+cudaError_t launch_guard(const double* blocksum, int nb, const unsigned long long* err,
+                         RunState* rs, double* hist, cudaStream_t s);
 int stage_tile_rows(int ndim, int lim);
 }  // namespace bf_exact
 namespace bf_fast {
@@ -450,6 +452,15 @@ struct bf_ctx {
   // profiling mode; a profiled graph records its own timing events
   cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   std::vector<TimerPair> gprof[2];
+  // batched iterate (bf_iterate): steps whose norms and guards stay on the device;
+  // their graphs end with the guard kernel instead of the per-step D2H
+  cudaGraphExec_t gexec_b[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  std::vector<TimerPair> gprof_b[2];
+  bool batching = false;
+  bool batch_off = false;          // BF_BATCH=0
+  RunState* d_run = nullptr;
+  double* d_hist = nullptr;        // [BATCH_MAX][5]
+  void* h_run = nullptr;           // pinned: RunState + hist
   bool capturing = false;
   bool graph_off = false;          // BF_GRAPH=0, or a capture that did not reproduce
   long long cur_epoch = 0;         // bumped by every stage launch (buffer swap)
@@ -506,6 +517,8 @@ struct bf_ctx {
   double* d_rank6 = nullptr;          // [6] own rank record (NCCL)
   double* d_gather = nullptr;         // [nranks][6]
   double* h_pinned = nullptr;         // blocksum + err staging
+  // RunState::stop is its first member
+  const int* stop_flag() const { return batching ? reinterpret_cast<const int*>(d_run) : nullptr; }
   // state
   int cur = 0;
   int ghost_buf = 0;
@@ -1458,6 +1471,7 @@ int run_ghost_launch(bf_ctx* ctx, const bf_ctx::GhostLaunch& L, int extended) {
   g.t_derived = ctx->t_derived;
   g.extended = extended;
   g.ipt = L.ipt;
+  g.stop = ctx->stop_flag();
   g.c = ctx->c;
   CK(ghost_fn(ctx)(g, ctx->stream));
   return BF_OK;
@@ -1677,6 +1691,7 @@ GhostArgs ghost_args(bf_ctx* ctx, bool unpack) {
   g.ipt = unpack ? ctx->ipt_unpack : ctx->ipt_fill;
   g.cur = ctx->cur;
   g.t_derived = ctx->t_derived;
+  g.stop = ctx->stop_flag();
   g.c = ctx->c;
   return g;
 }
@@ -1841,6 +1856,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.partial = ctx->d_partial;
   a.err = ctx->d_err;
   a.tmaps = ctx->d_tmaps;
+  a.stop = ctx->stop_flag();
   a.c = ctx->c;
   const bool vl = ctx->sch.precision != BF_PRECISION_EXACT && !ctx->sch.viscous &&
                   bf_fast::vl_active(ctx->sch.flux, flags);
@@ -2027,6 +2043,7 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   if (const char* e = std::getenv("BF_KC")) ctx->kc = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("BF_NO_OVERLAP")) ctx->no_overlap = e[0] == '1';
   if (const char* e = std::getenv("BF_GRAPH")) ctx->graph_off = e[0] == '0';
+  if (const char* e = std::getenv("BF_BATCH")) ctx->batch_off = e[0] == '0';
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
                                                                         cudaStreamNonBlocking) !=
                                                   cudaSuccess) {
@@ -2093,7 +2110,18 @@ void bf_destroy(bf_ctx* ctx) {
   for (auto& row : ctx->gexec)
     for (auto& ex : row)
       if (ex) cudaGraphExecDestroy(ex);
+  for (auto& row : ctx->gexec_b)
+    for (auto& ex : row)
+      if (ex) cudaGraphExecDestroy(ex);
+  cudaFree(ctx->d_run);
+  cudaFree(ctx->d_hist);
+  if (ctx->h_run) cudaFreeHost(ctx->h_run);
   for (auto& v : ctx->gprof)
+    for (auto& p : v) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+  for (auto& v : ctx->gprof_b)
     for (auto& p : v) {
       cudaEventDestroy(p.a);
       cudaEventDestroy(p.b);
@@ -2636,6 +2664,12 @@ int enqueue_step(bf_ctx* ctx, int step_index) {
     rc = launch_stage_kernel(ctx, k, stage_flags(ctx, step_index, k, nst), rk_alpha(nst, k));
     if (rc) return rc;
   }
+  if (ctx->batching) {   // norms and guards on the device (RunState)
+    ProfScope ps(ctx, 3);
+    CK(bf_exact::launch_guard(ctx->d_blocksum, (int)ctx->blocks.size(), ctx->d_err, ctx->d_run,
+                              ctx->d_hist, ctx->stream));
+    return BF_OK;
+  }
   return enqueue_collect(ctx);
 }
 
@@ -2697,7 +2731,9 @@ int enqueue_step_graph(bf_ctx* ctx, int step_index) {
   const int nst = ctx->sch.rk_stages;
   const StepState before = save_state(ctx);
   const int c0 = ctx->cur, pr = ctx->profiling ? 1 : 0;
-  if (!ctx->gexec[c0][pr]) {
+  auto& gexec = ctx->batching ? ctx->gexec_b : ctx->gexec;
+  auto& gprof = ctx->batching ? ctx->gprof_b : ctx->gprof;
+  if (!gexec[c0][pr]) {
     cudaGraph_t g = nullptr;
     const size_t npend = ctx->pending.size();
     if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
@@ -2729,11 +2765,11 @@ int enqueue_step_graph(bf_ctx* ctx, int step_index) {
       return 1;
     }
     for (auto& p : captured) p.owned_by_graph = true;
-    if (pr) ctx->gprof[c0] = captured;
-    ctx->gexec[c0][pr] = ex;
+    if (pr) gprof[c0] = captured;
+    gexec[c0][pr] = ex;
   }
-  CK(cudaGraphLaunch(ctx->gexec[c0][pr], ctx->stream));
-  if (pr) ctx->pending.insert(ctx->pending.end(), ctx->gprof[c0].begin(), ctx->gprof[c0].end());
+  CK(cudaGraphLaunch(gexec[c0][pr], ctx->stream));
+  if (pr) ctx->pending.insert(ctx->pending.end(), gprof[c0].begin(), gprof[c0].end());
   load_state(ctx, advanced(before, nst));
   return BF_OK;
 }
@@ -2811,13 +2847,89 @@ static int history_guard(const double* hist, int step, int has_target, double ta
   return (has_target && rmax <= target) ? 1 : 0;
 }
 
+constexpr int BATCH_MAX = 256;   // steps per batch (device history rows)
+
+// Steps first_step .. first_step + n - 1 enqueued back to back through the
+// batched graphs; the guard kernel of each step stops the rest of the batch
+// (RunState).  Host sequencing state follows the steps the device executed.
+static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_target,
+                     double target, int has_floor, double floor_, double factor,
+                     double* hist_out, int* done, int* status) {
+  if (!ctx->d_run) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(RunState)));
+    ctx->d_run = static_cast<RunState*>(p);
+    CK(cudaMalloc(&p, sizeof(double) * 5 * BATCH_MAX));
+    ctx->d_hist = static_cast<double*>(p);
+    CK(cudaMallocHost(&p, sizeof(RunState) + sizeof(double) * 5 * BATCH_MAX));
+    ctx->h_run = p;
+  }
+  RunState* hr = static_cast<RunState*>(ctx->h_run);
+  std::memset(hr, 0, sizeof(RunState));
+  hr->has_base = call_step > 0;
+  if (call_step > 0)
+    for (int v = 0; v < 5; ++v) hr->base[v] = hist_out[v];
+  hr->has_target = has_target;
+  hr->target = target;
+  hr->has_floor = has_floor;
+  hr->floor_ = floor_;
+  hr->factor = factor;
+  hr->ignore_errors = ignore_errors() ? 1 : 0;
+  CK(cudaMemcpyAsync(ctx->d_run, hr, sizeof(RunState), cudaMemcpyHostToDevice, ctx->stream));
+  const StepState before = save_state(ctx);
+  ctx->batching = true;
+  int rc = BF_OK;
+  for (int q = 0; q < n && rc == BF_OK; ++q) {
+    rc = enqueue_step_graph(ctx, first_step + q);
+    if (rc == 1) rc = fail(ctx, BF_EINVAL, "batched step graph unavailable");
+  }
+  ctx->batching = false;
+  if (rc) return rc;
+  double* hh = reinterpret_cast<double*>(hr + 1);
+  CK(cudaMemcpyAsync(hr, ctx->d_run, sizeof(RunState), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hh, ctx->d_hist, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->profiling) drain_profile(ctx);
+  const int ran = hr->steps + (hr->status == 3 ? 1 : 0);   // the failing step ran too
+  StepState st = before;
+  for (int q = 0; q < ran; ++q) st = advanced(st, ctx->sch.rk_stages);
+  load_state(ctx, st);
+  for (int q = 0; q < hr->steps; ++q)
+    for (int v = 0; v < 5; ++v) hist_out[5 * (call_step + q) + v] = hh[5 * q + v];
+  *done = hr->steps;
+  *status = hr->status;
+  if (hr->status == 3) {
+    decode_error(ctx, hr->key);
+    return BF_ENONPHYSICAL;
+  }
+  return BF_OK;
+}
+
 int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, double target,
                int has_floor, double floor_, double divergence_factor, double* hist_out,
                int* steps_done, int* status) {
   if (!ctx || !ctx->finalized) return fail(ctx, BF_EINVAL, "bf_iterate before bf_finalize");
+  CK(cudaSetDevice(ctx->device));
   *steps_done = 0;
   *status = 0;
-  for (int s = 0; s < max_steps; ++s) {
+  int s = 0;
+  while (s < max_steps) {
+    if (!ctx->batch_off && graph_eligible(ctx)) {
+      // device-side guards: no host round trip per step
+      const int n = std::min(max_steps - s, BATCH_MAX);
+      int done = 0, st = 0;
+      const int rc = run_batch(ctx, first_step + s, n, s, has_target, target, has_floor, floor_,
+                               divergence_factor, hist_out, &done, &st);
+      s += done;
+      *steps_done = s;
+      if (rc) return rc;
+      if (st) {
+        *status = st;
+        break;
+      }
+      continue;
+    }
     double ss[5];
     int rc = bf_step(ctx, first_step + s, ss, nullptr);
     if (rc) return rc;
@@ -2825,6 +2937,7 @@ int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, doubl
     *steps_done = s + 1;
     const int g = history_guard(hist_out, s, has_target, target, has_floor, floor_,
                                 divergence_factor);
+    ++s;
     if (g) {
       *status = g;
       break;

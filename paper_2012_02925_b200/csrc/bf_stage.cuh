@@ -93,6 +93,7 @@ struct Cfg {
 template <int NDIM, int FLUX, int LIM>
 __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
     stage_kernel(const StageArgs a) {
+  if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   using K = Cfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW, PC = K::PC;
   constexpr int NFX = K::NFX, NFY = K::NFY, NPX = K::NPX, NPY = K::NPY;

@@ -46,11 +46,14 @@ BF_DEV void tma_prefetch4(const void* tmap, int x, int y, int z, int s) {
                : "memory");
 }
 
-// 1/b: MUFU seed (~2^-22) and one Newton step (~2^-44 relative).  Used only for
-// the Van Albada limiter quotient, whose error enters the face states as
-// (error) x (eps/4) x D, i.e. ~1e-14 of the cell-to-cell difference.
+// 1/b of the Van Albada limiter quotient.  Default: the ~1 ulp reciprocal
+// (frcp).  -DBF_VA_RCP1: MUFU seed (~2^-22) and one Newton step (~2^-44
+// relative), 2.9% faster on C4 but its error, (error) x (eps/4) x D in the
+// face states, shifts long runs: C1 FAST vs EXACT after 250 / 1000 / 2000
+// steps 1.3e-12 / 1.0e-11 / 1.1e-11 of the freestream pressure, against
+// 9.6e-14 / 7.2e-13 / 1.8e-12 with frcp (profiles/r02_fast_drift_c1.jsonl).
 BF_DEV double frcp1(double b) {
-#ifdef BF_VA_RCP_FULL
+#ifndef BF_VA_RCP1
   return frcp(b);
 #endif
   double r;
@@ -349,6 +352,7 @@ struct VCfg {
 
 template <int NDIM, int LIM, bool K1, bool S0>
 __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl_stage_kernel(const __grid_constant__ StageArgs a) {
+  if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   using K = VCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
   constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
