@@ -489,12 +489,10 @@ __global__ void __launch_bounds__(128) viscous_kernel(const ViscArgs a) {
 }
 
 // Fixed-order per-block reduction of the per-tile partial sums.
-__global__ void __launch_bounds__(256) reduce_kernel(const double* partial, const int* tile_begin,
-                                                     int nblocks, double* out) {
-  __shared__ double red[256 * 5];
-  const int blk = blockIdx.x;
-  if (blk >= nblocks) return;
-  const int tb = tile_begin[blk], te = tile_begin[blk + 1];
+// Fixed-order sum of one block's per-tile partials by a 256-thread CTA (strided
+// per-thread sums, then a shared-memory tree): the same doubles whichever
+// kernel runs it.
+BF_DEV void block_sum(const double* partial, int tb, int te, double* red, double* out5) {
   double x[5] = {0, 0, 0, 0, 0};
   for (int t = tb + threadIdx.x; t < te; t += blockDim.x) {
 #pragma unroll
@@ -510,7 +508,16 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double* partial, cons
     }
     __syncthreads();
   }
-  if (threadIdx.x < 5) out[blk * 5 + threadIdx.x] = red[threadIdx.x];
+  if (threadIdx.x < 5) out5[threadIdx.x] = red[threadIdx.x];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) reduce_kernel(const double* partial, const int* tile_begin,
+                                                     int nblocks, double* out) {
+  __shared__ double red[256 * 5];
+  const int blk = blockIdx.x;
+  if (blk >= nblocks) return;
+  block_sum(partial, tile_begin[blk], tile_begin[blk + 1], red, out + blk * 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -612,15 +619,25 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// End of a batched-iterate step (RunState, bf_internal.h): the norms of the
-// step from the per-block sums in block order (as finish_collect sums them on
-// the host) and check_history_guards (solver.py:836-855) as history_guard in
-// bf_runtime.cu evaluates it, with numpy's NaN semantics.
-__global__ void guard_kernel(const double* blocksum, int nb, const unsigned long long* err,
-                             RunState* rs, double* hist) {
-  if (threadIdx.x != 0 || rs->stop) return;
+// End of a batched-iterate step (RunState, bf_internal.h), one launch instead of
+// the stage-0 reduce, the D2H of the sums and the host guard: the per-block
+// sums (reduce_kernel's arithmetic), the step's norms from them in block order
+// (as finish_collect sums them on the host), check_history_guards
+// (solver.py:836-855) as history_guard in bf_runtime.cu evaluates it, with
+// numpy's NaN semantics, and the reset of the error slot for the next step.
+__global__ void __launch_bounds__(256) guard_kernel(const double* partial, const int* tile_begin,
+                                                    int nb, double* blocksum,
+                                                    unsigned long long* err, RunState* rs,
+                                                    double* hist) {
+  __shared__ double red[256 * 5];
+  if (rs->stop) return;
+  // per-block sums exactly as reduce_kernel forms them (block_sum)
+  for (int b = 0; b < nb; ++b)
+    block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
+  if (threadIdx.x != 0) return;
   const int s = rs->steps;
   const unsigned long long key = *err;
+  *err = ~0ull;   // the next step's error slot (the per-step reset of bf_step)
   if (key != ~0ull && !rs->ignore_errors) {   // non-physical state in this step
     rs->key = key;
     rs->status = 3;
@@ -671,9 +688,9 @@ __global__ void guard_kernel(const double* blocksum, int nb, const unsigned long
   }
 }
 
-cudaError_t launch_guard(const double* blocksum, int nb, const unsigned long long* err,
-                         RunState* rs, double* hist, cudaStream_t s) {
-  guard_kernel<<<1, 32, 0, s>>>(blocksum, nb, err, rs, hist);
+cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
+                         unsigned long long* err, RunState* rs, double* hist, cudaStream_t s) {
+  guard_kernel<<<1, 256, 0, s>>>(partial, tile_begin, nb, blocksum, err, rs, hist);
   return cudaGetLastError();
 }
 

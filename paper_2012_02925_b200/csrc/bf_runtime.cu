@@ -36,8 +36,8 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s);
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
-cudaError_t launch_guard(const double* blocksum, int nb, const unsigned long long* err,
-                         RunState* rs, double* hist, cudaStream_t s);
+cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
+                         unsigned long long* err, RunState* rs, double* hist, cudaStream_t s);
 int stage_tile_rows(int ndim, int lim);
 }  // namespace bf_exact
 namespace bf_fast {
@@ -1909,7 +1909,7 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
       ctx->fill_pending = false;
     }
   }
-  if (flags & F_STAGE0) {
+  if ((flags & F_STAGE0) && !ctx->batching) {   // batched: summed by the guard kernel
     ProfScope ps(ctx, 3);
     auto red = ctx->sch.precision == BF_PRECISION_EXACT ? bf_exact::launch_reduce
                                                         : bf_fast::launch_reduce;
@@ -2656,7 +2656,7 @@ int bf_update_ghosts(bf_ctx* ctx) {
 // copies of its residual sums and error key.
 int enqueue_step(bf_ctx* ctx, int step_index) {
   const int nst = ctx->sch.rk_stages;
-  int rc = reset_error(ctx);
+  int rc = ctx->batching ? BF_OK : reset_error(ctx);   // batched: the guard kernel resets it
   if (rc) return rc;
   for (int k = 0; k < nst; ++k) {
     rc = ghosts_solo(ctx);
@@ -2666,8 +2666,8 @@ int enqueue_step(bf_ctx* ctx, int step_index) {
   }
   if (ctx->batching) {   // norms and guards on the device (RunState)
     ProfScope ps(ctx, 3);
-    CK(bf_exact::launch_guard(ctx->d_blocksum, (int)ctx->blocks.size(), ctx->d_err, ctx->d_run,
-                              ctx->d_hist, ctx->stream));
+    CK(bf_exact::launch_guard(ctx->d_partial, ctx->d_tile_begin, (int)ctx->blocks.size(),
+                              ctx->d_blocksum, ctx->d_err, ctx->d_run, ctx->d_hist, ctx->stream));
     return BF_OK;
   }
   return enqueue_collect(ctx);
@@ -2876,6 +2876,10 @@ static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_
   hr->factor = factor;
   hr->ignore_errors = ignore_errors() ? 1 : 0;
   CK(cudaMemcpyAsync(ctx->d_run, hr, sizeof(RunState), cudaMemcpyHostToDevice, ctx->stream));
+  {   // first step of the batch (later ones: the guard kernel)
+    const int r0 = reset_error(ctx);
+    if (r0) return r0;
+  }
   const StepState before = save_state(ctx);
   ctx->batching = true;
   int rc = BF_OK;

@@ -81,3 +81,19 @@ def test_native_arm_line():
     assert d["config"] == bench.workload_config(1, "weak")
     rep = d["repeats"]
     assert rep["n"] >= 3 and len(rep["ms"]) == rep["n"] and rep["median_ms"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_native_arm_two_gpus(scaling):
+    """--gpus 2 spawns two NCCL ranks itself (needs two visible GPUs)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    d = _run(["--gpus", "2", "--steps", "3", "--warmup", "3", "--skip-cpu", "--skip-e2e",
+              "--scaling", scaling, "--repeats", "1"], 1200)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["n_gpus"] == 2 and d["config"] == bench.workload_config(2, scaling)
+    assert d["scaling"] == scaling and d["comm"]["nranks"] == 2
+    assert all(r["messages_per_stage"] > 0 for r in d["comm"]["per_rank"])
