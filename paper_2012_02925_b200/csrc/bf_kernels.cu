@@ -266,7 +266,10 @@ BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m);
 // One task per CUDA block; the block covers ipt x GHOST_BLOCK items of it
 // (strided by GHOST_BLOCK; ipt = GHOST_ITEMS for large launches, 1 for small).  COPY items load all their values before the
 // first store (GHOST_ITEMS x 6 loads in flight per thread).
-__global__ void __launch_bounds__(GHOST_BLOCK) ghost_kernel(const GhostArgs a) {
+#ifndef BF_GHOST_MINB
+#define BF_GHOST_MINB 1
+#endif
+__global__ void __launch_bounds__(GHOST_BLOCK, BF_GHOST_MINB) ghost_kernel(const GhostArgs a) {
   __shared__ __align__(16) GhostTask ts;   // the task record, staged once
   if (a.stop && *a.stop) return;           // batched iterate stopped (RunState)
   const int2 bm = a.block_map[blockIdx.x];
@@ -352,9 +355,45 @@ BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m) {
     const double sg = t.side == 0 ? -1.0 : 1.0;
     const double* fn = b.base + (long long)ffn(d, 0) * fsz + fo;
     const double nx = sg * fn[0], ny = sg * fn[fsz], nz = sg * fn[2 * fsz];
+    // the usual two ghost layers: every mirror cell's values are loaded before
+    // any ghost store (an item's ghost and interior positions never coincide),
+    // so the loads of both layers are in flight together
+    double pre[2][5];
+    const bool two = t.depth == 2;
+    if (two) {
+#pragma unroll
+      for (int L = 0; L < 2; ++L) {
+        const long long oi = base + sd * ipos(L);
+        pre[L][0] = W[fsz + oi];
+        pre[L][1] = W[2 * fsz + oi];
+        pre[L][2] = W[3 * fsz + oi];
+        pre[L][3] = W[4 * fsz + oi];
+        pre[L][4] = cell_T(b, W, oi, a.t_derived, c);
+      }
+    }
     for (int L = 0; L < t.depth; ++L) {
       const long long og = base + sd * gpos(L);
       const long long oi = base + sd * ipos(L);
+      if (two) {
+        const double u = pre[L & 1][0], v = pre[L & 1][1], w = pre[L & 1][2];
+        if (bc == BC_SLIP) {
+          const double vn = u * nx + v * ny + w * nz;
+          W[fsz + og] = u - 2.0 * vn * nx;
+          W[2 * fsz + og] = v - 2.0 * vn * ny;
+          W[3 * fsz + og] = w - 2.0 * vn * nz;
+        } else {
+          W[fsz + og] = -u;
+          W[2 * fsz + og] = -v;
+          W[3 * fsz + og] = -w;
+        }
+        const double pg = pre[L & 1][3];
+        W[4 * fsz + og] = pg;
+        const double ti = pre[L & 1][4];
+        const double tg = (bc == BC_NOSLIP && c.has_tw) ? 2.0 * c.tw - ti : ti;
+        W[5 * fsz + og] = tg;
+        W[og] = pg / (c.R * tg);
+        continue;
+      }
       const double u = W[fsz + oi], v = W[2 * fsz + oi], w = W[3 * fsz + oi];
       if (bc == BC_SLIP) {
         const double vn = u * nx + v * ny + w * nz;
