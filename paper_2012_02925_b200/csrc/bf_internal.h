@@ -251,6 +251,19 @@ struct StageArgs {
   int push;
   int t_derived;        // interior T is p/(rho R) (viscous dt reads T)
   const int* stop;      // batched iterate: a set flag makes the launch a no-op (null: never)
+  // Fused ghost fill (cell-split kernel, one-rank ctx; off when fill_chunks is
+  // 0): the ghosts of W[cur] — the work of one ghost_kernel launch, cut into
+  // fill_chunks warp chunks, assigned round robin — are written inside the
+  // launch by the warps of its first fill_ctas CTAs; then come the tiles of
+  // tile_list: n_interior tiles that read no ghost cell, then the boundary
+  // tiles, which wait until fill_sync[1] (fill warps done) reaches every fill
+  // warp.  fill_sync[2] counts arrivals (fill warps + boundary tiles); the last
+  // one zeroes the counters for the next launch.
+  int fill_chunks;
+  int fill_ctas;
+  int n_interior;
+  unsigned* fill_sync;
+  GhostArgs fill;
   Consts c;
 };
 

@@ -42,6 +42,38 @@ BF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "mem
 BF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 BF_DEV void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// Programmatic dependent launch (griddepcontrol): the per-stage kernels are
+// launched with programmatic stream serialization, so the next one's CTAs are
+// dispatched while this one drains and wait in pdl_wait() — before anything
+// that reads what the previous kernel wrote (or writes what it reads) — until
+// it has completed and flushed.  pdl_trigger() lets the dependent launch be
+// scheduled once every CTA of this grid has started.
+BF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+BF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Whether this thread's launches use it (set_pdl, per context by the runtime:
+// on for one-wave grids, where it takes ~2 us off a C1 step; off for large
+// ones — C4 measured 1.6% slower with it).
+static thread_local int t_pdl = 0;
+void set_pdl(int on) { t_pdl = on; }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, const Args&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = t_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 BF_DEV void record_error(unsigned long long* err, unsigned long long key) {
   if (key < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, key);
 }
@@ -146,6 +178,12 @@ BF_DEV int face_flux(const double* c0, const double* c1, const double* c2, const
   if (bkind != BFACE_NONE) boundary_overwrite(bkind, side_sign, c0, c1, c2, c3, vs, nx, ny, nz, A, c, F);
   return err;
 }
+
+// Fused ghost fill (StageArgs::fill_ctas, defined after the ghost kernel below)
+__device__ __noinline__ void fill_work(const GhostArgs& g, int nchunks, int worker, int nworkers,
+                                       unsigned* sync, unsigned parties, GhostTask* slot);
+BF_DEV void fill_arrive(unsigned* sync, unsigned n, unsigned parties);
+BF_DEV void fill_wait(const unsigned* sync, int nworkers);
 
 #include "bf_stage.cuh"
 #if !BF_EXACT
@@ -271,7 +309,7 @@ BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m);
 #endif
 __global__ void __launch_bounds__(GHOST_BLOCK, BF_GHOST_MINB) ghost_kernel(const GhostArgs a) {
   __shared__ __align__(16) GhostTask ts;   // the task record, staged once
-  if (a.stop && *a.stop) return;           // batched iterate stopped (RunState)
+  pdl_trigger();
   const int2 bm = a.block_map[blockIdx.x];
   {
     static_assert(sizeof(GhostTask) % 8 == 0, "GhostTask words");
@@ -281,6 +319,8 @@ __global__ void __launch_bounds__(GHOST_BLOCK, BF_GHOST_MINB) ghost_kernel(const
     for (int w = threadIdx.x; w < NW; w += blockDim.x)
       reinterpret_cast<unsigned long long*>(&ts)[w] = src[w];
   }
+  pdl_wait();   // static tables above; the fields below were written by the previous kernel
+  if (a.stop && *a.stop) return;           // batched iterate stopped (RunState)
   __syncthreads();
   const GhostTask& t = ts;
   // items per task < 2^31 (a few face layers of one block)
@@ -306,6 +346,89 @@ __global__ void __launch_bounds__(GHOST_BLOCK, BF_GHOST_MINB) ghost_kernel(const
     const unsigned m = m0 + q * GHOST_BLOCK;
     if (m < items) bc_item(a, t, m);
   }
+}
+
+// ---- fused ghost fill: the work of one ghost_kernel launch done by warps of a
+// stage-kernel launch.  Chunk c is quarter (c & 3) of block-map entry c >> 2:
+// exactly the items threads (c & 3) * 32 + lane of that ghost_kernel block take,
+// so every ghost value is the same double the separate launch writes.
+BF_DEV void ghost_warp_chunk(const GhostArgs& a, const GhostTask& t, int2 bm, int quarter,
+                             int lane) {
+  const unsigned m0 = (unsigned)bm.y + (unsigned)(quarter * 32 + lane);
+  const unsigned items = (unsigned)t.items;
+  if (t.kind == GK_COPY) {
+    G6 v[GHOST_ITEMS];
+    long long doff[GHOST_ITEMS];
+#pragma unroll
+    for (int q = 0; q < GHOST_ITEMS; ++q) {
+      const unsigned m = m0 + q * GHOST_BLOCK;
+      if (q < a.ipt && m < items) copy_load(a, t, m, v[q], doff[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < GHOST_ITEMS; ++q) {
+      const unsigned m = m0 + q * GHOST_BLOCK;
+      if (q < a.ipt && m < items) copy_store(a, t, v[q], doff[q]);
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int q = 0; q < a.ipt; ++q) {
+    const unsigned m = m0 + q * GHOST_BLOCK;
+    if (m < items) bc_item(a, t, m);
+  }
+}
+
+// A participant is through with the counters; the last of `parties` resets them
+// for the next launch (every counter operation precedes its arrival).
+BF_DEV void fill_arrive(unsigned* sync, unsigned n, unsigned parties) {
+  if (atomicAdd(sync + 2, n) + n == parties) {
+    atomicExch(sync + 1, 0u);
+    atomicExch(sync + 2, 0u);
+  }
+}
+
+// Fill worker `worker` of `nworkers` (one warp): chunks worker, worker +
+// nworkers, ...; the chunk's task record is staged in the warp's shared-memory
+// slot (one coalesced load instead of a chain of field loads).  At the end one
+// release increment of the done counter (sync[1]) — the warp's stores are
+// ordered before it by __syncwarp and the cumulative __threadfence — and the
+// warp's arrival.  Out of line: the ghost code's registers stay out of the
+// stage kernel's allocation.
+__device__ __noinline__ void fill_work(const GhostArgs& g, int nchunks, int worker, int nworkers,
+                                       unsigned* sync, unsigned parties, GhostTask* slot) {
+  const int lane = threadIdx.x & 31;
+  constexpr int NW = (int)(sizeof(GhostTask) / 8);
+  int staged = -1;
+  for (int c = worker; c < nchunks; c += nworkers) {
+    const int2 bm = g.block_map[c >> 2];
+    if (bm.x != staged) {
+      __syncwarp();
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g.tasks + bm.x);
+      for (int w = lane; w < NW; w += 32) reinterpret_cast<unsigned long long*>(slot)[w] = src[w];
+      __syncwarp();
+      staged = bm.x;
+    }
+    ghost_warp_chunk(g, *slot, bm, c & 3, lane);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(sync + 1, 1u);
+    fill_arrive(sync, 1u, parties);
+  }
+}
+
+// Acquire: every fill worker's ghost stores are visible to this CTA (the
+// acquire load invalidates stale L1 lines); the proxy fence orders them before
+// the caller's TMA (async proxy) reads of the ghost cells.
+BF_DEV void fill_wait(const unsigned* sync, int nworkers) {
+  for (;;) {
+    unsigned d;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(sync + 1) : "memory");
+    if ((int)d >= nworkers) break;
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 BF_DEV void bc_item(const GhostArgs& a, const GhostTask& t, unsigned m) {
@@ -527,20 +650,25 @@ __global__ void __launch_bounds__(128) viscous_kernel(const ViscArgs a) {
   out[3 * fsz] = fe * A;
 }
 
-// Fixed-order per-block reduction of the per-tile partial sums.
-// Fixed-order sum of one block's per-tile partials by a 256-thread CTA (strided
-// per-thread sums, then a shared-memory tree): the same doubles whichever
-// kernel runs it.
+// Fixed-order per-block reduction of the per-tile partial sums by the first
+// GUARD_NT threads of a CTA (strided per-thread sums, then a shared-memory
+// tree; the other threads only take part in the barriers): the same doubles
+// whichever kernel runs it.
+constexpr int GUARD_NT = 256;
 BF_DEV void block_sum(const double* partial, int tb, int te, double* red, double* out5) {
+  const bool on = threadIdx.x < GUARD_NT;
   double x[5] = {0, 0, 0, 0, 0};
-  for (int t = tb + threadIdx.x; t < te; t += blockDim.x) {
+  if (on)
+    for (int t = tb + threadIdx.x; t < te; t += GUARD_NT) {
 #pragma unroll
-    for (int v = 0; v < 5; ++v) x[v] += partial[(long long)t * 5 + v];
+      for (int v = 0; v < 5; ++v) x[v] += __ldcg(partial + (long long)t * 5 + v);
+    }
+  if (on) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) red[threadIdx.x * 5 + v] = x[v];
   }
-#pragma unroll
-  for (int v = 0; v < 5; ++v) red[threadIdx.x * 5 + v] = x[v];
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+  for (int s = GUARD_NT / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) red[threadIdx.x * 5 + v] += red[(threadIdx.x + s) * 5 + v];
@@ -551,9 +679,11 @@ BF_DEV void block_sum(const double* partial, int tb, int te, double* red, double
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) reduce_kernel(const double* partial, const int* tile_begin,
+__global__ void __launch_bounds__(GUARD_NT) reduce_kernel(const double* partial, const int* tile_begin,
                                                      int nblocks, double* out) {
-  __shared__ double red[256 * 5];
+  __shared__ double red[GUARD_NT * 5];
+  pdl_trigger();
+  pdl_wait();
   const int blk = blockIdx.x;
   if (blk >= nblocks) return;
   block_sum(partial, tile_begin[blk], tile_begin[blk + 1], red, out + blk * 5);
@@ -588,8 +718,7 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
     attr_done |= (1ull << dev);
   }
   if (a.ntiles == 0) return cudaSuccess;
-  k<<<a.ntiles, K::NT, K::BYTES, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, (unsigned)a.ntiles, (unsigned)K::NT, K::BYTES, s, a);
 }
 
 template <int NDIM, int FLUX>
@@ -648,8 +777,7 @@ int stage_tile_rows(int ndim, int lim) {
 
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s) {
   if (a.total_items == 0 || a.nlaunch == 0) return cudaSuccess;
-  ghost_kernel<<<(unsigned)a.nlaunch, GHOST_BLOCK, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(ghost_kernel, (unsigned)a.nlaunch, (unsigned)GHOST_BLOCK, 0, s, a);
 }
 
 cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
@@ -664,18 +792,17 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
 // (as finish_collect sums them on the host), check_history_guards
 // (solver.py:836-855) as history_guard in bf_runtime.cu evaluates it, with
 // numpy's NaN semantics, and the reset of the error slot for the next step.
-__global__ void __launch_bounds__(256) guard_kernel(const double* partial, const int* tile_begin,
-                                                    int nb, double* blocksum,
-                                                    unsigned long long* err, RunState* rs,
-                                                    double* hist) {
-  __shared__ double red[256 * 5];
-  if (rs->stop) return;
+// The guard of one batched step (red: GUARD_NT x 5 doubles of shared memory;
+// every thread of the CTA calls it).
+BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, double* blocksum,
+                       unsigned long long* err, RunState* rs, double* hist, double* red) {
   // per-block sums exactly as reduce_kernel forms them (block_sum)
   for (int b = 0; b < nb; ++b)
     block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
   if (threadIdx.x != 0) return;
+  __threadfence_block();
   const int s = rs->steps;
-  const unsigned long long key = *err;
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(err);
   *err = ~0ull;   // the next step's error slot (the per-step reset of bf_step)
   if (key != ~0ull && !rs->ignore_errors) {   // non-physical state in this step
     rs->key = key;
@@ -727,17 +854,29 @@ __global__ void __launch_bounds__(256) guard_kernel(const double* partial, const
   }
 }
 
+__global__ void __launch_bounds__(GUARD_NT) guard_kernel(const double* partial,
+                                                         const int* tile_begin, int nb,
+                                                         double* blocksum,
+                                                         unsigned long long* err, RunState* rs,
+                                                         double* hist) {
+  __shared__ double red[GUARD_NT * 5];
+  pdl_trigger();
+  pdl_wait();
+  if (rs->stop) return;
+  guard_body(partial, tile_begin, nb, blocksum, err, rs, hist, red);
+}
+
 cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
                          unsigned long long* err, RunState* rs, double* hist, cudaStream_t s) {
-  guard_kernel<<<1, 256, 0, s>>>(partial, tile_begin, nb, blocksum, err, rs, hist);
-  return cudaGetLastError();
+  return launch_pdl(guard_kernel, 1u, (unsigned)GUARD_NT, 0, s, partial, tile_begin, nb, blocksum,
+                    err, rs, hist);
 }
 
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s) {
   if (nblocks == 0) return cudaSuccess;
-  reduce_kernel<<<nblocks, 256, 0, s>>>(partial, tile_begin, nblocks, out);
-  return cudaGetLastError();
+  return launch_pdl(reduce_kernel, (unsigned)nblocks, (unsigned)GUARD_NT, 0, s, partial, tile_begin,
+                    nblocks, out);
 }
 
 }  // namespace BF_NS

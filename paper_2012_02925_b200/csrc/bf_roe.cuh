@@ -144,6 +144,8 @@ struct RCfg {
 template <int NDIM, int LIM, bool K1, bool S0>
 __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
     roe_stage_kernel(const __grid_constant__ StageArgs a) {
+  pdl_trigger();                   // the next kernel may be dispatched (it waits for us)
+  pdl_wait();                      // the previous kernel's writes are complete and visible
   if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   using K = RCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
@@ -620,8 +622,7 @@ static cudaError_t launch_roe_s(const StageArgs& a, cudaStream_t s) {
     attr_done |= (1ull << dev);
   }
   if (a.ntiles == 0) return cudaSuccess;
-  k<<<a.ntiles, K::NT, K::BYTES, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, (unsigned)a.ntiles, (unsigned)K::NT, K::BYTES, s, a);
 }
 
 template <int NDIM, int LIM, bool K1>

@@ -39,6 +39,7 @@ cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblo
 cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
                          unsigned long long* err, RunState* rs, double* hist, cudaStream_t s);
 int stage_tile_rows(int ndim, int lim);
+void set_pdl(int on);
 }  // namespace bf_exact
 namespace bf_fast {
 cudaError_t launch_stage(int ndim, int flux, int lim, const StageArgs& a, cudaStream_t s);
@@ -48,6 +49,7 @@ bool vl_push_compiled();
 cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
+void set_pdl(int on);
 }  // namespace bf_fast
 }  // namespace bf
 
@@ -447,6 +449,17 @@ struct bf_ctx {
                                    // interior tiles (BF_HIDE_GHOSTS=1; measured slower)
   bool fill_pending = false;       // this stage's ghost fill is queued on comm_stream
   bool no_overlap = false;         // BF_NO_OVERLAP=1: exchange in line (A/B timing)
+  // fused ghost fill (StageArgs::fill_ctas): the cell-split kernel's launch fills
+  // the ghosts itself; tiles ordered interior-first (reading no ghost cell)
+  int* d_tiles_fused = nullptr;
+  int n_fused_in = 0;
+  int fused_mode = -1;             // BF_FUSED_FILL: 0 off, 1 on, unset: fused_fill_pays
+
+  int fill_ctas_env = 0;           // BF_FILL_CTAS=n: fill-only CTAs per fused launch
+  int num_sms = 148;
+  int pdl_mode = -1;               // BF_PDL: 0 off, 1 on, unset: one-wave grids (use_pdl)
+  unsigned* d_fill_sync = nullptr; // claim / done / arrived counters
+  bool fuse_next = false;          // the next stage launch fills the ghosts of W[cur]
   bool counted = false;           // registered in the per-device live-context count
   // one RK step as a CUDA graph (standalone Euler ctx), per starting buffer and
   // profiling mode; a profiled graph records its own timing events
@@ -1635,16 +1648,45 @@ int build_tiles(bf_ctx* ctx) {
         remote[ctx->index_of[L.block]][L.face] = true;
         any = true;
       }
-    std::vector<int> tin, tbd;
+    std::vector<int> tin, tbd, fin, fbd;
     const int TJ = bf_exact::stage_tile_rows(ctx->ndim, ctx->sch.limiter);
+    // a tile reads cells [i0 - HALO, i0 + TI + HALO) x [j0 - HALO, j0 + TJ + HALO) x
+    // [k0 - HALO, k0 + kc + HALO): it reads face f's ghost cells when that range
+    // crosses the face
+    auto touches = [&](const Tile& t, int f) {
+      const HostBlock& hb = ctx->blocks[t.block];
+      switch (f) {
+        case 0: return t.i0 < HALO;
+        case 1: return t.i0 + TI + HALO > hb.n[0];
+        case 2: return t.j0 < HALO;
+        case 3: return t.j0 + TJ + HALO > hb.n[1];
+        case 4: return ctx->ndim == 3 && t.k0 < HALO;
+        default: return ctx->ndim == 3 && t.k0 + t.kc + HALO > hb.n[2];
+      }
+    };
     for (int q = 0; q < (int)tiles.size(); ++q) {
       const Tile& t = tiles[q];
-      const HostBlock& hb = ctx->blocks[t.block];
       const auto& rf = remote[t.block];
-      const bool bd = (rf[0] && t.i0 == 0) || (rf[1] && t.i0 + TI >= hb.n[0]) ||
-                      (rf[2] && t.j0 == 0) || (rf[3] && t.j0 + TJ >= hb.n[1]) ||
-                      (ctx->ndim == 3 && ((rf[4] && t.k0 == 0) || (rf[5] && t.k0 + t.kc >= hb.n[2])));
+      bool bd = false, any_face = false;
+      for (int f = 0; f < 6; ++f) {
+        const bool hit = touches(t, f);
+        bd = bd || (rf[f] && hit);
+        any_face = any_face || hit;
+      }
       (bd ? tbd : tin).push_back(q);
+      (any_face ? fbd : fin).push_back(q);
+    }
+    // fused ghost fill order: tiles reading no ghost cell first, then the others
+    ctx->n_fused_in = (int)fin.size();
+    fin.insert(fin.end(), fbd.begin(), fbd.end());
+    {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, std::max<size_t>(fin.size(), 1) * sizeof(int)));
+      if (!fin.empty()) CK(cudaMemcpy(q, fin.data(), fin.size() * sizeof(int), cudaMemcpyHostToDevice));
+      ctx->d_tiles_fused = static_cast<int*>(q);
+      CK(cudaMalloc(&q, 4 * sizeof(unsigned)));
+      CK(cudaMemset(q, 0, 4 * sizeof(unsigned)));
+      ctx->d_fill_sync = static_cast<unsigned*>(q);
     }
     ctx->split_tiles = any;
     ctx->split_forced = force;
@@ -1844,6 +1886,46 @@ int stage_flags(bf_ctx* ctx, int step_index, int k, int nst) {
   return flags;
 }
 
+// Fused ghost fill (StageArgs::fill_ctas): on a one-rank inviscid ctx the FAST
+// cell-split Van Leer launch fills the ghosts of W[cur] itself — the first
+// fill_ctas CTAs do the ghost_kernel's work while the tiles that read no ghost
+// cell run, the boundary tiles wait for it — instead of a separate ghost launch
+// before every stage.  BF_FUSED_FILL=0 / 1 forces it off / on (A/B, tests;
+// default: fused_fill_pays), BF_FILL_CTAS=n sets the fill CTAs per launch (both
+// read at context creation).
+//
+// Fill-only CTAs of a fused launch: when the tiles and one fill warp per
+// chunk fit on the SMs at once, that many (latency: one chunk per warp);
+// otherwise BF_FILL_CTAS (default 16), which run beside the interior tiles.
+int fill_ctas_for(const bf_ctx* ctx) {
+  if (ctx->fill_ctas_env > 0) return ctx->fill_ctas_env;
+  const int wpc = TI * bf_exact::stage_tile_rows(ctx->ndim, ctx->sch.limiter) / 32;
+  const int one_each = (4 * ctx->nmap_fill + wpc - 1) / wpc;
+  if (ctx->ntiles + one_each <= ctx->num_sms) return one_each;
+  return 16;
+}
+
+// Where the fused fill pays (profiles/r02_fused_fill.jsonl): a small fill —
+// latency-bound, C2: 0.128 -> 0.117 ms per step — hidden behind at least a
+// wave of interior tiles.  A large one (C4: ~1.2M ghost items, 0.10 ms) is
+// bound by the SMs' outstanding strided-sector misses: squeezed onto a few
+// fill CTAs it takes as many SM-milliseconds as the whole-GPU ghost launch
+// (C4 stage 1.44-2.4 ms with 32-8 fill CTAs vs 1.20 + 0.10 ms), and with too
+// few interior tiles (C1) the boundary tiles just wait for it.
+bool fused_fill_pays(const bf_ctx* ctx) {
+  return ctx->items_fill <= (1LL << 18) && ctx->n_fused_in >= ctx->num_sms;
+}
+
+bool fused_fill_ok(const bf_ctx* ctx, int flags) {
+  const bool on = ctx->fused_mode < 0 ? fused_fill_pays(ctx) : ctx->fused_mode == 1;
+  return on && ctx->sch.precision != BF_PRECISION_EXACT && !ctx->sch.viscous &&
+         bf_fast::vl_active(ctx->sch.flux, flags) && ctx->nranks == 1 && !ctx->comm &&
+         !ctx->group && ctx->r1_bc.empty() && ctx->n_unpack == 0 && !ctx->split_forced &&
+         !ctx->hide_fill && ctx->other_filled && !ctx->pushed &&
+         !(ctx->push_ok && push_enabled()) && ctx->nmap_fill > 0 && ctx->ntiles > 0 &&
+         ctx->d_tiles_fused && ctx->d_fill_sync;
+}
+
 int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   StageArgs a{};
   a.blocks = ctx->d_blocks;
@@ -1877,12 +1959,21 @@ int launch_stage_kernel(bf_ctx* ctx, int k, int flags, double alpha) {
   a.push = (vl && ctx->push_ok && push_enabled()) ? 1 : 0;
   a.push_rules = ctx->d_push;
   a.push_range = ctx->d_push_range;
+  if (ctx->fuse_next) {   // this launch fills the ghosts of W[cur] (fused_fill_ok)
+    a.fill = ghost_args(ctx, false);
+    a.fill_ctas = fill_ctas_for(ctx);
+    a.fill_chunks = 4 * ctx->nmap_fill;
+    a.n_interior = ctx->n_fused_in;
+    a.fill_sync = ctx->d_fill_sync;
+    a.tile_list = ctx->d_tiles_fused;
+    ctx->fuse_next = false;
+  }
+  // two launches only when they buy an overlap (NCCL messages in flight) or
+  // when forced; the split costs tile-order L2 locality and a second tail
+  const bool split = !a.fill_chunks && ctx->split_tiles &&
+                     (ctx->split_forced || ctx->exchange_pending || ctx->fill_pending);
   {
     ProfScope ps(ctx, 0);
-    // two launches only when they buy an overlap (NCCL messages in flight) or
-    // when forced; the split costs tile-order L2 locality and a second tail
-    const bool split = ctx->split_tiles &&
-                       (ctx->split_forced || ctx->exchange_pending || ctx->fill_pending);
     if (!split) {
       CK(stage_fn(ctx)(ctx->ndim, ctx->sch.flux, ctx->sch.limiter, a, ctx->stream));
     } else {
@@ -2044,6 +2135,10 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   if (const char* e = std::getenv("BF_NO_OVERLAP")) ctx->no_overlap = e[0] == '1';
   if (const char* e = std::getenv("BF_GRAPH")) ctx->graph_off = e[0] == '0';
   if (const char* e = std::getenv("BF_BATCH")) ctx->batch_off = e[0] == '0';
+  if (const char* e = std::getenv("BF_FUSED_FILL")) ctx->fused_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = std::getenv("BF_FILL_CTAS")) ctx->fill_ctas_env = std::atoi(e);
+  if (const char* e = std::getenv("BF_PDL")) ctx->pdl_mode = e[0] == '0' ? 0 : 1;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
                                                                         cudaStreamNonBlocking) !=
                                                   cudaSuccess) {
@@ -2168,6 +2263,8 @@ void bf_destroy(bf_ctx* ctx) {
   if (ctx->ev_bd) cudaEventDestroy(ctx->ev_bd);
   cudaFree(ctx->d_tiles_in);
   cudaFree(ctx->d_tiles_bd);
+  cudaFree(ctx->d_tiles_fused);
+  cudaFree(ctx->d_fill_sync);
   const int dev = ctx->device;
   const bool counted = ctx->counted;
   delete ctx;
@@ -2652,16 +2749,31 @@ int bf_update_ghosts(bf_ctx* ctx) {
   return BF_OK;
 }
 
+// Programmatic dependent launch for this context's kernels (bf_kernels.cu
+// launch_pdl): on when the stage grid is one wave (launch latency dominates).
+void use_pdl(const bf_ctx* ctx) {
+  const int on = ctx->pdl_mode < 0 ? (ctx->ntiles <= ctx->num_sms ? 1 : 0) : ctx->pdl_mode;
+  bf_exact::set_pdl(on);
+  bf_fast::set_pdl(on);
+}
+
 // The device work of one RK step (solver.py:786-814) on ctx->stream, up to the
 // copies of its residual sums and error key.
 int enqueue_step(bf_ctx* ctx, int step_index) {
   const int nst = ctx->sch.rk_stages;
+  use_pdl(ctx);
   int rc = ctx->batching ? BF_OK : reset_error(ctx);   // batched: the guard kernel resets it
   if (rc) return rc;
   for (int k = 0; k < nst; ++k) {
-    rc = ghosts_solo(ctx);
-    if (rc) return rc;
-    rc = launch_stage_kernel(ctx, k, stage_flags(ctx, step_index, k, nst), rk_alpha(nst, k));
+    const int flags = stage_flags(ctx, step_index, k, nst);
+    if (fused_fill_ok(ctx, flags)) {   // the stage launch fills the ghosts itself
+      ctx->fuse_next = true;
+      ctx->ghost_buf = ctx->cur;
+    } else {
+      rc = ghosts_solo(ctx);
+      if (rc) return rc;
+    }
+    rc = launch_stage_kernel(ctx, k, flags, rk_alpha(nst, k));
     if (rc) return rc;
   }
   if (ctx->batching) {   // norms and guards on the device (RunState)

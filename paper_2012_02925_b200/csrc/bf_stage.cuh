@@ -93,6 +93,8 @@ struct Cfg {
 template <int NDIM, int FLUX, int LIM>
 __global__ void __launch_bounds__(Cfg<NDIM, LIM>::NT, Cfg<NDIM, LIM>::MINB)
     stage_kernel(const StageArgs a) {
+  pdl_trigger();                   // the next kernel may be dispatched (it waits for us)
+  pdl_wait();                      // the previous kernel's writes are complete and visible
   if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   using K = Cfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW, PC = K::PC;

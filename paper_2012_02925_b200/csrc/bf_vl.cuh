@@ -352,11 +352,25 @@ struct VCfg {
 
 template <int NDIM, int LIM, bool K1, bool S0>
 __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl_stage_kernel(const __grid_constant__ StageArgs a) {
-  if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
+  pdl_trigger();   // the next kernel may be dispatched (it waits in pdl_wait for this one)
   using K = VCfg<NDIM, LIM>;
   constexpr int NT = K::NT, TJ = K::TJ, PLANE = K::PLANE, PW = K::PW;
-  constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
   extern __shared__ __align__(128) double smem[];
+  // fused ghost fill (StageArgs::fill_chunks): fill-only CTAs first, then the
+  // tiles — interior first; the boundary tiles wait for the whole fill
+  const bool fused = a.fill_chunks > 0;
+  const int nworkers = a.fill_ctas * (NT / 32);
+  const unsigned parties = (unsigned)(nworkers + a.ntiles - a.n_interior);
+  if (fused && (int)blockIdx.x < a.fill_ctas) {
+    pdl_wait();
+    if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
+    fill_work(a.fill, a.fill_chunks, (int)(blockIdx.x * (NT / 32) + threadIdx.x / 32), nworkers,
+              a.fill_sync, parties, reinterpret_cast<GhostTask*>(smem) + threadIdx.x / 32);
+    return;
+  }
+  const int cta = fused ? (int)blockIdx.x - a.fill_ctas : (int)blockIdx.x;
+  const bool wait_fill = fused && cta >= a.n_interior;
+  constexpr int NFX = K::NFX, NFY = K::NFY, NHY = K::NHY;
   double* const sW = smem + K::OW;
   double* const sHP = smem + K::OHP;
   double* const sHM = smem + K::OHM;
@@ -369,7 +383,7 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
   PushSmem* const sPS = reinterpret_cast<PushSmem*>(smem + K::OPS);
   // bars[0..2]: plane ring, bars[3]: geometry group, bars[4]: Q0 / dt group
 
-  const int tile_id = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
+  const int tile_id = a.tile_list ? a.tile_list[cta] : cta;
   const Tile t = a.tiles[tile_id];
   const DevBlock b = a.blocks[t.block];
   const Consts& c = a.c;
@@ -483,9 +497,18 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
   double lamz = 0.0;                 // z part of the stage-0 lambda of cell k
   double rsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
+  // static tables (tile, block, tensor maps) are read before the wait: up to
+  // here the CTA overlaps the previous kernel's drain
+  if (tid < NTMAP) asm volatile("prefetch.tensormap [%0];" ::"l"(tm + tid * 128) : "memory");
+  pdl_wait();                      // the previous kernel's writes are complete and visible
+  if (a.stop && *a.stop) return;   // batched iterate stopped (RunState)
   if (tid == 0) {
     for (int q = 0; q < 5; ++q) mbar_init(bars + q, 1);
     fence_mbar_init();
+    if (wait_fill) {   // the fill workers' ghost stores, published by the barrier below
+      fill_wait(a.fill_sync, nworkers);
+      fill_arrive(a.fill_sync, 1u, parties);
+    }
   }
   if (BF_VL_PUSH && a.push) {   // this block's ghost-push rules -> shared memory
     const int* rg = a.push_range + t.block * 12;
@@ -930,8 +953,7 @@ static cudaError_t launch_vl_s(const StageArgs& a, cudaStream_t s) {
     attr_done |= (1ull << dev);
   }
   if (a.ntiles == 0) return cudaSuccess;
-  k<<<a.ntiles, K::NT, K::BYTES, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, (unsigned)(a.ntiles + (a.fill_chunks ? a.fill_ctas : 0)), (unsigned)K::NT, K::BYTES, s, a);
 }
 
 template <int NDIM, int LIM, bool K1>
