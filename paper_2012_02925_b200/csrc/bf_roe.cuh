@@ -107,6 +107,10 @@ BF_DEV double recon_side(double wm, double w0, double wp, const Consts& c) {
   }
 }
 
+#ifndef BF_ROE_SMEM_BLOCK
+#define BF_ROE_SMEM_BLOCK 0
+#endif
+
 template <int NDIM, int LIM>
 struct RCfg {
   static constexpr int TJ = Cfg<NDIM, LIM>::TJ;   // same tiles as the other stage kernels
@@ -132,7 +136,8 @@ struct RCfg {
   static constexpr int OZQ = r16(OQ + 6 * NT);
   static constexpr int ORS = r16(OZQ + (NDIM == 3 ? 5 * NT : 0));   // [NT/32][5] sum(R^2)
   static constexpr int OBAR = r16(ORS + 5 * (NT / 32));
-  static constexpr int TOTAL = OBAR + 8;
+  static constexpr int OBLK = OBAR + 8;                  // the tile's DevBlock
+  static constexpr int TOTAL = OBLK + (int)(sizeof(DevBlock) + 7) / 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr int MINB = (NDIM == 2) ? BF_VL2D_MINB : 1;
   static constexpr unsigned WBYTES = 5u * PLANE * 8u;
@@ -165,7 +170,18 @@ __global__ void __launch_bounds__(RCfg<NDIM, LIM>::NT, RCfg<NDIM, LIM>::MINB)
 
   const int tile_id = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
   const Tile t = a.tiles[tile_id];
+#if BF_ROE_SMEM_BLOCK
+  // the block record in shared memory (as in vl_stage_kernel): measured 1%
+  // slower here (C4 Roe stage 1.527 vs 1.512 ms), off by default
+  DevBlock* const sBk = reinterpret_cast<DevBlock*>(smem + K::OBLK);
+  if (threadIdx.x < sizeof(DevBlock) / 8)
+    reinterpret_cast<unsigned long long*>(sBk)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(a.blocks + t.block)[threadIdx.x];
+  __syncthreads();
+  const DevBlock& b = *sBk;
+#else
   const DevBlock b = a.blocks[t.block];
+#endif
   const Consts& c = a.c;
   const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
   const int tid = threadIdx.x;

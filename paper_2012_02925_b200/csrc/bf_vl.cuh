@@ -35,6 +35,12 @@
 #ifndef BF_VL_PUSH
 #define BF_VL_PUSH 0
 #endif
+// The tile's block record (DevBlock) in shared memory instead of a register
+// copy: C4 stage 1.158 -> 1.115 ms (S1 spills 32/52 B -> 0; the k loop reloaded
+// spilled invariants from local memory every plane).  -DBF_VL_SMEM_BLOCK=0: copy.
+#ifndef BF_VL_SMEM_BLOCK
+#define BF_VL_SMEM_BLOCK 1
+#endif
 #ifndef BF_VL2D_MINB
 #define BF_VL2D_MINB 2
 #endif
@@ -342,7 +348,8 @@ struct VCfg {
   static constexpr int OQ = r16(OZG + (NDIM == 3 ? 8 * NT : 0));   // [6][TJ][TI] Q0, dt/V
   static constexpr int OPS = r16(OQ + (QLDG ? 5 * (NT / 32) : 6 * NT));   // PushSmem
   static constexpr int OBAR = r16(OPS + (BF_VL_PUSH ? (int)((sizeof(PushSmem) + 7) / 8) : 0));
-  static constexpr int TOTAL = OBAR + 8;
+  static constexpr int OBLK = OBAR + 8;                  // the tile's DevBlock (BF_VL_SMEM_BLOCK)
+  static constexpr int TOTAL = OBLK + (int)(sizeof(DevBlock) + 7) / 8;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr unsigned WBYTES = 5u * PLANE * 8u;
   static constexpr unsigned GYZBYTES = (4u * NFY + (NDIM == 3 ? 4u * NT : 0u)) * 8u;
@@ -385,7 +392,18 @@ __global__ void __launch_bounds__(VCfg<NDIM, LIM>::NT, VCfg<NDIM, LIM>::MINB) vl
 
   const int tile_id = a.tile_list ? a.tile_list[cta] : cta;
   const Tile t = a.tiles[tile_id];
+#if BF_VL_SMEM_BLOCK
+  // the block record in shared memory: its fields are re-read with LDS instead
+  // of being held in registers across the k loop (or spilled to local memory)
+  DevBlock* const sBk = reinterpret_cast<DevBlock*>(smem + K::OBLK);
+  if (threadIdx.x < sizeof(DevBlock) / 8)
+    reinterpret_cast<unsigned long long*>(sBk)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(a.blocks + t.block)[threadIdx.x];
+  __syncthreads();
+  const DevBlock& b = *sBk;
+#else
   const DevBlock b = a.blocks[t.block];
+#endif
   const Consts& c = a.c;
   const unsigned char* const tm = a.tmaps + (size_t)t.block * NTMAP * 128;
   const int tid = threadIdx.x;
