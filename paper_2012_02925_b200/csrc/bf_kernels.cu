@@ -796,29 +796,38 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
 // every thread of the CTA calls it).
 BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, double* blocksum,
                        unsigned long long* err, RunState* rs, double* hist, double* red) {
-  // per-block sums exactly as reduce_kernel forms them (block_sum)
-  for (int b = 0; b < nb; ++b)
+  // thread 0 loads the run state and the step's error key up front: their
+  // latency overlaps the sums (one launch-bound chain less on small grids)
+  RunState r;
+  unsigned long long key = ~0ull;
+  if (threadIdx.x == 0) {
+    r = *rs;
+    key = *reinterpret_cast<volatile unsigned long long*>(err);
+  }
+  // per-block sums exactly as reduce_kernel forms them (block_sum); the step's
+  // norms from them in block order (thread 0 reads each block's sums from red[0..4]
+  // before the next block_sum writes its own slots there)
+  double h[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b) {
     block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
+    if (threadIdx.x == 0)
+      for (int v = 0; v < 5; ++v) h[v] = h[v] + red[v];
+  }
   if (threadIdx.x != 0) return;
-  __threadfence_block();
-  const int s = rs->steps;
-  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(err);
+  const int s = r.steps;
   *err = ~0ull;   // the next step's error slot (the per-step reset of bf_step)
-  if (key != ~0ull && !rs->ignore_errors) {   // non-physical state in this step
+  if (key != ~0ull && !r.ignore_errors) {   // non-physical state in this step
     rs->key = key;
     rs->status = 3;
     rs->stop = 1;
     return;
   }
-  double h[5] = {0, 0, 0, 0, 0};
-  for (int b = 0; b < nb; ++b)
-    for (int v = 0; v < 5; ++v) h[v] = h[v] + blocksum[5 * b + v];
   for (int v = 0; v < 5; ++v) {
     h[v] = sqrt(h[v]);
     hist[5 * s + v] = h[v];
   }
-  if (!rs->has_base) {
-    for (int v = 0; v < 5; ++v) rs->base[v] = h[v];
+  if (!r.has_base) {
+    for (int v = 0; v < 5; ++v) rs->base[v] = r.base[v] = h[v];
     rs->has_base = 1;
   }
   rs->steps = s + 1;
@@ -829,23 +838,23 @@ BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, dou
     return m;
   };
   int g = 0;
-  if (rs->has_floor && npmax(h) <= rs->floor_) {
+  if (r.has_floor && npmax(h) <= r.floor_) {
     g = 1;
   } else {
-    const double* bs = rs->base;
+    const double* bs = r.base;
     const double bmax = npmax(bs);
     bool any = false, bad = false;
     double rmax = 0.0;
     for (int v = 0; v < 5; ++v) {
       if (!(bs[v] > 1e-12 * bmax)) continue;
-      const double r = h[v] / bs[v];
-      if (!isfinite(r)) bad = true;
-      rmax = any ? (r > rmax ? r : rmax) : r;
+      const double q = h[v] / bs[v];
+      if (!isfinite(q)) bad = true;
+      rmax = any ? (q > rmax ? q : rmax) : q;
       any = true;
     }
     if (any) {
-      if (bad || rmax > rs->factor) g = 2;
-      else if (rs->has_target && rmax <= rs->target) g = 1;
+      if (bad || rmax > r.factor) g = 2;
+      else if (r.has_target && rmax <= r.target) g = 1;
     }
   }
   if (g) {
