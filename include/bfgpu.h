@@ -132,12 +132,22 @@ int bf_add_block(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
    P = dims + 2*ghost, element strides node_strides[0..ndim-1] along i, j, k
    (the reference's C-ordered Block.nodes[c] is passed as it is).  Face geometry and volumes are computed on the device
    with compute_metrics' operation order (mesh.py:250-331), bitwise equal to
-   the host metrics; an inverted interior cell returns BF_EMETRIC with the
-   reference's MetricError text.  Moves ndim/9 of bf_add_block's geometry
-   bytes (one node triple per cell instead of nine face-vector components). */
+   the host metrics; an inverted interior cell is reported by bf_sync_blocks
+   (or bf_finalize) as BF_EMETRIC with the reference's MetricError text.
+   Asynchronous: the node copy (pinned `nodes` move at full link speed) and
+   the metric kernels of one block overlap the next call's allocation and
+   copy; `nodes` must stay valid until bf_sync_blocks / bf_finalize returns.
+   Moves ndim/9 of bf_add_block's geometry bytes (one node triple per cell
+   instead of nine face-vector components). */
 int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_depth,
                        const double* const* nodes, const long long node_strides[3],
                        const double* const* source);
+
+/* Wait for the bf_add_block_nodes registrations in flight; the first block
+   (in registration order) with an inverted interior cell -> BF_EMETRIC
+   "block <id>: inverted cell at interior index (i, j, k)" (mesh.py
+   compute_metrics' MetricError).  Called by bf_finalize as well.         */
+int bf_sync_blocks(bf_ctx* ctx);
 
 /* One physical patch (solver.py:281-403, 526-580).  box[6] = (i0,i1,j0,j1,k0,k1)
    in the block's interior cell indices (BoundarySpec.box).  dirichlet: for

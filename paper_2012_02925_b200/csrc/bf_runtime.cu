@@ -411,6 +411,7 @@ struct HostBlock {
   std::vector<unsigned char> bface_h[6];
   unsigned char* bface_d[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool has_src = false;
+  unsigned long long* d_bad = nullptr;   // bf_add_block_nodes: inverted-cell flag in flight
   int tile_begin = 0, tile_end = 0;
   long long cells() const { return (long long)n[0] * n[1] * n[2]; }
   long long off(int i, int j, int k) const { return i + sy * (long long)j + sz * (long long)k; }
@@ -437,6 +438,8 @@ struct bf_ctx {
   // halo exchange overlapped with interior tiles (bf_step): messages + unpack on
   // comm_stream while the stage kernel runs the tiles that read no remote ghost
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // bf_add_block_nodes: node copies
+  std::vector<std::pair<double*, size_t>> staging;   // node buffers in flight (bf_sync_blocks)
   cudaEvent_t ev_filled = nullptr, ev_unpacked = nullptr;
   cudaEvent_t ev_bd = nullptr;     // boundary tiles of the stage done (comm_stream)
   int* d_tiles_in = nullptr;       // tile ids reading no remote-received ghost cell
@@ -2201,7 +2204,12 @@ void bf_destroy(bf_ctx* ctx) {
   // leave an unpack queued on comm_stream) drains before they are recycled
   cudaStreamSynchronize(ctx->stream);
   if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  for (auto& hb : ctx->blocks)
+    if (hb.d_bad) cudaFree(hb.d_bad);
+  for (auto& b : ctx->staging) arena_free(ctx->device, b.first, b.second);
+  ctx->staging.clear();
   for (auto& row : ctx->gexec)
     for (auto& ex : row)
       if (ex) cudaGraphExecDestroy(ex);
@@ -2258,6 +2266,7 @@ void bf_destroy(bf_ctx* ctx) {
   else if (ctx->comm) nccl().CommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->ev_filled) cudaEventDestroy(ctx->ev_filled);
   if (ctx->ev_unpacked) cudaEventDestroy(ctx->ev_unpacked);
   if (ctx->ev_bd) cudaEventDestroy(ctx->ev_bd);
@@ -2430,18 +2439,43 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
       return fail(ctx, BF_EINVAL, "node arrays must be dense (strides %lld %lld %lld)", st[0],
                   st[1], st[2]);
   }
+  static const bool trace = std::getenv("BF_TRACE_BLOCKS") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "bf_add_block_nodes %d %-8s %8.3f ms\n", block_id, what,
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   int rc = add_block_arena(ctx, block_id, dims, ghost_depth, source != nullptr, hb);
   if (rc) return rc;
+  mark("arena");
   const int ndim = ctx->ndim;
   DevBlock& d = hb.dev;
   cudaStream_t st = ctx->stream;
+  // the node copy runs on the copy stream, beside this block's arena memset and
+  // the previous block's metric kernels on ctx->stream (no host sync per block:
+  // bf_sync_blocks checks the metric flags)
+  if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaEvent_t ev = nullptr;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   // padded node arrays (P0+1) x (P1+1) [x (P2+1)], Fortran order
   const long long N0 = hb.P[0] + 1, N1 = hb.P[1] + 1, N2 = ndim == 3 ? hb.P[2] + 1 : 1;
   const long long nn = N0 * N1 * N2;
-  double* dn = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&dn), sizeof(double) * ndim * nn, st));
+  // node staging from the arena cache (no stream-ordered pool growth on the host
+  // path of every block); back to the cache at bf_sync_blocks
+  const size_t dn_bytes = sizeof(double) * ndim * nn;
+  double* dn = static_cast<double*>(arena_alloc(ctx->device, dn_bytes));
+  if (!dn) return fail(ctx, BF_ECUDA, "cudaMalloc(%zu bytes) failed for block %d nodes", dn_bytes, block_id);
+  ctx->staging.push_back({dn, dn_bytes});
   for (int c = 0; c < ndim; ++c)
-    CK(cudaMemcpyAsync(dn + c * nn, nodes[c], sizeof(double) * nn, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dn + c * nn, nodes[c], sizeof(double) * nn, cudaMemcpyHostToDevice,
+                       ctx->copy_stream));
+  mark("copy");
+  CK(cudaEventRecord(ev, ctx->copy_stream));
+  CK(cudaStreamWaitEvent(st, ev, 0));
+  CK(cudaEventDestroy(ev));   // released once the recorded work completes
   ctx->bytes_h2d += (long long)sizeof(double) * ndim * nn;
   NodeView nv{dn, dn + nn, ndim == 3 ? dn + 2 * nn : nullptr, node_strides[0], node_strides[1],
               ndim == 3 ? node_strides[2] : 0};
@@ -2466,10 +2500,6 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
                                                          hb.n[0], hb.n[1], hb.n[2], hb.g, hb.gk,
                                                          bad);
   CK(cudaGetLastError());
-  unsigned long long hbad = ~0ull;
-  CK(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
-  CK(cudaFreeAsync(bad, st));
-  CK(cudaFreeAsync(dn, st));
   if (hb.has_src) {
     const long long n = ncell;
     double* tmp = nullptr;
@@ -2483,14 +2513,8 @@ int bf_add_block_nodes(bf_ctx* ctx, int block_id, const int dims[3], int ghost_d
     }
     CK(cudaFreeAsync(tmp, st));
   }
-  CK(cudaStreamSynchronize(st));
-  if (hbad != ~0ull) {
-    const unsigned long long k = hbad % (unsigned long long)hb.n[2];
-    const unsigned long long r = hbad / (unsigned long long)hb.n[2];
-    const unsigned long long j = r % (unsigned long long)hb.n[1], i = r / (unsigned long long)hb.n[1];
-    return fail(ctx, BF_EMETRIC, "block %d: inverted cell at interior index (%llu, %llu, %llu)",
-                block_id, i, j, k);
-  }
+  mark("metrics");
+  hb.d_bad = bad;   // inverted-cell flag, checked by bf_sync_blocks
   d.order = (int)ctx->blocks.size();
   ctx->index_of[block_id] = (int)ctx->blocks.size();
   guard.commit();
@@ -2610,9 +2634,34 @@ int bf_add_link(bf_ctx* ctx, int block_id, int face, const int box[6], const int
   return BF_OK;
 }
 
+int bf_sync_blocks(bf_ctx* ctx) {
+  if (!ctx) return BF_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (auto& b : ctx->staging) arena_free(ctx->device, b.first, b.second);
+  ctx->staging.clear();
+  int rc = BF_OK;
+  for (HostBlock& hb : ctx->blocks) {
+    if (!hb.d_bad) continue;
+    unsigned long long bad = ~0ull;
+    CK(cudaMemcpy(&bad, hb.d_bad, sizeof bad, cudaMemcpyDeviceToHost));
+    CK(cudaFree(hb.d_bad));
+    hb.d_bad = nullptr;
+    if (bad != ~0ull && rc == BF_OK) {
+      const unsigned long long k = bad % (unsigned long long)hb.n[2];
+      const unsigned long long r = bad / (unsigned long long)hb.n[2];
+      const unsigned long long j = r % (unsigned long long)hb.n[1], i = r / (unsigned long long)hb.n[1];
+      rc = fail(ctx, BF_EMETRIC, "block %d: inverted cell at interior index (%llu, %llu, %llu)",
+                hb.id, i, j, k);
+    }
+  }
+  return rc;
+}
+
 int bf_finalize(bf_ctx* ctx) {
   if (!ctx) return BF_EINVAL;
   if (ctx->finalized) return BF_OK;
+  if (int rc0 = bf_sync_blocks(ctx)) return rc0;
   static const bool trace = std::getenv("BF_TRACE_FINALIZE") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {

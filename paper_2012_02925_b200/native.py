@@ -61,6 +61,7 @@ PROTOTYPES = {
     "bf_last_error": (_I, [_P, C.c_char_p, C.c_size_t]),
     "bf_add_block": (_I, [_P, _I, _PI, _I, _PPD, _PD, _PPD]),
     "bf_add_block_nodes": (_I, [_P, _I, _PI, _I, _PPD, _PLL, _PPD]),
+    "bf_sync_blocks": (_I, [_P]),
     "bf_add_bc_patch": (_I, [_P, _I, _I, _I, _PI, _PD]),
     "bf_add_bc_patch_ext": (_I, [_P, _I, _I, _I, _PI, _PD, _PD]),
     "bf_add_viscous_geometry": (_I, [_P, _I, _PPD]),

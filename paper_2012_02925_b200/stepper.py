@@ -180,6 +180,7 @@ class GpuContext:
         if not self.ctx:
             raise NativeLibraryError(f"bf_create failed (device {device}, rank {rank}/{nranks})")
         self.setups = {}
+        self._keep_nodes = []
         for cid in self.child_ids:
             s = setups[cid] if setups is not None else \
                 _BlockSetup(plan, cid, gas, config, freestream, metrics_fn)
@@ -200,6 +201,7 @@ class GpuContext:
                     self.ctx, cid, native.ints(s.block.dims), s.block.ghost_depth,
                     native.dptrs(nodes), (C.c_longlong * 3)(*st), None))
                 self.timing["blocks_s"].append(time.perf_counter() - t_blk)
+                self._keep_nodes.append(nodes)   # read asynchronously until bf_sync_blocks
                 continue
             fv = []
             for d in range(self.ndim):
@@ -211,6 +213,10 @@ class GpuContext:
             self._check(self.L.bf_add_block(self.ctx, cid, native.ints(s.block.dims),
                                             s.block.ghost_depth, native.dptrs(fv),
                                             native.dptr(vol), src))
+        t_sync = time.perf_counter()
+        self._check(self.L.bf_sync_blocks(self.ctx))   # device metrics done; inverted cells raise
+        self.timing["sync_s"] = time.perf_counter() - t_sync
+        self._keep_nodes = []
         if self.viscous:   # face gradient matrices (solver.py:582-642), host numpy
             geometry, _ = _geometry()
             for cid in self.child_ids:
