@@ -794,30 +794,15 @@ cudaError_t launch_viscous(const ViscArgs& a, int nlaunch, cudaStream_t s) {
 // numpy's NaN semantics, and the reset of the error slot for the next step.
 // The guard of one batched step (red: GUARD_NT x 5 doubles of shared memory;
 // every thread of the CTA calls it).
-BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, double* blocksum,
-                       unsigned long long* err, RunState* rs, double* hist, double* red) {
-  // thread 0 loads the run state and the step's error key up front: their
-  // latency overlaps the sums (one launch-bound chain less on small grids)
-  RunState r;
-  unsigned long long key = ~0ull;
-  if (threadIdx.x == 0) {
-    r = *rs;
-    key = *reinterpret_cast<volatile unsigned long long*>(err);
-  }
-  // per-block sums exactly as reduce_kernel forms them (block_sum); the step's
-  // norms from them in block order (thread 0 reads each block's sums from red[0..4]
-  // before the next block_sum writes its own slots there)
-  double h[5] = {0, 0, 0, 0, 0};
-  for (int b = 0; b < nb; ++b) {
-    block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
-    if (threadIdx.x == 0)
-      for (int v = 0; v < 5; ++v) h[v] = h[v] + red[v];
-  }
-  if (threadIdx.x != 0) return;
+// The history guards of one step from its global Σ R² (h, the five sums) and
+// error state; thread 0 of the calling CTA.  r: the run state loaded up front.
+BF_DEV void guard_tail(double h[5], unsigned long long key, int bad_rank, RunState& r,
+                       RunState* rs, double* hist, unsigned long long* err) {
   const int s = r.steps;
   *err = ~0ull;   // the next step's error slot (the per-step reset of bf_step)
-  if (key != ~0ull && !r.ignore_errors) {   // non-physical state in this step
+  if ((key != ~0ull || bad_rank >= 0) && !r.ignore_errors) {   // non-physical state in this step
     rs->key = key;
+    rs->pad = bad_rank;   // the first rank that recorded one (multi-rank batches)
     rs->status = 3;
     rs->stop = 1;
     return;
@@ -863,6 +848,60 @@ BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, dou
   }
 }
 
+BF_DEV void guard_body(const double* partial, const int* tile_begin, int nb, double* blocksum,
+                       unsigned long long* err, RunState* rs, double* hist, double* red) {
+  // thread 0 loads the run state and the step's error key up front: their
+  // latency overlaps the sums (one launch-bound chain less on small grids)
+  RunState r;
+  unsigned long long key = ~0ull;
+  if (threadIdx.x == 0) {
+    r = *rs;
+    key = *reinterpret_cast<volatile unsigned long long*>(err);
+  }
+  // per-block sums exactly as reduce_kernel forms them (block_sum); the step's
+  // norms from them in block order (thread 0 reads each block's sums from red[0..4]
+  // before the next block_sum writes its own slots there)
+  double h[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b) {
+    block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
+    if (threadIdx.x == 0)
+      for (int v = 0; v < 5; ++v) h[v] = h[v] + red[v];
+  }
+  if (threadIdx.x != 0) return;
+  guard_tail(h, key, -1, r, rs, hist, err);
+}
+
+// Multi-rank batches (bf_iterate over NCCL / loopback ranks): before the
+// rank allgather, this rank's record [Σ over its blocks in id order (as
+// finish_collect sums them), error key bits]; after it, the global sums in
+// rank order (as rank_allgather sums them) and the guards, every rank alike.
+__global__ void rank_record_kernel(const double* blocksum, int nb, const unsigned long long* err,
+                                   double* rec6, const RunState* rs) {
+  pdl_wait();
+  if (rs->stop) return;
+  double s[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b)
+    for (int v = 0; v < 5; ++v) s[v] = s[v] + blocksum[5 * b + v];
+  for (int v = 0; v < 5; ++v) rec6[v] = s[v];
+  rec6[5] = __longlong_as_double((long long)*err);
+}
+
+__global__ void rank_guard_kernel(const double* gather, int nranks, int rank,
+                                  unsigned long long* err, RunState* rs, double* hist) {
+  pdl_wait();
+  if (rs->stop) return;
+  RunState r = *rs;
+  double tot[5];
+  int bad = -1;
+  for (int q = 0; q < nranks; ++q) {
+    for (int v = 0; v < 5; ++v) tot[v] = (q == 0) ? gather[6 * q + v] : tot[v] + gather[6 * q + v];
+    const unsigned long long k = (unsigned long long)__double_as_longlong(gather[6 * q + 5]);
+    if (k != ~0ull && bad < 0) bad = q;
+  }
+  const unsigned long long own = (unsigned long long)__double_as_longlong(gather[6 * rank + 5]);
+  guard_tail(tot, own, bad, r, rs, hist, err);
+}
+
 __global__ void __launch_bounds__(GUARD_NT) guard_kernel(const double* partial,
                                                          const int* tile_begin, int nb,
                                                          double* blocksum,
@@ -879,6 +918,17 @@ cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, d
                          unsigned long long* err, RunState* rs, double* hist, cudaStream_t s) {
   return launch_pdl(guard_kernel, 1u, (unsigned)GUARD_NT, 0, s, partial, tile_begin, nb, blocksum,
                     err, rs, hist);
+}
+
+cudaError_t launch_rank_record(const double* blocksum, int nb, const unsigned long long* err,
+                               double* rec6, const RunState* rs, cudaStream_t s) {
+  return launch_pdl(rank_record_kernel, 1u, 1u, 0, s, blocksum, nb, err, rec6, rs);
+}
+
+cudaError_t launch_rank_guard(const double* gather, int nranks, int rank,
+                              unsigned long long* err, RunState* rs, double* hist,
+                              cudaStream_t s) {
+  return launch_pdl(rank_guard_kernel, 1u, 1u, 0, s, gather, nranks, rank, err, rs, hist);
 }
 
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,

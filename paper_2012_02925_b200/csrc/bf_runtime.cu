@@ -38,6 +38,11 @@ cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblo
                           cudaStream_t s);
 cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
                          unsigned long long* err, RunState* rs, double* hist, cudaStream_t s);
+cudaError_t launch_rank_record(const double* blocksum, int nb, const unsigned long long* err,
+                               double* rec6, const RunState* rs, cudaStream_t s);
+cudaError_t launch_rank_guard(const double* gather, int nranks, int rank,
+                              unsigned long long* err, RunState* rs, double* hist,
+                              cudaStream_t s);
 int stage_tile_rows(int ndim, int lim);
 void set_pdl(int on);
 }  // namespace bf_exact
@@ -473,6 +478,9 @@ struct bf_ctx {
   cudaGraphExec_t gexec_b[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   std::vector<TimerPair> gprof_b[2];
   bool batching = false;
+  // multi-rank batched iterate (NCCL / loopback ranks): per step the rank record,
+  // its allgather and the guards stay on the device (rank_record / rank_guard)
+  bool mr_batching = false;
   bool batch_off = false;          // BF_BATCH=0
   RunState* d_run = nullptr;
   double* d_hist = nullptr;        // [BATCH_MAX][5]
@@ -534,7 +542,9 @@ struct bf_ctx {
   double* d_gather = nullptr;         // [nranks][6]
   double* h_pinned = nullptr;         // blocksum + err staging
   // RunState::stop is its first member
-  const int* stop_flag() const { return batching ? reinterpret_cast<const int*>(d_run) : nullptr; }
+  const int* stop_flag() const {
+    return (batching || mr_batching) ? reinterpret_cast<const int*>(d_run) : nullptr;
+  }
   // state
   int cur = 0;
   int ghost_buf = 0;
@@ -2811,7 +2821,8 @@ void use_pdl(const bf_ctx* ctx) {
 int enqueue_step(bf_ctx* ctx, int step_index) {
   const int nst = ctx->sch.rk_stages;
   use_pdl(ctx);
-  int rc = ctx->batching ? BF_OK : reset_error(ctx);   // batched: the guard kernel resets it
+  // batched: the guard kernel resets it
+  int rc = (ctx->batching || ctx->mr_batching) ? BF_OK : reset_error(ctx);
   if (rc) return rc;
   for (int k = 0; k < nst; ++k) {
     const int flags = stage_flags(ctx, step_index, k, nst);
@@ -2824,6 +2835,15 @@ int enqueue_step(bf_ctx* ctx, int step_index) {
     }
     rc = launch_stage_kernel(ctx, k, flags, rk_alpha(nst, k));
     if (rc) return rc;
+  }
+  if (ctx->mr_batching) {   // rank record -> allgather -> global norms and guards, on the device
+    ProfScope ps(ctx, 3);
+    CK(bf_exact::launch_rank_record(ctx->d_blocksum, (int)ctx->blocks.size(), ctx->d_err,
+                                    ctx->d_rank6, ctx->d_run, ctx->stream));
+    NK(net(ctx).AllGather(ctx->d_rank6, ctx->d_gather, 6, ncclDouble, ctx->comm, ctx->stream));
+    CK(bf_exact::launch_rank_guard(ctx->d_gather, ctx->nranks, ctx->rank, ctx->d_err, ctx->d_run,
+                                   ctx->d_hist, ctx->stream));
+    return BF_OK;
   }
   if (ctx->batching) {   // norms and guards on the device (RunState)
     ProfScope ps(ctx, 3);
@@ -3015,7 +3035,7 @@ constexpr int BATCH_MAX = 256;   // steps per batch (device history rows)
 // (RunState).  Host sequencing state follows the steps the device executed.
 static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_target,
                      double target, int has_floor, double floor_, double factor,
-                     double* hist_out, int* done, int* status) {
+                     double* hist_out, int* done, int* status, bool multi_rank = false) {
   if (!ctx->d_run) {
     void* p = nullptr;
     CK(cudaMalloc(&p, sizeof(RunState)));
@@ -3042,13 +3062,19 @@ static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_
     if (r0) return r0;
   }
   const StepState before = save_state(ctx);
-  ctx->batching = true;
   int rc = BF_OK;
-  for (int q = 0; q < n && rc == BF_OK; ++q) {
-    rc = enqueue_step_graph(ctx, first_step + q);
-    if (rc == 1) rc = fail(ctx, BF_EINVAL, "batched step graph unavailable");
+  if (multi_rank) {   // every rank enqueues the same n steps: the exchanges stay matched
+    ctx->mr_batching = true;
+    for (int q = 0; q < n && rc == BF_OK; ++q) rc = enqueue_step(ctx, first_step + q);
+    ctx->mr_batching = false;
+  } else {
+    ctx->batching = true;
+    for (int q = 0; q < n && rc == BF_OK; ++q) {
+      rc = enqueue_step_graph(ctx, first_step + q);
+      if (rc == 1) rc = fail(ctx, BF_EINVAL, "batched step graph unavailable");
+    }
+    ctx->batching = false;
   }
-  ctx->batching = false;
   if (rc) return rc;
   double* hh = reinterpret_cast<double*>(hr + 1);
   CK(cudaMemcpyAsync(hr, ctx->d_run, sizeof(RunState), cudaMemcpyDeviceToHost, ctx->stream));
@@ -3057,18 +3083,34 @@ static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->profiling) drain_profile(ctx);
   const int ran = hr->steps + (hr->status == 3 ? 1 : 0);   // the failing step ran too
-  StepState st = before;
-  for (int q = 0; q < ran; ++q) st = advanced(st, ctx->sch.rk_stages);
-  load_state(ctx, st);
+  if (!multi_rank || ran < n) {   // host bookkeeping of the steps the device executed
+    const bool filled = multi_rank ? (before.other_filled || ran > 0) : before.other_filled;
+    StepState st = before;
+    for (int q = 0; q < ran; ++q) st = advanced(st, ctx->sch.rk_stages);
+    st.other_filled = filled;
+    load_state(ctx, st);
+  }
   for (int q = 0; q < hr->steps; ++q)
     for (int v = 0; v < 5; ++v) hist_out[5 * (call_step + q) + v] = hh[5 * q + v];
   *done = hr->steps;
   *status = hr->status;
   if (hr->status == 3) {
+    if (hr->key == NO_ERROR)   // another rank's state (bf_step's rank_allgather message)
+      return fail(ctx, BF_ENONPHYSICAL, "rank %d: non-physical state", hr->pad);
     decode_error(ctx, hr->key);
     return BF_ENONPHYSICAL;
   }
   return BF_OK;
+}
+
+// Multi-rank contexts whose steps can run back to back with the norms and
+// guards on the device: the rank record is allgathered on the stream (NCCL or
+// loopback), every rank evaluates the same global guards, so every rank stops
+// after the same step and the remaining launches of the batch are no-ops.
+bool mr_batch_eligible(const bf_ctx* ctx) {
+  return ctx->comm && ctx->nranks > 1 && !ctx->group && !ctx->sch.viscous &&
+         ctx->r1_bc.empty() && ctx->sch.limiter_freeze_at <= 0 &&
+         !(ctx->push_ok && push_enabled());
 }
 
 int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, double target,
@@ -3080,12 +3122,13 @@ int bf_iterate(bf_ctx* ctx, int first_step, int max_steps, int has_target, doubl
   *status = 0;
   int s = 0;
   while (s < max_steps) {
-    if (!ctx->batch_off && graph_eligible(ctx)) {
+    const bool mr = !ctx->batch_off && mr_batch_eligible(ctx);
+    if (!ctx->batch_off && (graph_eligible(ctx) || mr)) {
       // device-side guards: no host round trip per step
       const int n = std::min(max_steps - s, BATCH_MAX);
       int done = 0, st = 0;
       const int rc = run_batch(ctx, first_step + s, n, s, has_target, target, has_floor, floor_,
-                               divergence_factor, hist_out, &done, &st);
+                               divergence_factor, hist_out, &done, &st, mr);
       s += done;
       *steps_done = s;
       if (rc) return rc;

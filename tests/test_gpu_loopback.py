@@ -208,3 +208,33 @@ def test_two_process_nccl_when_two_gpus(tmp_path):
                           "29541", str(script)], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "NCCL2-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_loopback_device_guards_equal_host_loop(monkeypatch, nranks):
+    """Multi-rank bf_iterate batches: the rank record, its allgather and the
+    history guards run on the device (rank_record / rank_guard kernels), every
+    rank stops after the same step.  Against BF_BATCH=0 (host collect, host
+    allgather and host guard per step): the same steps, bitwise the same norms
+    and fields, a target reached mid-batch included."""
+    plan = cases.make_plan(geometry.multiblock_box_3d(3), nranks)
+    sched = planning.reorder_boundaries(plan)
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    st = _stepper()
+    monkeypatch.setenv("BF_BATCH", "0")
+    probe = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=30, init="perturbed",
+                                   precision="fast")
+    target = float(np.max(probe.relative_history()[17]))
+    runs = {}
+    for batch in ("0", "1"):
+        monkeypatch.setenv("BF_BATCH", batch)
+        runs[batch] = st.run_distributed_gpu(plan, sched, GAS, cfg, fs, max_steps=30,
+                                             residual_target=target, init="perturbed",
+                                             precision="fast")
+    a, b = runs["0"], runs["1"]
+    assert a.steps == b.steps and a.converged == b.converged and a.steps < 30
+    np.testing.assert_array_equal(a.history, b.history)
+    for cid in a.fields:
+        for n in a.fields[cid]:
+            np.testing.assert_array_equal(a.fields[cid][n], b.fields[cid][n], err_msg=f"{cid} {n}")
