@@ -193,7 +193,8 @@ struct RunState {
   int has_base;         // base = the call's first-step norms
   unsigned long long key;   // error key of status 3
   double base[5];
-  int has_target, has_floor, ignore_errors, pad;
+  int has_target, has_floor, ignore_errors;
+  int bad_rank;         // status 3 of a multi-rank batch: first rank with a recorded error
   double target, floor_, factor;
 };
 

@@ -802,7 +802,7 @@ BF_DEV void guard_tail(double h[5], unsigned long long key, int bad_rank, RunSta
   *err = ~0ull;   // the next step's error slot (the per-step reset of bf_step)
   if ((key != ~0ull || bad_rank >= 0) && !r.ignore_errors) {   // non-physical state in this step
     rs->key = key;
-    rs->pad = bad_rank;   // the first rank that recorded one (multi-rank batches)
+    rs->bad_rank = bad_rank;   // the first rank that recorded one (multi-rank batches)
     rs->status = 3;
     rs->stop = 1;
     return;

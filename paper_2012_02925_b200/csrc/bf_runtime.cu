@@ -3096,7 +3096,7 @@ static int run_batch(bf_ctx* ctx, int first_step, int n, int call_step, int has_
   *status = hr->status;
   if (hr->status == 3) {
     if (hr->key == NO_ERROR)   // another rank's state (bf_step's rank_allgather message)
-      return fail(ctx, BF_ENONPHYSICAL, "rank %d: non-physical state", hr->pad);
+      return fail(ctx, BF_ENONPHYSICAL, "rank %d: non-physical state", hr->bad_rank);
     decode_error(ctx, hr->key);
     return BF_ENONPHYSICAL;
   }
