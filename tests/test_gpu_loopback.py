@@ -238,3 +238,16 @@ def test_loopback_device_guards_equal_host_loop(monkeypatch, nranks):
     for cid in a.fields:
         for n in a.fields[cid]:
             np.testing.assert_array_equal(a.fields[cid][n], b.fields[cid][n], err_msg=f"{cid} {n}")
+
+
+def test_loopback_odd_block_sizes_tile_halo_classification():
+    """A tile is interior only if its whole 2-cell halo stays off every remote
+    face: with 65 cells along the cut axis the tile at i0 = 32 reads cell 65 —
+    a ghost cell the unpack writes while the interior tiles run (the overlap
+    path).  Bitwise equal to the serial driver (FAST, 3 steps)."""
+    grid = geometry.cartesian_box_3d(130, mms=False)
+    plan = planning.decompose(grid, 2, 3)
+    assert any(65 in c.dims for c in plan.children), [c.dims for c in plan.children]
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    cfg = SchemeConfig(flux="van_leer", limiter="van_albada", cfl=0.8)
+    assert_same_as_serial(plan, cfg, fs, 3, "perturbed", "fast")
