@@ -159,12 +159,19 @@ struct GhostTask {
 // Ghost launches are block-aligned: CUDA block b covers items
 // [block_map[b].y, +GHOST_BLOCK * ipt) of task block_map[b].x (one task per block).
 constexpr int GHOST_BLOCK = 128;
-constexpr int GHOST_ITEMS = 4;                       // items per thread (large launches)
+#ifndef BF_GHOST_ITEMS
+#define BF_GHOST_ITEMS 4
+#endif
+constexpr int GHOST_ITEMS = BF_GHOST_ITEMS;          // max items per thread (unrolled loads)
 constexpr int GHOST_SPAN = GHOST_BLOCK * GHOST_ITEMS;  // items per CUDA block (large launches)
 // Small launches (fewer items than a few full-occupancy waves of GHOST_SPAN
 // blocks, e.g. 2D grids) use one item per thread: more blocks, shorter chains.
 constexpr long long GHOST_SMALL_ITEMS = 148LL * 4 * GHOST_SPAN;
-inline int ghost_ipt(long long total_items) { return total_items >= GHOST_SMALL_ITEMS ? GHOST_ITEMS : 1; }
+// Large launches: 2 items per thread (with the blocks interleaved across tasks, C4
+// fill 0.091-0.095 ms at 4, 0.087 ms at 2; profiles/r02_ghost_ipt.txt).
+inline int ghost_ipt(long long total_items) {
+  return total_items >= GHOST_SMALL_ITEMS ? (GHOST_ITEMS < 2 ? GHOST_ITEMS : 2) : 1;
+}
 
 struct GhostArgs {
   const DevBlock* blocks;

@@ -1127,6 +1127,9 @@ int build_tables(bf_ctx* ctx) {
   };
   ctx->ipt_fill = ghost_ipt(ctx->items_fill);
   ctx->ipt_unpack = ghost_ipt(ctx->items_unpack);
+  if (const char* e = std::getenv("BF_GHOST_IPT")) {   // A/B: items per thread of the fill
+    ctx->ipt_fill = std::max(1, std::min(GHOST_ITEMS, std::atoi(e)));
+  }
   if (int rc = block_map(fill, &ctx->d_map_fill, &ctx->nmap_fill, ctx->ipt_fill)) return rc;
   if (int rc = block_map(unp, &ctx->d_map_unpack, &ctx->nmap_unpack, ctx->ipt_unpack)) return rc;
   if (!fill.empty()) {
