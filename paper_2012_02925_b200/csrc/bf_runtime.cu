@@ -466,6 +466,7 @@ struct bf_ctx {
   int fill_ctas_env = 0;           // BF_FILL_CTAS=n: fill-only CTAs per fused launch
   int num_sms = 148;
   int pdl_mode = -1;               // BF_PDL: 0 off, 1 on, unset: one-wave grids (use_pdl)
+  bool ghost_interleave = true;    // BF_GHOST_INTERLEAVE=0: ghost blocks in task order
   unsigned* d_fill_sync = nullptr; // claim / done / arrived counters
   bool fuse_next = false;          // the next stage launch fills the ghosts of W[cur]
   bool counted = false;           // registered in the per-device live-context count
@@ -1104,11 +1105,7 @@ int build_tables(bf_ctx* ctx) {
     // i-face rows (32-byte sectors half used) and the dense j/k-face rows then
     // share the DRAM at any moment (C4 fill 0.101 -> 0.094 ms); BF_GHOST_INTERLEAVE=0:
     // task order.  Items and their values are unchanged, only the block order.
-    static const bool interleave = [] {
-      const char* e = std::getenv("BF_GHOST_INTERLEAVE");
-      return !(e && e[0] == '0');
-    }();
-    if (interleave) {   // each task's blocks spread evenly over the launch
+    if (ctx->ghost_interleave) {   // each task's blocks spread evenly over the launch
       std::vector<long long> cnt(ts.size(), 0), seen(ts.size(), 0);
       for (const int2& e : m) ++cnt[e.x];
       std::vector<std::pair<double, int2>> key;
@@ -2172,6 +2169,7 @@ bf_ctx* bf_create(int ndim, const bf_gas* gas, const bf_scheme* scheme, const bf
   if (const char* e = std::getenv("BF_FUSED_FILL")) ctx->fused_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = std::getenv("BF_FILL_CTAS")) ctx->fill_ctas_env = std::atoi(e);
   if (const char* e = std::getenv("BF_PDL")) ctx->pdl_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = std::getenv("BF_GHOST_INTERLEAVE")) ctx->ghost_interleave = e[0] != '0';
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own_stream,
                                                                         cudaStreamNonBlocking) !=

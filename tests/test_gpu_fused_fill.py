@@ -98,3 +98,16 @@ def test_fused_fill_replaces_the_ghost_launches(monkeypatch):
         assert n_ghost <= 2, n_ghost
     finally:
         gpu.close()
+
+
+def test_ghost_block_order_does_not_change_values(monkeypatch):
+    """The ghost launch's CUDA blocks are spread over the launch across tasks
+    (and 2 items per thread); the tasks of one launch write disjoint ghost
+    cells, so the order is invisible in the results: bitwise equal to the task
+    order (BF_GHOST_INTERLEAVE=0) with the separate fill launch."""
+    plan, cfg, fs = CASES["c4_l6"]()
+    monkeypatch.setenv("BF_GHOST_INTERLEAVE", "1")
+    a = _run(monkeypatch, False, plan, cfg, fs, 6)
+    monkeypatch.setenv("BF_GHOST_INTERLEAVE", "0")
+    b = _run(monkeypatch, False, plan, cfg, fs, 6)
+    _same(a, b)
