@@ -656,26 +656,44 @@ __global__ void __launch_bounds__(128) viscous_kernel(const ViscArgs a) {
 // whichever kernel runs it.
 constexpr int GUARD_NT = 256;
 BF_DEV void block_sum(const double* partial, int tb, int te, double* red, double* out5) {
+  // strided per-thread sums, a shuffle tree per warp, then warp 0 over the warp
+  // sums (two barriers instead of a shared-memory tree's eight); the block's five
+  // sums end in out5 and red[0..4]
+  constexpr int NW = GUARD_NT / 32;
   const bool on = threadIdx.x < GUARD_NT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double x[5] = {0, 0, 0, 0, 0};
   if (on)
     for (int t = tb + threadIdx.x; t < te; t += GUARD_NT) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) x[v] += __ldcg(partial + (long long)t * 5 + v);
     }
-  if (on) {
 #pragma unroll
-    for (int v = 0; v < 5; ++v) red[threadIdx.x * 5 + v] = x[v];
+  for (int v = 0; v < 5; ++v)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x[v] += __shfl_down_sync(0xffffffffu, x[v], off);
+  if (on && lane == 0) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) red[warp * 5 + v] = x[v];
   }
   __syncthreads();
-  for (int s = GUARD_NT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
+  if (threadIdx.x < 32) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) red[threadIdx.x * 5 + v] += red[(threadIdx.x + s) * 5 + v];
+    for (int v = 0; v < 5; ++v) {
+      double y = lane < NW ? red[lane * 5 + v] : 0.0;
+#pragma unroll
+      for (int off = NW / 2; off > 0; off >>= 1) y += __shfl_down_sync(0xffffffffu, y, off);
+      x[v] = y;
     }
-    __syncthreads();
   }
-  if (threadIdx.x < 5) out5[threadIdx.x] = red[threadIdx.x];
+  __syncthreads();   // every warp's red reads are done before thread 0 overwrites red[0..4]
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      red[v] = x[v];
+      out5[v] = x[v];
+    }
+  }
   __syncthreads();
 }
 
@@ -902,22 +920,46 @@ __global__ void rank_guard_kernel(const double* gather, int nranks, int rank,
   guard_tail(tot, own, bad, r, rs, hist, err);
 }
 
+// One CTA per block forms the block's sums (block_sum); the last CTA to finish
+// (counter, reset by it) sums the blocks in id order and evaluates the guards.
 __global__ void __launch_bounds__(GUARD_NT) guard_kernel(const double* partial,
                                                          const int* tile_begin, int nb,
                                                          double* blocksum,
                                                          unsigned long long* err, RunState* rs,
-                                                         double* hist) {
+                                                         double* hist, unsigned* count) {
   __shared__ double red[GUARD_NT * 5];
+  __shared__ int last;
   pdl_trigger();
   pdl_wait();
   if (rs->stop) return;
-  guard_body(partial, tile_begin, nb, blocksum, err, rs, hist, red);
+  if (nb == 1 || !count) {   // one block (or no counter): the whole guard in this CTA
+    guard_body(partial, tile_begin, nb, blocksum, err, rs, hist, red);
+    return;
+  }
+  const int b = blockIdx.x;
+  block_sum(partial, tile_begin[b], tile_begin[b + 1], red, blocksum + 5 * b);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(count, 1u) == (unsigned)(nb - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  *count = 0u;
+  RunState r = *rs;
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(err);
+  double h[5] = {0, 0, 0, 0, 0};
+  for (int q = 0; q < nb; ++q)
+    for (int v = 0; v < 5; ++v) h[v] = h[v] + __ldcg(blocksum + 5 * q + v);
+  guard_tail(h, key, -1, r, rs, hist, err);
 }
 
 cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
-                         unsigned long long* err, RunState* rs, double* hist, cudaStream_t s) {
-  return launch_pdl(guard_kernel, 1u, (unsigned)GUARD_NT, 0, s, partial, tile_begin, nb, blocksum,
-                    err, rs, hist);
+                         unsigned long long* err, RunState* rs, double* hist, unsigned* count,
+                         cudaStream_t s) {
+  const unsigned grid = (nb > 1 && count) ? (unsigned)nb : 1u;
+  return launch_pdl(guard_kernel, grid, (unsigned)GUARD_NT, 0, s, partial, tile_begin, nb,
+                    blocksum, err, rs, hist, count);
 }
 
 cudaError_t launch_rank_record(const double* blocksum, int nb, const unsigned long long* err,

@@ -37,7 +37,8 @@ cudaError_t launch_ghost(const GhostArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partial, const int* tile_begin, int nblocks, double* out,
                           cudaStream_t s);
 cudaError_t launch_guard(const double* partial, const int* tile_begin, int nb, double* blocksum,
-                         unsigned long long* err, RunState* rs, double* hist, cudaStream_t s);
+                         unsigned long long* err, RunState* rs, double* hist, unsigned* count,
+                         cudaStream_t s);
 cudaError_t launch_rank_record(const double* blocksum, int nb, const unsigned long long* err,
                                double* rec6, const RunState* rs, cudaStream_t s);
 cudaError_t launch_rank_guard(const double* gather, int nranks, int rank,
@@ -467,7 +468,7 @@ struct bf_ctx {
   int num_sms = 148;
   int pdl_mode = -1;               // BF_PDL: 0 off, 1 on, unset: one-wave grids (use_pdl)
   bool ghost_interleave = true;    // BF_GHOST_INTERLEAVE=0: ghost blocks in task order
-  unsigned* d_fill_sync = nullptr; // claim / done / arrived counters
+  unsigned* d_fill_sync = nullptr; // [1] fill warps done, [2] arrivals; [3] guard-kernel CTA counter
   bool fuse_next = false;          // the next stage launch fills the ghosts of W[cur]
   bool counted = false;           // registered in the per-device live-context count
   // one RK step as a CUDA graph (standalone Euler ctx), per starting buffer and
@@ -2867,7 +2868,8 @@ int enqueue_step(bf_ctx* ctx, int step_index) {
   if (ctx->batching) {   // norms and guards on the device (RunState)
     ProfScope ps(ctx, 3);
     CK(bf_exact::launch_guard(ctx->d_partial, ctx->d_tile_begin, (int)ctx->blocks.size(),
-                              ctx->d_blocksum, ctx->d_err, ctx->d_run, ctx->d_hist, ctx->stream));
+                              ctx->d_blocksum, ctx->d_err, ctx->d_run, ctx->d_hist,
+                              ctx->d_fill_sync ? ctx->d_fill_sync + 3 : nullptr, ctx->stream));
     return BF_OK;
   }
   return enqueue_collect(ctx);
