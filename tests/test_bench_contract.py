@@ -73,6 +73,9 @@ def test_native_arm_line():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    # a repeated call (recycled arenas) and the cold first call beside it
+    assert e["cold"]["value"] > 0 and "arenas" in e and "arenas" in e["cold"]
+    assert set(e["phases_s"]) >= {"blocks", "finalize", "upload", "steps", "download"}
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert "workload" in d["config"]

@@ -107,3 +107,29 @@ def test_device_and_host_metrics_runs_identical(precision):
     for cid in a.solvers:
         for n in FIELD_NAMES:
             np.testing.assert_array_equal(a.solvers[cid].fields[n], b.solvers[cid].fields[n])
+
+
+def test_async_registration_reports_the_inverted_block():
+    """bf_add_block_nodes returns before its metric kernels finish (the next
+    block's node copy overlaps them); bf_sync_blocks, called at the end of
+    GpuContext construction, reports the first registered block with an
+    inverted cell — here the second of two children — with the reference text."""
+    from paper_2012_02925_b200 import stepper
+    grid = warped_box_3d(dims=(12, 5, 4))
+    plan = planning.decompose(grid, 2, 3)
+    cid = sorted(c.id for c in plan.children)[1]
+    setups = stepper.host_setups(plan, [c.id for c in plan.children], GAS,
+                                 SchemeConfig(flux="van_leer"),
+                                 cases.freestream_for("multiblock_box_3d", GAS, 3))
+    blk = setups[cid].block
+    g = blk.ghost_depth
+    blk.nodes = blk.nodes.copy()
+    blk.nodes[0, g + 3, g + 2, g + 2] += 5.0
+    with pytest.raises(MetricError) as host_err:
+        geometry.compute_metrics(blk)
+    fs = cases.freestream_for("multiblock_box_3d", GAS, 3)
+    with pytest.raises(MetricError) as dev_err:
+        stepper.GpuContext(plan, [c.id for c in plan.children], GAS, SchemeConfig(flux="van_leer"),
+                           fs, setups=setups)
+    assert str(dev_err.value) == str(host_err.value)
+    assert str(dev_err.value).startswith(f"block {cid}:")
